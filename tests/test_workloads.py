@@ -1,0 +1,57 @@
+"""Generators produce the shapes BASELINE.json's configs describe (CPU only)."""
+import numpy as np
+
+import workloads as W
+
+
+def _lens(w):
+    return w.offsets[1:] - w.offsets[:-1]
+
+
+def test_c1_shape():
+    w = W.make("C1")
+    L = _lens(w)
+    assert w.n == 100_000 and L.min() == 4 and L.max() == 12
+    assert w.units.min() >= ord("a") and w.units.max() <= ord("z")
+    w2 = W.make("C1")
+    assert np.array_equal(w.units, w2.units)  # seeded
+
+
+def test_c2_vocab_and_zipf():
+    words = W.c2_vocab(W.MASTER_SEED + 2, 2000)
+    assert len(set(words)) == 2000 and max(len(x) for x in words) <= 20
+    w = W.c2(200_000, vocab_size=2000)
+    L = _lens(w)
+    assert L.min() >= 1 and L.max() <= 20
+    # the most frequent word has probability 1/H_2000 ~ 12.2%
+    strings = {}
+    for i in range(0, w.n, 50):
+        s = w.units[w.offsets[i]:w.offsets[i + 1]].tobytes()
+        strings[s] = strings.get(s, 0) + 1
+    top = max(strings.values()) / (w.n / 50)
+    assert 0.09 < top < 0.16
+
+
+def test_c3_shape():
+    w = W.c3(50_000)
+    L = _lens(w)
+    assert w.units.dtype == np.uint16 and L.min() == 2 and L.max() == 4
+    assert w.units.min() >= 0x4E00 and w.units.max() <= 0x9FFF
+
+
+def test_c4_shape():
+    w = W.c4(10_000)
+    assert (_lens(w) == 24).all()
+    u = w.units.reshape(-1, 24)
+    assert (u[:, :16] == u[0, :16]).all()
+    assert len(np.unique(u[:, 16:], axis=0)) > 9_900
+
+
+def test_c5_shape():
+    w = W.c5(1 << 16)
+    L = _lens(w)
+    assert L.min() == 8 and L.max() == 24
+    n_sorted = w.meta["sorted"]
+    s = [w.units[w.offsets[i]:w.offsets[i + 1]].tobytes() for i in range(w.n)]
+    assert all(s[i] <= s[i + 1] for i in range(n_sorted - 1))
+    assert w.n - len(set(s)) >= w.meta["dup"] * 0.9
