@@ -1,0 +1,144 @@
+// encode.cu -- A1: husky coding of every string (Alg. 2-4).
+//
+// One thread per string (ENC_ITEMS strings in flight per thread, grid-stride
+// over a persistent grid).  The prefix window (9 ASCII bytes or 4 UTF-16 units)
+// is fetched with at most two aligned 8-byte loads; the 7-bit-per-char packing
+// of asciiToLong is a 3-step mask/shift compaction instead of
+// a 9-step fold, and unicodeToLong's 16-bit packing + ">>> 1"
+// is a half-word swap.  Fused into the same pass (no extra HBM read):
+//   * the 8 x 256 digit histograms the onesweep radix needs (A2),
+//   * Alg. 3's `perfect` flag as an OR of "not perfect",
+//   * the ASCII domain check (unit > 0x7F inside the code window; reading R5),
+//   * the offsets monotonicity check.
+#include "husky_internal.cuh"
+#include "kernels.cuh"
+
+namespace husky {
+
+// asciiToLong on the (already length-masked) first 8 bytes `lo` (byte k at bits
+// 8k..8k+7) and 9th byte `b8`:  code = sum_k (b_k & 0x7F) << 7*(8-k).
+__device__ __forceinline__ uint64_t pack_ascii(uint64_t lo, uint64_t b8) {
+  uint64_t x = ((uint64_t)__byte_perm((uint32_t)(lo >> 32), 0, 0x0123)) |
+               ((uint64_t)__byte_perm((uint32_t)lo, 0, 0x0123) << 32);  // byte-swap: char 0 on top
+  x &= 0x7F7F7F7F7F7F7F7Full;
+  x = (x & 0x007F007F007F007Full) | ((x & 0x7F007F007F007F00ull) >> 1);
+  x = (x & 0x00003FFF00003FFFull) | ((x & 0x3FFF00003FFF0000ull) >> 2);
+  x = (x & 0x000000000FFFFFFFull) | ((x & 0x0FFFFFFF00000000ull) >> 4);
+  return (x << 7) | (b8 & 0x7F);
+}
+
+template <int CODER>
+__device__ __forceinline__ uint64_t encode_one(const void *units, int64_t o0, int64_t len,
+                                               uint32_t &viol) {
+  using T = CoderTraits<CODER>;
+  if (len < 0) { viol |= kOffsetsBad; len = 0; }
+  if (len > T::kPL) viol |= kNotPerfect;
+  if (CODER == HUSKY_CODER_ASCII) {
+    int m = len < 9 ? (int)len : 9;
+    uint64_t lo = 0, b8 = 0;
+    if (m > 0) {
+      uintptr_t a = (uintptr_t)((const uint8_t *)units + o0);
+      const uint64_t *w = (const uint64_t *)(a & ~(uintptr_t)7);
+      int sh = (int)(a & 7);
+      uint64_t w0 = __ldg(w);
+      uint64_t w1 = (sh + m > 8) ? __ldg(w + 1) : 0ull;
+      lo = sh ? ((w0 >> (8 * sh)) | (w1 << (64 - 8 * sh))) : w0;
+      b8 = (m == 9) ? ((w1 >> (8 * sh)) & 0xFF) : 0ull;
+      if (m < 8) lo &= (1ull << (8 * m)) - 1;
+    }
+    if ((lo & 0x8080808080808080ull) | (b8 & 0x80)) viol |= kDomainBad;
+    return pack_ascii(lo, b8);
+  } else {
+    int m = len < 4 ? (int)len : 4;
+    uint64_t lo = 0;
+    if (m > 0) {
+      uintptr_t a = (uintptr_t)((const uint16_t *)units + o0);
+      const uint64_t *w = (const uint64_t *)(a & ~(uintptr_t)7);
+      int sh = (int)(a & 7);
+      uint64_t w0 = __ldg(w);
+      uint64_t w1 = (sh + 2 * m > 8) ? __ldg(w + 1) : 0ull;
+      lo = sh ? ((w0 >> (8 * sh)) | (w1 << (64 - 8 * sh))) : w0;
+      if (m < 4) lo &= (1ull << (16 * m)) - 1;
+    }
+    // units u0..u3 little-endian in lo -> (u0<<48 | u1<<32 | u2<<16 | u3) >> 1
+    uint64_t be = ((uint64_t)__byte_perm((uint32_t)lo, 0, 0x1032) << 32) |
+                  (uint64_t)__byte_perm((uint32_t)(lo >> 32), 0, 0x1032);
+    return be >> 1;
+  }
+}
+
+template <int CODER, bool HIST>
+__global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__ units,
+                                                        const int64_t *__restrict__ offsets, uint64_t n,
+                                                        uint64_t *__restrict__ codes, DevState *st) {
+  __shared__ uint32_t sh_hist[HIST ? 8 * 256 : 1];
+  if (HIST) {
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) sh_hist[i] = 0;
+    __syncthreads();
+  }
+  uint32_t viol = 0;
+  const uint32_t lane = lane_id();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kEncItems;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * kEncItems; base < n; base += stride) {
+    int64_t o0[kEncItems], o1[kEncItems];
+#pragma unroll
+    for (int k = 0; k < kEncItems; ++k) {
+      uint64_t i = base + threadIdx.x + (uint64_t)k * blockDim.x;
+      if (i < n) { o0[k] = __ldg(offsets + i); o1[k] = __ldg(offsets + i + 1); }
+      else { o0[k] = 0; o1[k] = 0; }
+    }
+    uint64_t code[kEncItems];
+#pragma unroll
+    for (int k = 0; k < kEncItems; ++k) code[k] = encode_one<CODER>(units, o0[k], o1[k] - o0[k], viol);
+#pragma unroll
+    for (int k = 0; k < kEncItems; ++k) {
+      uint64_t i = base + threadIdx.x + (uint64_t)k * blockDim.x;
+      bool valid = i < n;
+      if (valid) codes[i] = code[k];
+      if (HIST) {
+        uint32_t vmask = __ballot_sync(0xFFFFFFFFu, valid);
+        if (vmask == 0) continue;
+        int leader = __ffs(vmask) - 1;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          uint32_t dig = (uint32_t)(code[k] >> (8 * d)) & 0xFF;
+          uint32_t ld = __shfl_sync(0xFFFFFFFFu, dig, leader);
+          if (__all_sync(0xFFFFFFFFu, !valid || dig == ld)) {
+            if ((int)lane == leader) atomicAdd(&sh_hist[d * 256 + ld], __popc(vmask));
+          } else if (valid) {
+            atomicAdd(&sh_hist[d * 256 + dig], 1u);
+          }
+        }
+      }
+    }
+  }
+  // reduce violation bits: one atomic per warp that saw any
+  viol = __reduce_or_sync(0xFFFFFFFFu, viol);
+  if (lane == 0 && viol) atomicOr(&st->violations, viol);
+  if (HIST) {
+    __syncthreads();
+    uint32_t *g = &st->hist[0][0];
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
+      if (sh_hist[i]) atomicAdd(g + i, sh_hist[i]);
+  }
+}
+
+void launch_encode(int coder, bool hist, const void *units, const int64_t *offsets, uint64_t n,
+                   uint64_t *codes, DevState *st, int num_sms, cudaStream_t s) {
+  if (n == 0) return;
+  Scope sc_(ST_ENCODE, s, n);
+  uint64_t per_block = (uint64_t)kEncThreads * kEncItems;
+  uint64_t blocks = (n + per_block - 1) / per_block;
+  uint64_t cap = (uint64_t)num_sms * kEncBlocksPerSM;
+  if (blocks > cap) blocks = cap;
+  dim3 g((unsigned)blocks), b(kEncThreads);
+  if (coder == HUSKY_CODER_ASCII) {
+    if (hist) k_encode<HUSKY_CODER_ASCII, true><<<g, b, 0, s>>>(units, offsets, n, codes, st);
+    else k_encode<HUSKY_CODER_ASCII, false><<<g, b, 0, s>>>(units, offsets, n, codes, st);
+  } else {
+    if (hist) k_encode<HUSKY_CODER_UNICODE, true><<<g, b, 0, s>>>(units, offsets, n, codes, st);
+    else k_encode<HUSKY_CODER_UNICODE, false><<<g, b, 0, s>>>(units, offsets, n, codes, st);
+  }
+}
+
+}  // namespace husky

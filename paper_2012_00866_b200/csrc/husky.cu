@@ -1,0 +1,394 @@
+// husky.cu -- host orchestration and the C ABI of libhusky (single GPU).
+//
+// husky_sort = Alg. 1 re-expressed for one B200:
+//   encode (A1, Alg. 2-4)  ->  onesweep LSD radix of (code, index) (A2, Alg. 1
+//   line 3)  ->  run detection + pairwise order check (A3, "we can easily
+//   determine whether our encoding was perfect")  ->  fix-up
+//   of dirty runs (A5, the cleanup of Alg. 1 line 5 restricted to where
+//   inversions can be) with giant-run refinement (A6)  ->  gather (A4).
+// Host<->device synchronisation points: after the histogram scan (trivial-pass
+// mask, input violations), after run classification (giant-run count), once per
+// giant refinement round, and at the end (outcome).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "husky_internal.cuh"
+#include "kernels.cuh"
+#include "host_common.h"
+
+namespace husky {
+
+thread_local std::string g_last_error;
+
+Profiler &profiler() {
+  static Profiler *p = new Profiler;  // never destroyed: events may outlive static teardown
+  return *p;
+}
+
+husky_status fail(husky_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+int device_sm_count() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+Layout make_layout(uint64_t n) {
+  Layout L;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  L.n = n;
+  L.tiles_r = radix_tiles(n);
+  L.tiles_s = scan_tiles(n) > gather_tiles(n) ? scan_tiles(n) : gather_tiles(n);
+  L.cap_sm = n / 2 + 1;
+  L.cap_g = n / (kMediumMax + 1) + 1;
+  L.state = take(sizeof(DevState));
+  L.keysA = take(n * 8);
+  L.keysB = take(n * 8);
+  L.vals = take(n * 4);
+  L.lb_radix = take(L.tiles_r * 256 * 8);
+  L.lb_scan = take(L.tiles_s * 8);
+  L.run_start = take(L.cap_sm * 4);
+  L.run_end = take(L.cap_sm * 4);
+  L.dirty = take(L.cap_sm);
+  L.list_sm = take(L.cap_sm * 8);
+  L.list_g = take(L.cap_g * 8);
+  L.total = off;
+  return L;
+}
+
+struct HostSnap {  // small prefix of DevState read back at sync points
+  uint32_t trivial_mask, violations;
+};
+
+static husky_status cuda_check(const char *where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(HUSKY_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+  return HUSKY_OK;
+}
+
+#define HCHECK(expr)                                                                          \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) return fail(HUSKY_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
+                       uint32_t *d_perm, void *d_sorted_units, int64_t *d_sorted_offsets, void *d_ws,
+                       size_t ws_bytes, husky_outcome *h_out, cudaStream_t s) {
+  if (h_out) memset(h_out, 0, sizeof *h_out);
+  if (coder != HUSKY_CODER_ASCII && coder != HUSKY_CODER_UNICODE)
+    return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  if (n >= 0xFFFFFFFFull) return fail(HUSKY_ERR_INVALID_ARG, "n = %llu >= 2^32 - 1", (unsigned long long)n);
+  if ((d_sorted_units == nullptr) != (d_sorted_offsets == nullptr))
+    return fail(HUSKY_ERR_INVALID_ARG, "d_sorted_units and d_sorted_offsets must both be set or both NULL");
+  if (n == 0) {
+    if (h_out) { h_out->perfect = 1; h_out->domain_ok = 1; }
+    if (d_sorted_offsets) HCHECK(cudaMemsetAsync(d_sorted_offsets, 0, 8, s));
+    HCHECK(cudaStreamSynchronize(s));
+    return HUSKY_OK;
+  }
+  if (!d_units || !d_offsets || !d_perm || !d_ws)
+    return fail(HUSKY_ERR_INVALID_ARG, "null required pointer");
+  if ((uintptr_t)d_ws % 256) return fail(HUSKY_ERR_INVALID_ARG, "workspace not 256-byte aligned");
+  Layout L = make_layout(n);
+  if (ws_bytes < L.total)
+    return fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, L.total);
+
+  Sorter S;
+  S.coder = coder;
+  S.units = d_units;
+  S.offsets = d_offsets;
+  S.n = n;
+  S.perm = d_perm;
+  S.ws = (uint8_t *)d_ws;
+  S.L = L;
+  S.s = s;
+  S.sms = device_sm_count();
+  S.st = S.at<DevState>(L.state);
+  DevState *st = S.st;
+
+  HCHECK(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+  HCHECK(S.reset_lookback());
+
+  // ---- A1 encode (+ digit histograms, flags) and the histogram scan
+  launch_encode(coder, true, d_units, d_offsets, n, S.keysA(), st, S.sms, s);
+  launch_hist_scan(n, st, s);
+  HostSnap snap;
+  HCHECK(cudaMemcpyAsync(&snap, &st->trivial_mask, sizeof snap, cudaMemcpyDeviceToHost, s));
+  HCHECK(cudaStreamSynchronize(s));
+  if (husky_status e = cuda_check("encode")) return e;
+  if (snap.violations & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing");
+  if (coder == HUSKY_CODER_ASCII && (snap.violations & kDomainBad))
+    return fail(HUSKY_ERR_DOMAIN, "ASCII coder: a unit > 0x7F inside a code prefix (Alg. 4 mask is not monotone there)");
+
+  // ---- A2 key sort: (code, index) -> sorted codes, perm
+  uint64_t *sorted_codes = nullptr;
+  if (husky_status e = S.radix(S.keysA(), nullptr, n, snap.trivial_mask, d_perm, S.at<uint32_t>(L.vals),
+                               &sorted_codes))
+    return e;
+
+  // ---- A3 run detection + order check, classification
+  uint32_t *run_start = S.at<uint32_t>(L.run_start), *run_end = S.at<uint32_t>(L.run_end);
+  uint8_t *dirty = S.at<uint8_t>(L.dirty);
+  uint2 *list_sm = S.at<uint2>(L.list_sm), *list_g = S.at<uint2>(L.list_g);
+  HCHECK(cudaMemsetAsync(dirty, 0, L.cap_sm, s));
+  launch_runs_scan(coder, 0, sorted_codes, n, d_perm, d_units, d_offsets, 0, run_start, run_end, dirty, st,
+                   S.lb_scan(), S.next_counter(), S.next_epoch(), s);
+  launch_runs_classify(run_start, run_end, dirty, st, list_sm, L.cap_sm, list_g, true, S.sms, s);
+  uint32_t n_giant = 0;
+  HCHECK(cudaMemcpyAsync(&n_giant, &st->n_giant, 4, cudaMemcpyDeviceToHost, s));
+  HCHECK(cudaStreamSynchronize(s));
+  if (husky_status e = cuda_check("radix/runs")) return e;
+
+  // ---- A6 giant-run refinement (rare: runs > 4096 strings with an inversion)
+  struct Seg { uint32_t start, len, from; };
+  std::vector<Seg> queue;
+  if (n_giant) {
+    std::vector<uint2> g(n_giant);
+    HCHECK(cudaMemcpy(g.data(), list_g, n_giant * sizeof(uint2), cudaMemcpyDeviceToHost));
+    for (auto &x : g) queue.push_back({x.x, x.y, (uint32_t)(coder == HUSKY_CODER_ASCII ? 9 : 3)});
+  }
+  const uint32_t win = coder == HUSKY_CODER_ASCII ? 7 : 3;
+  for (size_t qi = 0; qi < queue.size(); ++qi) {
+    Seg seg = queue[qi];
+    S.refine_rounds++;
+    uint32_t *perm_seg = d_perm + seg.start;
+    // reset histogram + segment scratch
+    HCHECK(cudaMemsetAsync(st->hist, 0, sizeof(st->hist), s));
+    HCHECK(cudaMemsetAsync(&st->trivial_mask, 0, 4, s));
+    HCHECK(cudaMemsetAsync(&st->seg_L, 0xFF, 4, s));
+    HCHECK(cudaMemsetAsync(&st->seg_has_short, 0, 4, s));
+    launch_seg_prep(coder, perm_seg, seg.len, d_units, d_offsets, seg.from, st, s);
+    launch_seg_key2(coder, perm_seg, seg.len, d_units, d_offsets, seg.from, S.keysA(), st, S.sms, s);
+    launch_hist_scan(seg.len, st, s);
+    uint32_t info[2];
+    HCHECK(cudaMemcpyAsync(&snap, &st->trivial_mask, sizeof snap, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaMemcpyAsync(info, &st->seg_L, 8, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaStreamSynchronize(s));
+    uint32_t Lcur = info[1] ? seg.from : info[0];
+    uint64_t *sorted_key2 = nullptr;
+    // payload: the segment's perm entries; sorted back into perm_seg
+    if (husky_status e = S.radix(S.keysA(), perm_seg, seg.len, snap.trivial_mask, perm_seg,
+                                 S.at<uint32_t>(L.vals), &sorted_key2))
+      return e;
+    // sub-runs of equal key with tag == cap are still ambiguous
+    HCHECK(cudaMemsetAsync(dirty, 0, seg.len / 2 + 1, s));
+    HCHECK(cudaMemsetAsync(&st->n_giant, 0, 4, s));
+    launch_runs_scan(coder, 1, sorted_key2, seg.len, perm_seg, d_units, d_offsets, seg.start, run_start,
+                     run_end, dirty, st, S.lb_scan(), S.next_counter(), S.next_epoch(), s);
+    launch_runs_classify(run_start, run_end, dirty, st, list_sm, L.cap_sm, list_g, false, S.sms, s);
+    HCHECK(cudaMemcpyAsync(&n_giant, &st->n_giant, 4, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaStreamSynchronize(s));
+    if (husky_status e = cuda_check("refine")) return e;
+    if (n_giant) {
+      std::vector<uint2> g(n_giant);
+      HCHECK(cudaMemcpy(g.data(), list_g, n_giant * sizeof(uint2), cudaMemcpyDeviceToHost));
+      for (auto &x : g) queue.push_back({x.x, x.y, Lcur + win});
+    }
+  }
+
+  // ---- A5 fix-up of small / medium dirty runs (counts read on device)
+  launch_fix_small(coder, list_sm, st, d_perm, d_units, d_offsets, S.sms, s);
+  launch_fix_medium(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s);
+
+  // ---- A4 gather
+  if (d_sorted_units)
+    launch_gather(coder, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),
+                  S.next_counter(), S.next_epoch(), s);
+
+  DevState hs;
+  HCHECK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, s));
+  HCHECK(cudaStreamSynchronize(s));
+  if (husky_status e = cuda_check("fixup/gather")) return e;
+  if (h_out) {
+    h_out->perfect = !(hs.violations & kNotPerfect);
+    h_out->domain_ok = !(hs.violations & kDomainBad) || coder != HUSKY_CODER_ASCII;
+    h_out->n_in_runs = hs.n_in_runs;
+    h_out->max_run = hs.max_run;
+    for (int c = 0; c < 4; ++c) h_out->runs_by_class[c] = hs.runs_by_class[c];
+    h_out->n_runs = hs.runs_total;
+    h_out->refine_rounds = S.refine_rounds;
+    h_out->radix_passes = S.radix_passes;
+  }
+  return HUSKY_OK;
+}
+
+}  // namespace husky
+
+using namespace husky;
+
+namespace husky {
+__device__ DevState g_encode_state;
+}
+
+extern "C" {
+
+static const char *kStageNames[ST_COUNT] = {"encode", "hist_scan", "radix_pass", "runs_scan", "runs_classify",
+                                            "fix_small", "fix_medium", "refine", "gather", "multi"};
+
+void husky_profile_enable(int on) {
+  Profiler &P = profiler();
+  P.flush();
+  std::lock_guard<std::mutex> g(P.mu);
+  P.on = on != 0;
+}
+
+void husky_profile_reset(void) {
+  Profiler &P = profiler();
+  P.flush();
+  std::lock_guard<std::mutex> g(P.mu);
+  for (int i = 0; i < ST_COUNT; ++i) { P.ms[i] = 0; P.launches[i] = 0; P.elems[i] = 0; }
+}
+
+int husky_profile_read(double *ms, uint64_t *launches, uint64_t *elems, int max_stages) {
+  Profiler &P = profiler();
+  P.flush();
+  std::lock_guard<std::mutex> g(P.mu);
+  int k = max_stages < ST_COUNT ? max_stages : ST_COUNT;
+  for (int i = 0; i < k; ++i) {
+    if (ms) ms[i] = P.ms[i];
+    if (launches) launches[i] = P.launches[i];
+    if (elems) elems[i] = P.elems[i];
+  }
+  return ST_COUNT;
+}
+
+const char *husky_profile_stage_name(int stage) {
+  return stage >= 0 && stage < ST_COUNT ? kStageNames[stage] : "";
+}
+
+uint64_t husky_launch_count(void) {
+  Profiler &P = profiler();
+  std::lock_guard<std::mutex> g(P.mu);
+  return P.total_launches;
+}
+
+size_t husky_unit_bytes(int coder) {
+  return coder == HUSKY_CODER_ASCII ? 1 : coder == HUSKY_CODER_UNICODE ? 2 : 0;
+}
+
+const char *husky_last_error(void) { return g_last_error.c_str(); }
+
+husky_status husky_encode(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
+                          uint64_t *d_codes, int32_t *h_perfect, void *stream) {
+  if (coder != HUSKY_CODER_ASCII && coder != HUSKY_CODER_UNICODE)
+    return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) {
+    if (h_perfect) *h_perfect = 1;
+    return HUSKY_OK;
+  }
+  if (!d_units || !d_offsets || !d_codes) return fail(HUSKY_ERR_INVALID_ARG, "null required pointer");
+  // flags live in a module-scope device word: concurrent husky_encode calls
+  // that request h_perfect on the same device must not overlap (documented).
+  DevState *st = nullptr;
+  HCHECK(cudaGetSymbolAddress((void **)&st, g_encode_state));
+  uint32_t *viol = &st->violations;
+  HCHECK(cudaMemsetAsync(viol, 0, 4, s));
+  launch_encode(coder, false, d_units, d_offsets, n, d_codes, st, device_sm_count(), s);
+  if (husky_status e = cuda_check("encode")) return e;
+  if (h_perfect) {
+    uint32_t v = 0;
+    HCHECK(cudaMemcpyAsync(&v, viol, 4, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaStreamSynchronize(s));
+    if (v & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing");
+    *h_perfect = !(v & kNotPerfect);
+  }
+  return HUSKY_OK;
+}
+
+husky_status husky_sort_workspace(int coder, uint64_t n, uint64_t total_units, size_t *bytes) {
+  (void)total_units;
+  if (coder != HUSKY_CODER_ASCII && coder != HUSKY_CODER_UNICODE)
+    return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  if (!bytes) return fail(HUSKY_ERR_INVALID_ARG, "bytes is NULL");
+  *bytes = make_layout(n).total;
+  return HUSKY_OK;
+}
+
+husky_status husky_sort(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
+                        uint32_t *d_perm, void *d_sorted_units, int64_t *d_sorted_offsets, void *d_ws,
+                        size_t ws_bytes, husky_outcome *h_out, void *stream) {
+  return sort_impl(coder, d_units, d_offsets, n, d_perm, d_sorted_units, d_sorted_offsets, d_ws, ws_bytes,
+                   h_out, (cudaStream_t)stream);
+}
+
+// host-buffer variant: [device units | device offsets | device perm | sorted units | sorted offsets | sort ws]
+static size_t host_layout(int coder, uint64_t n, uint64_t total_units, size_t *o_units, size_t *o_off,
+                          size_t *o_perm, size_t *o_su, size_t *o_so, size_t *o_ws) {
+  size_t w = husky_unit_bytes(coder), off = 0;
+  auto take = [&](size_t b) { size_t o = off; off = align_up(off + b, 256); return o; };
+  *o_units = take(total_units * w + 16);
+  *o_off = take((n + 1) * 8);
+  *o_perm = take(n * 4 + 4);
+  *o_su = take(total_units * w + 16);
+  *o_so = take((n + 1) * 8);
+  *o_ws = take(make_layout(n).total);
+  return off;
+}
+
+husky_status husky_sort_host_workspace(int coder, uint64_t n, uint64_t total_units, size_t *bytes) {
+  if (coder != HUSKY_CODER_ASCII && coder != HUSKY_CODER_UNICODE)
+    return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  if (!bytes) return fail(HUSKY_ERR_INVALID_ARG, "bytes is NULL");
+  size_t a, b, c, d, e, f;
+  *bytes = host_layout(coder, n, total_units, &a, &b, &c, &d, &e, &f);
+  return HUSKY_OK;
+}
+
+husky_status husky_sort_host(int coder, const void *h_units, const int64_t *h_offsets, uint64_t n,
+                             uint32_t *h_perm, void *h_sorted_units, int64_t *h_sorted_offsets,
+                             void *d_ws, size_t ws_bytes, husky_outcome *h_out, void *stream) {
+  if (coder != HUSKY_CODER_ASCII && coder != HUSKY_CODER_UNICODE)
+    return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  if (!h_offsets || (n && (!h_perm || !h_units)) || !d_ws)
+    return fail(HUSKY_ERR_INVALID_ARG, "null required pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t total = n ? (uint64_t)(h_offsets[n] - h_offsets[0]) : 0;
+  if (n && h_offsets[n] < h_offsets[0]) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing");
+  size_t o_units, o_off, o_perm, o_su, o_so, o_ws;
+  size_t need = host_layout(coder, n, total, &o_units, &o_off, &o_perm, &o_su, &o_so, &o_ws);
+  if (ws_bytes < need) return fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, need);
+  uint8_t *ws = (uint8_t *)d_ws;
+  size_t w = husky_unit_bytes(coder);
+  // the device offsets are rebased to 0 so the device unit copy starts at unit 0
+  int64_t base = n ? h_offsets[0] : 0;
+  HCHECK(cudaMemcpyAsync(ws + o_units, (const uint8_t *)h_units + base * w, total * w, cudaMemcpyHostToDevice, s));
+  HCHECK(cudaMemcpyAsync(ws + o_off, h_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
+  const void *du = ws + o_units;
+  if (base != 0) du = (const uint8_t *)du - base * (int64_t)w;  // offsets index the original buffer
+  bool want_units = h_sorted_units != nullptr && h_sorted_offsets != nullptr;
+  husky_status st = sort_impl(coder, du, (const int64_t *)(ws + o_off), n, (uint32_t *)(ws + o_perm),
+                              want_units ? (void *)(ws + o_su) : nullptr,
+                              want_units ? (int64_t *)(ws + o_so) : nullptr, ws + o_ws, ws_bytes - o_ws,
+                              h_out, s);
+  if (st != HUSKY_OK) return st;
+  HCHECK(cudaMemcpyAsync(h_perm, ws + o_perm, n * 4, cudaMemcpyDeviceToHost, s));
+  if (want_units) {
+    HCHECK(cudaMemcpyAsync(h_sorted_units, ws + o_su, total * w, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaMemcpyAsync(h_sorted_offsets, ws + o_so, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  }
+  HCHECK(cudaStreamSynchronize(s));
+  return HUSKY_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+// husky_internal.cuh -- shared device helpers and the workspace-resident state
+// of libhusky (sm_100a only).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/husky.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libhusky is written for sm_100a (B200) only"
+#endif
+
+namespace husky {
+
+// ---------------------------------------------------------------- constants
+// Code windows: ASCII 9 units x 7 bits, UNICODE 4 x 16 bits.
+// S  = number of leading units fully determined by equal codes (R6):
+//      ASCII 9; UNICODE 3 (unit 3 loses its low bit to ">>> 1").
+// PL = perfect length (reading R4): ASCII 9, UNICODE 3.
+template <int CODER> struct CoderTraits;
+template <> struct CoderTraits<HUSKY_CODER_ASCII> {
+  using unit_t = uint8_t;
+  static constexpr int kUnitBytes = 1, kS = 9, kPL = 9;
+  static constexpr int kWin = 7;    // refinement window: 7 units x 8 bits
+  static constexpr int kTagCap = 8; // tag value meaning "continues past the window"
+};
+template <> struct CoderTraits<HUSKY_CODER_UNICODE> {
+  using unit_t = uint16_t;
+  static constexpr int kUnitBytes = 2, kS = 3, kPL = 3;
+  static constexpr int kWin = 3;    // 3 units x 16 bits
+  static constexpr int kTagCap = 4;
+};
+
+constexpr int kSmallMax = 32;    // dirty runs up to this many strings: one warp
+constexpr int kMediumMax = 4096; // ... up to this many: one CTA (bitonic in smem)
+
+// violation bits (OR-reduced; zero-initialised state)
+constexpr uint32_t kNotPerfect = 1u, kDomainBad = 2u, kOffsetsBad = 4u;
+
+// ------------------------------------------------------ device-resident state
+// Lives at the start of the caller's workspace; zeroed once per husky_sort.
+struct DevState {
+  uint32_t hist[8][256];      // digit histograms of the 64-bit keys (A1 / A6 re-key)
+  uint32_t digit_start[8][256];
+  uint32_t trivial_mask;      // bit d: all keys share digit d
+  uint32_t violations;        // kNotPerfect | kDomainBad | kOffsetsBad
+  uint32_t tile_counter[64];  // dynamic tile ids, one per launch slot
+  uint32_t n_runs;            // runs (>= 2 equal keys) found by the last run scan
+  uint32_t n_small, n_medium, n_giant; // dirty-run list fill counts
+  unsigned long long n_in_runs, max_run;
+  unsigned long long runs_by_class[4];
+  uint32_t seg_L;             // refinement: common-prefix length of the segment
+  uint32_t seg_has_short;     // refinement: segment contains a string with len <= PL
+  unsigned long long runs_total; // runs found by the main (code) scan
+  uint32_t pad[28];
+};
+
+// ----------------------------------------------------------- small helpers
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Decoupled look-back flag word: [63:62] status (1 = aggregate, 2 = inclusive),
+// [61:54] epoch (1..255), [53:0] value.
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 54) - 1;
+__device__ __forceinline__ unsigned long long make_flag(unsigned long long status, uint32_t epoch,
+                                                        unsigned long long v) {
+  return status | ((unsigned long long)epoch << 54) | (v & kValMask);
+}
+// Walks predecessors of `tile` at stride `stride` (flags[t*stride]) until an
+// inclusive prefix is found; returns the exclusive prefix for `tile`.
+__device__ __forceinline__ unsigned long long lookback(const unsigned long long *flags, uint32_t tile,
+                                                       uint32_t stride, uint32_t epoch) {
+  unsigned long long excl = 0;
+  int64_t j = (int64_t)tile - 1;
+  while (j >= 0) {
+    unsigned long long w = ld_relaxed_u64(flags + (uint64_t)j * stride);
+    uint32_t ep = (uint32_t)(w >> 54) & 0xFF;
+    unsigned long long st = w & (3ull << 62);
+    if (ep != epoch || st == 0) continue;  // not yet published in this epoch
+    excl += w & kValMask;
+    if (st == kFlagInc) break;
+    --j;
+  }
+  return excl;
+}
+
+// Warp inclusive scan (Kogge-Stone over shuffles).
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T t = __shfl_up_sync(0xFFFFFFFFu, v, o);
+    if (lane >= (uint32_t)o) v += t;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan for blockDim.x == THREADS.  `warp_tot` is smem of
+// THREADS/32 elements.  Returns the exclusive prefix; *total = block sum.
+// Contains __syncthreads (all threads must call).
+template <typename T, int THREADS>
+__device__ __forceinline__ T block_exclusive_scan(T v, T *total, T *warp_tot) {
+  constexpr int NW = THREADS / 32;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  T inc = warp_inclusive_scan(v);
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T x = lane < NW ? warp_tot[lane] : T(0);
+    T xi = warp_inclusive_scan(x);
+    if (lane < NW) warp_tot[lane] = xi - x;  // exclusive per warp
+    if (lane == NW - 1) warp_tot[NW] = xi;   // block total (warp_tot has NW+1 slots)
+  }
+  __syncthreads();
+  T r = warp_tot[warp] + inc - v;
+  *total = warp_tot[NW];
+  return r;
+}
+
+// Unaligned little-endian load of 8 bytes at byte address p, reading only the
+// aligned 8-byte words that contain bytes [p, p + need) (need in 1..8), so it
+// never touches a word without a needed byte.
+__device__ __forceinline__ uint64_t load8_unaligned(const uint8_t *p, int need) {
+  uintptr_t a = (uintptr_t)p;
+  const uint64_t *w = (const uint64_t *)(a & ~(uintptr_t)7);
+  int sh = (int)(a & 7);
+  uint64_t lo = __ldg(w);
+  if (sh == 0) return lo;
+  uint64_t v = lo >> (8 * sh);
+  if (sh + need > 8) v |= __ldg(w + 1) << (64 - 8 * sh);
+  return v;
+}
+
+// Compare two unit strings a[0..la), b[0..lb) lexicographically (unsigned units),
+// starting at unit `from` (units before it are known equal).  Returns <0, 0, >0
+// where 0 means equal content AND equal length.
+template <int CODER>
+__device__ __forceinline__ int cmp_units_from(const void *units, int64_t oa, int64_t la, int64_t ob,
+                                              int64_t lb, int64_t from) {
+  constexpr int W = CoderTraits<CODER>::kUnitBytes;
+  int64_t m = (la < lb ? la : lb);
+  const uint8_t *base = (const uint8_t *)units;
+  for (int64_t k = from; k < m;) {
+    int64_t rem_units = m - k;
+    int take = (int)(rem_units * W < 8 ? rem_units * W : 8);  // bytes
+    uint64_t x = load8_unaligned(base + (oa + k) * W, take);
+    uint64_t y = load8_unaligned(base + (ob + k) * W, take);
+    if (take < 8) {
+      uint64_t msk = (1ull << (8 * take)) - 1;
+      x &= msk;
+      y &= msk;
+    }
+    uint64_t d = x ^ y;
+    if (d) {
+      int bit = __ffsll((long long)d) - 1;
+      int sh = (bit / (8 * W)) * (8 * W);
+      uint64_t um = W == 1 ? 0xFFull : 0xFFFFull;
+      uint64_t ux = (x >> sh) & um, uy = (y >> sh) & um;
+      return ux < uy ? -1 : 1;
+    }
+    k += take / W;
+  }
+  if (la != lb) return la < lb ? -1 : 1;
+  return 0;
+}
+
+// Exact comparator for two strings whose husky codes are EQUAL (R6):
+// if either length <= PL the shorter one is a prefix of the longer (order by
+// length, then index); otherwise units [0, S) are equal and the comparison
+// starts at unit `from` (>= S when the caller knows a longer common prefix).
+template <int CODER>
+__device__ __forceinline__ int cmp_equal_code(const void *units, const int64_t *offsets, uint32_t ia,
+                                              uint32_t ib, int64_t from) {
+  using T = CoderTraits<CODER>;
+  int64_t oa = offsets[ia], la = offsets[ia + 1] - oa;
+  int64_t ob = offsets[ib], lb = offsets[ib + 1] - ob;
+  int c;
+  if (la <= T::kPL || lb <= T::kPL) c = (la < lb) ? -1 : (la > lb ? 1 : 0);
+  else c = cmp_units_from<CODER>(units, oa, la, ob, lb, from);
+  if (c) return c;
+  return ia < ib ? -1 : (ia > ib ? 1 : 0);
+}
+
+}  // namespace husky

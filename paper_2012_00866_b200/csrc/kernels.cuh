@@ -1,0 +1,61 @@
+// kernels.cuh -- launch wrappers shared between the kernel files and the host
+// orchestration (husky.cu).  Not part of the ABI.
+#pragma once
+#include "husky_internal.cuh"
+#include "profile.h"
+
+namespace husky {
+
+// A1 encode
+constexpr int kEncThreads = 512, kEncItems = 4, kEncBlocksPerSM = 2;
+void launch_encode(int coder, bool hist, const void *units, const int64_t *offsets, uint64_t n,
+                   uint64_t *codes, DevState *st, int num_sms, cudaStream_t s);
+
+// A2 onesweep radix
+constexpr int kRadixThreads = 256, kRadixItems = 16, kRadixTile = kRadixThreads * kRadixItems;
+inline uint64_t radix_tiles(uint64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
+void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s);
+// One stable LSD pass on digit `digit` (bits 8*digit..8*digit+7).  vals_in == NULL
+// synthesises payload = index.  lb: radix_tiles(n)*256 look-back words.
+void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,
+                     uint32_t *vals_out, uint64_t n, int digit, DevState *st,
+                     unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
+void launch_iota(uint32_t *perm, uint64_t n, cudaStream_t s);
+
+// A3 run detection (single-pass scan with decoupled look-back)
+constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+inline uint64_t scan_tiles(uint64_t n) { return (n + kScanTile - 1) / kScanTile; }
+// mode 0: keys are husky codes; a pair inside a run is checked with the exact
+//         equal-code comparator (strings via perm -> offsets -> units).
+// mode 1: keys are refinement keys; a pair is unresolved iff its tag is the cap.
+void launch_runs_scan(int coder, int mode, const uint64_t *keys, uint64_t n, const uint32_t *perm,
+                      const void *units, const int64_t *offsets, uint32_t base, uint32_t *run_start,
+                      uint32_t *run_end, uint8_t *dirty, DevState *st, unsigned long long *lb,
+                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
+void launch_runs_classify(const uint32_t *run_start, const uint32_t *run_end, const uint8_t *dirty,
+                          DevState *st, uint2 *list_sm, uint64_t cap_sm, uint2 *list_g,
+                          bool count_stats, int num_sms, cudaStream_t s);
+
+// A5 fix-up of dirty runs (lists filled by classify; counts read on device)
+void launch_fix_small(int coder, const uint2 *list_sm, const DevState *st, uint32_t *perm,
+                      const void *units, const int64_t *offsets, int num_sms, cudaStream_t s);
+void launch_fix_medium(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
+                       uint32_t *perm, const void *units, const int64_t *offsets, int num_sms,
+                       cudaStream_t s);
+
+// A6 giant-run refinement
+void launch_seg_prep(int coder, const uint32_t *perm_seg, uint64_t len, const void *units,
+                     const int64_t *offsets, uint32_t from, DevState *st, cudaStream_t s);
+void launch_seg_key2(int coder, const uint32_t *perm_seg, uint64_t len, const void *units,
+                     const int64_t *offsets, uint32_t from, uint64_t *key2, DevState *st,
+                     int num_sms, cudaStream_t s);
+
+// A4 gather
+constexpr int kGatherThreads = 256, kGatherItems = 4, kGatherTile = kGatherThreads * kGatherItems;
+constexpr int kGatherStage = 32 * 1024;
+inline uint64_t gather_tiles(uint64_t n) { return (n + kGatherTile - 1) / kGatherTile; }
+void launch_gather(int coder, const uint32_t *perm, uint64_t n, const void *units,
+                   const int64_t *offsets, void *sorted_units, int64_t *sorted_offsets,
+                   unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
+
+}  // namespace husky

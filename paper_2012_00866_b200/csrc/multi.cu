@@ -1,0 +1,696 @@
+// multi.cu -- E: the hot path sharded as a sample sort over P GPUs (one process
+// per GPU, NCCL over NVLink 5 / NVSwitch), plus a single-GPU "loopback" driver
+// that runs P virtual ranks through the very same phases with device-to-device
+// copies as the transport (used to test the sharded path on one GPU).
+//
+// Not in the paper (single-threaded Java); the design follows
+// from the husky-code contract: buckets are ranges of CODES,
+// so a run of equal codes never straddles two GPUs and every rank can resolve
+// its runs locally.  Phases:
+//   1. encode the local strings (A1) and take s regular samples of the codes;
+//      all-gather the P*s samples (+ each rank's input-violation word);
+//   2. every rank picks the same P-1 splitters (husky_select_splitters);
+//      bucket(code) = #splitters <= code; per-destination string/unit counts;
+//      all-to-all of the counts (grouped send/recv);
+//   3. stable partition by bucket = one onesweep pass on the bucket digit, then
+//      the A4 gather builds the send buffers (units, lengths, global indices);
+//      grouped ncclSend/ncclRecv of the three arrays;
+//   4. lengths -> offsets scan, the single-GPU husky_sort on the received bucket
+//      (received order = ascending global index, so the index tie-break holds),
+//      perm remapped to global indices.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "host_common.h"
+
+namespace husky {
+
+constexpr int kSamplesPerRank = 4096;
+constexpr int kMaxWorld = 256;  // bucket ids must fit one radix digit
+constexpr int kSampleStride = kSamplesPerRank + 1;  // + the rank's violation word
+
+#define HCHECK(expr)                                                                               \
+  do {                                                                                             \
+    cudaError_t e_ = (expr);                                                                       \
+    if (e_ != cudaSuccess) return fail(HUSKY_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_));   \
+  } while (0)
+#define NCHECK(expr)                                                                               \
+  do {                                                                                             \
+    ncclResult_t r_ = (expr);                                                                      \
+    if (r_ != ncclSuccess) return fail(HUSKY_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r_));   \
+  } while (0)
+
+// ------------------------------------------------------------------ kernels
+__global__ void k_sample(const uint64_t *__restrict__ codes, uint64_t n, uint64_t *__restrict__ out,
+                         const DevState *st) {
+  for (int i = threadIdx.x; i < kSamplesPerRank; i += blockDim.x)
+    out[i] = n ? codes[(uint64_t)i * n / kSamplesPerRank] : ~0ull;  // ~0: "no sample" (codes < 2^63)
+  if (threadIdx.x == 0) out[kSamplesPerRank] = st->violations;
+}
+
+__global__ void __launch_bounds__(256)
+    k_bucket(const uint64_t *__restrict__ codes, uint64_t n, const uint64_t *__restrict__ splitters,
+             int nsplit, int world, const int64_t *__restrict__ offsets, uint64_t *__restrict__ keys,
+             DevState *st, unsigned long long *counts) {
+  __shared__ uint64_t s_split[kMaxWorld];
+  __shared__ unsigned long long s_cnt[kMaxWorld], s_units[kMaxWorld];
+  for (int i = threadIdx.x; i < kMaxWorld; i += blockDim.x) {
+    s_split[i] = i < nsplit ? splitters[i] : ~0ull;
+    s_cnt[i] = 0;
+    s_units[i] = 0;
+  }
+  __syncthreads();
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = codes[i];
+    int lo = 0, hi = nsplit;  // number of splitters <= c
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (s_split[mid] <= c) lo = mid + 1;
+      else hi = mid;
+    }
+    keys[i] = (uint64_t)lo;
+    atomicAdd(&s_cnt[lo], 1ull);
+    atomicAdd(&s_units[lo], (unsigned long long)(offsets[i + 1] - offsets[i]));
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < world; b += blockDim.x) {
+    if (s_cnt[b]) {
+      atomicAdd(&counts[2 * b], s_cnt[b]);
+      atomicAdd(&counts[2 * b + 1], s_units[b]);
+      atomicAdd(&st->hist[0][b], (uint32_t)s_cnt[b]);
+    }
+  }
+}
+
+__global__ void k_send_meta(const uint32_t *__restrict__ send_perm, uint64_t n, const int64_t *__restrict__ offsets,
+                            uint32_t gbase, uint32_t *__restrict__ gidx, uint32_t *__restrict__ lens) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t p = send_perm[j];
+    gidx[j] = gbase + p;
+    lens[j] = (uint32_t)(offsets[p + 1] - offsets[p]);
+  }
+}
+
+// exclusive scan of u32 lengths -> int64 offsets[n+1] (single pass, look-back)
+__global__ void __launch_bounds__(kScanThreads)
+    k_lens_to_offsets(const uint32_t *__restrict__ lens, uint64_t n, int64_t *__restrict__ offsets,
+                      unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, int64_t add) {
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_wt[kScanThreads / 32 + 1];
+  __shared__ unsigned long long s_base;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t p0 = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  unsigned long long v[kScanItems], sum = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    v[j] = p0 + j < n ? lens[p0 + j] : 0;
+    sum += v[j];
+  }
+  unsigned long long tot;
+  unsigned long long ex = block_exclusive_scan<unsigned long long, kScanThreads>(sum, &tot, s_wt);
+  if (threadIdx.x == 0) {
+    unsigned long long *f = lb + tile, b;
+    if (tile == 0) {
+      b = 0;
+      st_relaxed_u64(f, make_flag(kFlagInc, epoch, tot));
+    } else {
+      st_relaxed_u64(f, make_flag(kFlagAgg, epoch, tot));
+      b = lookback(lb, tile, 1, epoch);
+      st_relaxed_u64(f, make_flag(kFlagInc, epoch, b + tot));
+    }
+    s_base = b;
+    if ((uint64_t)(tile + 1) * kScanTile >= n) offsets[n] = (int64_t)(b + tot) + add;
+  }
+  __syncthreads();
+  unsigned long long d = s_base + ex;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    if (p0 + j < n) offsets[p0 + j] = (int64_t)d + add;
+    d += v[j];
+  }
+}
+
+__global__ void k_remap(uint32_t *perm, uint64_t n, const uint32_t *__restrict__ gidx) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    perm[i] = gidx[perm[i]];
+}
+
+__global__ void k_add_base(int64_t *o, uint64_t n, int64_t add) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    o[i] += add;
+}
+
+static unsigned grid_for(uint64_t n) {
+  uint64_t b = (n + 255) / 256;
+  return (unsigned)(b < 1 ? 1 : (b > 4096 ? 4096 : b));
+}
+
+// ------------------------------------------------------------------ host side
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Comm {
+  ncclComm_t nccl = nullptr;
+  int rank = 0, world = 1;
+};
+
+struct MultiLayout {
+  Layout L;  // state, keysA (= codes), keysB, vals, lb_radix, lb_scan used by the Sorter
+  size_t send_perm = 0, samples = 0, splitters = 0, counts = 0, rcounts = 0, send_units = 0,
+         send_offsets = 0, send_gidx = 0, send_lens = 0, total = 0;
+};
+
+static MultiLayout make_multi_layout(int coder, uint64_t n, uint64_t units, int world) {
+  MultiLayout M;
+  size_t off = 0;
+  auto take = [&](size_t b) { size_t o = off; off = align_up(off + b, 256); return o; };
+  size_t w = coder == HUSKY_CODER_ASCII ? 1 : 2;
+  Layout &L = M.L;
+  L.n = n;
+  L.tiles_r = radix_tiles(n);
+  L.tiles_s = std::max(scan_tiles(n), gather_tiles(n));
+  L.state = take(sizeof(DevState));
+  L.keysA = take(n * 8 + 8);
+  L.keysB = take(n * 8 + 8);
+  L.vals = take(n * 4 + 4);
+  L.lb_radix = take(L.tiles_r * 256 * 8 + 8);
+  L.lb_scan = take(L.tiles_s * 8 + 8);
+  M.send_perm = take(n * 4 + 4);
+  M.samples = take((size_t)world * kSampleStride * 8);
+  M.splitters = take((size_t)world * 8);
+  M.counts = take((size_t)world * 16);
+  M.rcounts = take((size_t)world * 16);
+  M.send_units = take(units * w + 16);
+  M.send_offsets = take((n + 1) * 8);
+  M.send_gidx = take(n * 4 + 4);
+  M.send_lens = take(n * 4 + 4);
+  M.total = off;
+  L.total = off;
+  return M;
+}
+
+struct RecvLayout {
+  size_t units = 0, offsets = 0, lens = 0, gidx = 0, lb = 0, sort_ws = 0, total = 0;
+};
+static RecvLayout make_recv_layout(int coder, uint64_t n_out, uint64_t units_out) {
+  RecvLayout R;
+  size_t off = 0;
+  auto take = [&](size_t b) { size_t o = off; off = align_up(off + b, 256); return o; };
+  size_t w = coder == HUSKY_CODER_ASCII ? 1 : 2;
+  R.units = take(units_out * w + 16);
+  R.offsets = take((n_out + 1) * 8);
+  R.lens = take(n_out * 4 + 4);
+  R.gidx = take(n_out * 4 + 4);
+  R.lb = take(scan_tiles(n_out) * 8 + 8);
+  R.sort_ws = take(make_layout(n_out).total);
+  R.total = off;
+  return R;
+}
+
+// One rank's state across the phases (a plan).
+struct Plan {
+  Comm *comm = nullptr;  // null in loopback mode
+  int coder = 0, rank = 0, world = 1;
+  const void *units = nullptr;
+  const int64_t *offsets = nullptr;
+  uint64_t n = 0, gbase = 0, local_units = 0;
+  uint8_t *ws = nullptr;
+  MultiLayout M;
+  cudaStream_t s = nullptr;
+  Sorter S;
+  std::vector<uint64_t> send_cnt, send_u, recv_cnt, recv_u;  // per peer
+  uint64_t n_out = 0, units_out = 0;
+  std::vector<uint64_t> splitters;
+
+  template <typename T> T *at(size_t o) const { return reinterpret_cast<T *>(ws + o); }
+  DevState *st() const { return at<DevState>(M.L.state); }
+  size_t w() const { return coder == HUSKY_CODER_ASCII ? 1 : 2; }
+
+  void init_sorter() {
+    S.coder = coder;
+    S.units = units;
+    S.offsets = offsets;
+    S.n = n;
+    S.ws = ws;
+    S.L = M.L;
+    S.s = s;
+    S.sms = device_sm_count();
+    S.st = st();
+    S.perm = at<uint32_t>(M.send_perm);
+  }
+
+  // phase 1: encode + regular sample (+ violation word) into samples[rank]
+  husky_status phase1() {
+    init_sorter();
+    HCHECK(cudaMemsetAsync(st(), 0, sizeof(DevState), s));
+    HCHECK(S.reset_lookback());
+    launch_encode(coder, false, units, offsets, n, at<uint64_t>(M.L.keysA), st(), S.sms, s);
+    { Scope sc_(ST_MULTI, s, 0); }
+    k_sample<<<1, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, at<uint64_t>(M.samples) + (size_t)rank * kSampleStride,
+                               st());
+    HCHECK(cudaGetLastError());
+    return HUSKY_OK;
+  }
+
+  // after the samples are gathered: splitters, then bucket + counts (phase 2)
+  husky_status choose_splitters() {
+    std::vector<uint64_t> all((size_t)world * kSampleStride);
+    HCHECK(cudaMemcpyAsync(all.data(), at<uint64_t>(M.samples), all.size() * 8, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaStreamSynchronize(s));
+    uint32_t viol = 0;
+    std::vector<uint64_t> smp;
+    smp.reserve((size_t)world * kSamplesPerRank);
+    for (int r = 0; r < world; ++r) {
+      viol |= (uint32_t)all[(size_t)r * kSampleStride + kSamplesPerRank];
+      for (int i = 0; i < kSamplesPerRank; ++i) {
+        uint64_t v = all[(size_t)r * kSampleStride + i];
+        if (v != ~0ull) smp.push_back(v);
+      }
+    }
+    if (viol & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing (some rank)");
+    if (coder == HUSKY_CODER_ASCII && (viol & kDomainBad))
+      return fail(HUSKY_ERR_DOMAIN, "ASCII coder: a unit > 0x7F inside a code prefix (some rank)");
+    splitters.assign(world > 1 ? world - 1 : 0, 0);
+    if (world > 1) husky_select_splitters(smp.data(), smp.size(), world, splitters.data());
+    if (world > 1)
+      HCHECK(cudaMemcpyAsync(at<uint64_t>(M.splitters), splitters.data(), splitters.size() * 8,
+                             cudaMemcpyHostToDevice, s));
+    return HUSKY_OK;
+  }
+
+  husky_status phase2() {
+    HCHECK(cudaMemsetAsync(at<uint8_t>(M.counts), 0, (size_t)world * 16, s));
+    HCHECK(cudaMemsetAsync(st()->hist, 0, sizeof(st()->hist), s));
+    if (n) {
+      unsigned blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)S.sms * 4);
+      { Scope sc_(ST_MULTI, s, 0); }
+      k_bucket<<<blocks, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, at<uint64_t>(M.splitters), world - 1, world,
+                                      offsets, at<uint64_t>(M.L.keysB), st(), at<unsigned long long>(M.counts));
+      launch_hist_scan(n, st(), s);
+      HCHECK(cudaGetLastError());
+    }
+    return HUSKY_OK;
+  }
+
+  husky_status read_counts() {
+    std::vector<uint64_t> c((size_t)world * 2), rc((size_t)world * 2);
+    HCHECK(cudaMemcpyAsync(c.data(), at<uint64_t>(M.counts), c.size() * 8, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaMemcpyAsync(rc.data(), at<uint64_t>(M.rcounts), rc.size() * 8, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaStreamSynchronize(s));
+    send_cnt.resize(world); send_u.resize(world); recv_cnt.resize(world); recv_u.resize(world);
+    n_out = units_out = 0;
+    for (int p = 0; p < world; ++p) {
+      send_cnt[p] = c[2 * p]; send_u[p] = c[2 * p + 1];
+      recv_cnt[p] = rc[2 * p]; recv_u[p] = rc[2 * p + 1];
+      n_out += recv_cnt[p];
+      units_out += recv_u[p];
+    }
+    return HUSKY_OK;
+  }
+
+  // phase 3: stable partition by bucket + send buffers
+  husky_status phase3() {
+    if (n == 0) return HUSKY_OK;
+    uint64_t *sorted_keys = nullptr;
+    // bucket ids only occupy digit 0
+    if (husky_status e = S.radix(at<uint64_t>(M.L.keysB), nullptr, n, 0xFEu, at<uint32_t>(M.send_perm),
+                                 at<uint32_t>(M.L.vals), &sorted_keys))
+      return e;
+    { Scope sc_(ST_MULTI, s, 0); }
+    k_send_meta<<<grid_for(n), 256, 0, s>>>(at<uint32_t>(M.send_perm), n, offsets, (uint32_t)gbase,
+                                            at<uint32_t>(M.send_gidx), at<uint32_t>(M.send_lens));
+    launch_gather(coder, at<uint32_t>(M.send_perm), n, units, offsets, at<void>(M.send_units),
+                  at<int64_t>(M.send_offsets), S.lb_scan(), S.next_counter(), S.next_epoch(), s);
+    HCHECK(cudaGetLastError());
+    return HUSKY_OK;
+  }
+
+  // phase 4 on the received bucket (recv buffers already filled)
+  husky_status phase4(uint8_t *rws, const RecvLayout &R, uint32_t *d_perm_out, void *d_sorted_units_out,
+                      int64_t *d_sorted_offsets_out, husky_outcome *h_out) {
+    if (n_out == 0) {
+      if (h_out) { memset(h_out, 0, sizeof *h_out); h_out->perfect = 1; h_out->domain_ok = 1; }
+      if (d_sorted_offsets_out) HCHECK(cudaMemsetAsync(d_sorted_offsets_out, 0, 8, s));
+      return HUSKY_OK;
+    }
+    HCHECK(cudaMemsetAsync(rws + R.lb, 0, scan_tiles(n_out) * 8 + 8, s));
+    HCHECK(cudaMemsetAsync(&st()->tile_counter[63], 0, 4, s));
+    { Scope sc_(ST_MULTI, s, 0); }
+    k_lens_to_offsets<<<(unsigned)scan_tiles(n_out), kScanThreads, 0, s>>>(
+        (const uint32_t *)(rws + R.lens), n_out, (int64_t *)(rws + R.offsets), (unsigned long long *)(rws + R.lb),
+        &st()->tile_counter[63], 1, 0);
+    HCHECK(cudaGetLastError());
+    husky_status e = sort_impl(coder, rws + R.units, (const int64_t *)(rws + R.offsets), n_out, d_perm_out,
+                               d_sorted_units_out, d_sorted_offsets_out, rws + R.sort_ws,
+                               make_layout(n_out).total, h_out, s);
+    if (e) return e;
+    { Scope sc_(ST_MULTI, s, 0); }
+    k_remap<<<grid_for(n_out), 256, 0, s>>>(d_perm_out, n_out, (const uint32_t *)(rws + R.gidx));
+    HCHECK(cudaGetLastError());
+    return HUSKY_OK;
+  }
+};
+
+// exchange over NCCL: counts (phase 2) and data (phase 3)
+static husky_status nccl_allgather_samples(Plan &P) {
+  uint64_t *buf = P.at<uint64_t>(P.M.samples);
+  NCHECK(ncclAllGather(buf + (size_t)P.rank * kSampleStride, buf, kSampleStride, ncclUint64, P.comm->nccl, P.s));
+  return HUSKY_OK;
+}
+
+static husky_status nccl_alltoall_counts(Plan &P) {
+  uint64_t *c = P.at<uint64_t>(P.M.counts), *rc = P.at<uint64_t>(P.M.rcounts);
+  NCHECK(ncclGroupStart());
+  for (int p = 0; p < P.world; ++p) {
+    NCHECK(ncclSend(c + 2 * p, 2, ncclUint64, p, P.comm->nccl, P.s));
+    NCHECK(ncclRecv(rc + 2 * p, 2, ncclUint64, p, P.comm->nccl, P.s));
+  }
+  NCHECK(ncclGroupEnd());
+  return HUSKY_OK;
+}
+
+static husky_status nccl_exchange(Plan &P, uint8_t *rws, const RecvLayout &R) {
+  const size_t w = P.w();
+  uint64_t so = 0, su = 0, ro = 0, ru = 0;
+  NCHECK(ncclGroupStart());
+  for (int p = 0; p < P.world; ++p) {
+    if (P.send_cnt[p]) {
+      NCHECK(ncclSend(P.at<uint8_t>(P.M.send_units) + su * w, P.send_u[p] * w, ncclUint8, p, P.comm->nccl, P.s));
+      NCHECK(ncclSend(P.at<uint32_t>(P.M.send_lens) + so, P.send_cnt[p], ncclUint32, p, P.comm->nccl, P.s));
+      NCHECK(ncclSend(P.at<uint32_t>(P.M.send_gidx) + so, P.send_cnt[p], ncclUint32, p, P.comm->nccl, P.s));
+    }
+    if (P.recv_cnt[p]) {
+      NCHECK(ncclRecv(rws + R.units + ru * w, P.recv_u[p] * w, ncclUint8, p, P.comm->nccl, P.s));
+      NCHECK(ncclRecv((uint32_t *)(rws + R.lens) + ro, P.recv_cnt[p], ncclUint32, p, P.comm->nccl, P.s));
+      NCHECK(ncclRecv((uint32_t *)(rws + R.gidx) + ro, P.recv_cnt[p], ncclUint32, p, P.comm->nccl, P.s));
+    }
+    so += P.send_cnt[p]; su += P.send_u[p]; ro += P.recv_cnt[p]; ru += P.recv_u[p];
+  }
+  NCHECK(ncclGroupEnd());
+  return HUSKY_OK;
+}
+
+static bool valid_coder(int c) { return c == HUSKY_CODER_ASCII || c == HUSKY_CODER_UNICODE; }
+
+}  // namespace husky
+
+using namespace husky;
+
+extern "C" {
+
+husky_status husky_select_splitters(const uint64_t *h_samples, uint64_t n_samples, int world,
+                                    uint64_t *h_splitters) {
+  if (world < 1 || world > kMaxWorld) return fail(HUSKY_ERR_INVALID_ARG, "world %d out of range", world);
+  if (world == 1) return HUSKY_OK;
+  if (!h_splitters || (n_samples && !h_samples)) return fail(HUSKY_ERR_INVALID_ARG, "null pointer");
+  std::vector<uint64_t> v(h_samples, h_samples + n_samples);
+  std::sort(v.begin(), v.end());
+  for (int k = 1; k < world; ++k)
+    h_splitters[k - 1] = n_samples ? v[(size_t)((unsigned __int128)k * n_samples / world)] : ~0ull;
+  return HUSKY_OK;
+}
+
+husky_status husky_comm_unique_id(uint8_t id[128]) {
+  if (!id) return fail(HUSKY_ERR_INVALID_ARG, "id is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId u;
+  NCHECK(ncclGetUniqueId(&u));
+  memcpy(id, &u, 128);
+  return HUSKY_OK;
+}
+
+husky_status husky_comm_create(int rank, int world, const uint8_t id[128], void **comm) {
+  if (!id || !comm || world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+    return fail(HUSKY_ERR_INVALID_ARG, "bad comm arguments (rank %d, world %d)", rank, world);
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  Comm *c = new Comm;
+  c->rank = rank;
+  c->world = world;
+  ncclResult_t r = ncclCommInitRank(&c->nccl, world, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(HUSKY_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *comm = c;
+  return HUSKY_OK;
+}
+
+husky_status husky_comm_destroy(void *comm) {
+  if (!comm) return HUSKY_OK;
+  Comm *c = (Comm *)comm;
+  ncclResult_t r = ncclCommDestroy(c->nccl);
+  delete c;
+  if (r != ncclSuccess) return fail(HUSKY_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
+  return HUSKY_OK;
+}
+
+husky_status husky_sort_multi_workspace(int coder, uint64_t n_local, uint64_t local_units, int world,
+                                        size_t *bytes) {
+  if (!valid_coder(coder) || !bytes || world < 1 || world > kMaxWorld)
+    return fail(HUSKY_ERR_INVALID_ARG, "bad arguments");
+  *bytes = make_multi_layout(coder, n_local, local_units, world).total;
+  return HUSKY_OK;
+}
+
+husky_status husky_sort_multi_plan(void *comm, int coder, const void *d_units, const int64_t *d_offsets,
+                                   uint64_t n_local, uint64_t global_base, void *d_ws, size_t ws_bytes,
+                                   void **plan, uint64_t *h_n_out, uint64_t *h_units_out, void *stream) {
+  if (!comm || !valid_coder(coder) || !plan || !d_offsets || !d_ws || (n_local && !d_units))
+    return fail(HUSKY_ERR_INVALID_ARG, "null required pointer or unknown coder");
+  if (global_base + n_local >= 0xFFFFFFFFull) return fail(HUSKY_ERR_INVALID_ARG, "global index >= 2^32 - 1");
+  if ((uintptr_t)d_ws % 256) return fail(HUSKY_ERR_INVALID_ARG, "workspace not 256-byte aligned");
+  Comm *c = (Comm *)comm;
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t o[2] = {0, 0};
+  if (n_local) {
+    HCHECK(cudaMemcpyAsync(&o[0], d_offsets, 8, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaMemcpyAsync(&o[1], d_offsets + n_local, 8, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaStreamSynchronize(s));
+  }
+  Plan *P = new Plan;
+  P->comm = c;
+  P->coder = coder;
+  P->rank = c->rank;
+  P->world = c->world;
+  P->units = d_units;
+  P->offsets = d_offsets;
+  P->n = n_local;
+  P->gbase = global_base;
+  P->local_units = (uint64_t)(o[1] - o[0]);
+  P->ws = (uint8_t *)d_ws;
+  P->s = s;
+  P->M = make_multi_layout(coder, n_local, P->local_units, c->world);
+  husky_status e = HUSKY_OK;
+  if (ws_bytes < P->M.total) e = fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, P->M.total);
+  if (!e) e = P->phase1();
+  if (!e) e = nccl_allgather_samples(*P);
+  if (!e) e = P->choose_splitters();
+  if (!e) e = P->phase2();
+  if (!e) e = nccl_alltoall_counts(*P);
+  if (!e) e = P->read_counts();
+  if (e) { delete P; return e; }
+  if (h_n_out) *h_n_out = P->n_out;
+  if (h_units_out) *h_units_out = P->units_out;
+  *plan = P;
+  return HUSKY_OK;
+}
+
+husky_status husky_sort_multi_recv_workspace(void *plan, size_t *bytes) {
+  if (!plan || !bytes) return fail(HUSKY_ERR_INVALID_ARG, "null pointer");
+  Plan *P = (Plan *)plan;
+  *bytes = make_recv_layout(P->coder, P->n_out, P->units_out).total;
+  return HUSKY_OK;
+}
+
+husky_status husky_sort_multi_exec(void *plan, uint32_t *d_perm_out, void *d_sorted_units_out,
+                                   int64_t *d_sorted_offsets_out, void *d_recv_ws, size_t recv_ws_bytes,
+                                   husky_outcome *h_out, void *stream) {
+  if (!plan || (!d_perm_out && ((Plan *)plan)->n_out) || !d_recv_ws)
+    return fail(HUSKY_ERR_INVALID_ARG, "null required pointer");
+  if ((d_sorted_units_out == nullptr) != (d_sorted_offsets_out == nullptr))
+    return fail(HUSKY_ERR_INVALID_ARG, "sorted units/offsets must both be set or both NULL");
+  Plan *P = (Plan *)plan;
+  P->s = (cudaStream_t)stream;
+  P->S.s = P->s;
+  RecvLayout R = make_recv_layout(P->coder, P->n_out, P->units_out);
+  if (recv_ws_bytes < R.total) return fail(HUSKY_ERR_WORKSPACE, "recv workspace %zu < %zu", recv_ws_bytes, R.total);
+  if ((uintptr_t)d_recv_ws % 256) return fail(HUSKY_ERR_INVALID_ARG, "workspace not 256-byte aligned");
+  if (husky_status e = P->phase3()) return e;
+  if (husky_status e = nccl_exchange(*P, (uint8_t *)d_recv_ws, R)) return e;
+  if (husky_status e = P->phase4((uint8_t *)d_recv_ws, R, d_perm_out, d_sorted_units_out, d_sorted_offsets_out, h_out))
+    return e;
+  HCHECK(cudaStreamSynchronize(P->s));
+  return HUSKY_OK;
+}
+
+husky_status husky_plan_destroy(void *plan) {
+  delete (Plan *)plan;
+  return HUSKY_OK;
+}
+
+husky_status husky_sort_multi(void *comm, int coder, const void *d_units, const int64_t *d_offsets,
+                              uint64_t n_local, uint64_t global_base, uint32_t *d_perm_out,
+                              void *d_sorted_units_out, int64_t *d_sorted_offsets_out, uint64_t cap_n,
+                              uint64_t cap_units, uint64_t *h_n_out, uint64_t *h_units_out, void *d_ws,
+                              size_t ws_bytes, husky_outcome *h_out, void *stream) {
+  // d_ws holds the plan workspace followed by the receive workspace
+  if (!d_ws) return fail(HUSKY_ERR_INVALID_ARG, "null workspace");
+  if (!comm || !valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "null comm or unknown coder");
+  Comm *c = (Comm *)comm;
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t o[2] = {0, 0};
+  if (n_local) {
+    HCHECK(cudaMemcpyAsync(&o[0], d_offsets, 8, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaMemcpyAsync(&o[1], d_offsets + n_local, 8, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaStreamSynchronize(s));
+  }
+  size_t plan_bytes = make_multi_layout(coder, n_local, (uint64_t)(o[1] - o[0]), c->world).total;
+  if (ws_bytes < plan_bytes) return fail(HUSKY_ERR_WORKSPACE, "workspace %zu < plan %zu", ws_bytes, plan_bytes);
+  void *plan = nullptr;
+  uint64_t n_out = 0, u_out = 0;
+  if (husky_status e = husky_sort_multi_plan(comm, coder, d_units, d_offsets, n_local, global_base, d_ws,
+                                             plan_bytes, &plan, &n_out, &u_out, stream))
+    return e;
+  if (h_n_out) *h_n_out = n_out;
+  if (h_units_out) *h_units_out = u_out;
+  size_t rb = make_recv_layout(coder, n_out, u_out).total;
+  husky_status e = HUSKY_OK;
+  if (n_out > cap_n || u_out > cap_units) e = fail(HUSKY_ERR_CAPACITY, "shard needs %llu strings / %llu units",
+                                                   (unsigned long long)n_out, (unsigned long long)u_out);
+  // NOTE: every rank must reach the exchange; a capacity failure on one rank
+  // would leave its peers blocked, so callers size outputs from the plan query.
+  else if (ws_bytes < plan_bytes + rb) e = fail(HUSKY_ERR_WORKSPACE, "workspace too small for receive buffers");
+  else e = husky_sort_multi_exec(plan, d_perm_out, d_sorted_units_out, d_sorted_offsets_out,
+                                 (uint8_t *)d_ws + align_up(plan_bytes, 256), ws_bytes - align_up(plan_bytes, 256),
+                                 h_out, stream);
+  husky_plan_destroy(plan);
+  return e;
+}
+
+// ------------------------------------------------------------ loopback driver
+// Sorts n strings as if block-distributed over `world` virtual ranks of ONE GPU,
+// running exactly the sample-sort phases above with device-to-device copies as
+// the transport.  Output = the rank-order concatenation (global perm, sorted
+// units, global sorted offsets).  h_shard_n (nullable, world entries) receives
+// the shard sizes.  Test hook for the sharded path; declared in husky.h.
+static uint64_t lb_base(uint64_t n, int world, int r) { return (uint64_t)((unsigned __int128)n * r / world); }
+
+husky_status husky_sort_multi_loopback_workspace(int coder, int world, uint64_t n, uint64_t total_units,
+                                                 size_t *bytes) {
+  if (!valid_coder(coder) || !bytes || world < 1 || world > kMaxWorld) return fail(HUSKY_ERR_INVALID_ARG, "bad args");
+  size_t tot = 0;
+  for (int r = 0; r < world; ++r) {
+    uint64_t nr = lb_base(n, world, r + 1) - lb_base(n, world, r);
+    tot += align_up(make_multi_layout(coder, nr, total_units, world).total, 256);  // units bound per rank
+  }
+  tot += align_up(make_recv_layout(coder, n, total_units).total, 256);  // shared recv + sort ws (worst case)
+  tot += align_up((size_t)world * 256, 256) * world;
+  *bytes = tot;
+  return HUSKY_OK;
+}
+
+husky_status husky_sort_multi_loopback(int coder, int world, const void *d_units, const int64_t *d_offsets,
+                                       uint64_t n, uint32_t *d_perm, void *d_sorted_units,
+                                       int64_t *d_sorted_offsets, void *d_ws, size_t ws_bytes,
+                                       uint64_t *h_shard_n, husky_outcome *h_out, void *stream) {
+  if (!valid_coder(coder) || world < 1 || world > kMaxWorld || !d_offsets || !d_ws || (n && (!d_units || !d_perm)))
+    return fail(HUSKY_ERR_INVALID_ARG, "bad arguments");
+  if ((d_sorted_units == nullptr) != (d_sorted_offsets == nullptr))
+    return fail(HUSKY_ERR_INVALID_ARG, "sorted units/offsets must both be set or both NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<int64_t> bo(world + 1);
+  for (int r = 0; r <= world; ++r)
+    HCHECK(cudaMemcpyAsync(&bo[r], d_offsets + lb_base(n, world, r), 8, cudaMemcpyDeviceToHost, s));
+  HCHECK(cudaStreamSynchronize(s));
+  uint64_t total_units = (uint64_t)(bo[world] - bo[0]);
+  size_t need = 0;
+  husky_sort_multi_loopback_workspace(coder, world, n, total_units, &need);
+  if (ws_bytes < need) return fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, need);
+  uint8_t *ws = (uint8_t *)d_ws;
+  size_t off = 0;
+  std::vector<Plan> P(world);
+  for (int r = 0; r < world; ++r) {
+    Plan &p = P[r];
+    p.coder = coder; p.rank = r; p.world = world; p.units = d_units;
+    p.offsets = d_offsets + lb_base(n, world, r);
+    p.n = lb_base(n, world, r + 1) - lb_base(n, world, r);
+    p.gbase = lb_base(n, world, r);
+    p.local_units = (uint64_t)(bo[r + 1] - bo[r]);
+    p.s = s;
+    p.M = make_multi_layout(coder, p.n, p.local_units, world);
+    p.ws = ws + off;
+    off += align_up(make_multi_layout(coder, p.n, total_units, world).total, 256);
+  }
+  uint8_t *rws_all = ws + off;
+  // phase 1 + "all-gather" of the samples
+  for (auto &p : P) if (husky_status e = p.phase1()) return e;
+  for (int r = 0; r < world; ++r)
+    for (int q = 0; q < world; ++q)
+      if (q != r)
+        HCHECK(cudaMemcpyAsync(P[r].at<uint64_t>(P[r].M.samples) + (size_t)q * kSampleStride,
+                               P[q].at<uint64_t>(P[q].M.samples) + (size_t)q * kSampleStride, kSampleStride * 8,
+                               cudaMemcpyDeviceToDevice, s));
+  for (auto &p : P) if (husky_status e = p.choose_splitters()) return e;
+  for (auto &p : P) if (husky_status e = p.phase2()) return e;
+  // "all-to-all" of the counts: rcounts[r][q] = counts[q][r]
+  for (int r = 0; r < world; ++r)
+    for (int q = 0; q < world; ++q)
+      HCHECK(cudaMemcpyAsync(P[r].at<uint64_t>(P[r].M.rcounts) + 2 * q, P[q].at<uint64_t>(P[q].M.counts) + 2 * r, 16,
+                             cudaMemcpyDeviceToDevice, s));
+  for (auto &p : P) if (husky_status e = p.read_counts()) return e;
+  for (auto &p : P) if (husky_status e = p.phase3()) return e;
+  // data exchange + local sorts, one destination rank at a time (shared recv ws)
+  const size_t w = coder == HUSKY_CODER_ASCII ? 1 : 2;
+  uint64_t out_n = 0, out_u = 0;
+  husky_outcome agg;
+  memset(&agg, 0, sizeof agg);
+  agg.perfect = 1; agg.domain_ok = 1;
+  for (int r = 0; r < world; ++r) {
+    Plan &dst = P[r];
+    RecvLayout R = make_recv_layout(coder, dst.n_out, dst.units_out);
+    uint64_t ro = 0, ru = 0;
+    for (int q = 0; q < world; ++q) {
+      Plan &src = P[q];
+      uint64_t so = 0, su = 0;
+      for (int k = 0; k < r; ++k) { so += src.send_cnt[k]; su += src.send_u[k]; }
+      uint64_t cnt = src.send_cnt[r], u = src.send_u[r];
+      if (cnt) {
+        HCHECK(cudaMemcpyAsync(rws_all + R.units + ru * w, src.at<uint8_t>(src.M.send_units) + su * w, u * w,
+                               cudaMemcpyDeviceToDevice, s));
+        HCHECK(cudaMemcpyAsync((uint32_t *)(rws_all + R.lens) + ro, src.at<uint32_t>(src.M.send_lens) + so, cnt * 4,
+                               cudaMemcpyDeviceToDevice, s));
+        HCHECK(cudaMemcpyAsync((uint32_t *)(rws_all + R.gidx) + ro, src.at<uint32_t>(src.M.send_gidx) + so, cnt * 4,
+                               cudaMemcpyDeviceToDevice, s));
+      }
+      ro += cnt; ru += u;
+    }
+    husky_outcome o;
+    // empty shards write nothing (their offsets slot belongs to the previous shard)
+    void *su_out = (d_sorted_units && dst.n_out) ? (uint8_t *)d_sorted_units + out_u * w : nullptr;
+    int64_t *so_out = (d_sorted_offsets && dst.n_out) ? d_sorted_offsets + out_n : nullptr;
+    // offsets slot out_n is shared with the previous shard's end: write it first
+    if (husky_status e = dst.phase4(rws_all, R, d_perm + out_n, su_out, so_out, &o)) return e;
+    if (so_out && out_u && dst.n_out)
+      { Scope sc_(ST_MULTI, s, 0); }
+      k_add_base<<<grid_for(dst.n_out + 1), 256, 0, s>>>(so_out, dst.n_out + 1, (int64_t)out_u);
+    if (h_shard_n) h_shard_n[r] = dst.n_out;
+    agg.perfect &= o.perfect; agg.domain_ok &= o.domain_ok;
+    agg.n_runs += o.n_runs; agg.n_in_runs += o.n_in_runs;
+    agg.max_run = std::max(agg.max_run, o.max_run);
+    for (int c = 0; c < 4; ++c) agg.runs_by_class[c] += o.runs_by_class[c];
+    agg.refine_rounds += o.refine_rounds; agg.radix_passes += o.radix_passes;
+    out_n += dst.n_out; out_u += dst.units_out;
+  }
+  if (n == 0 && d_sorted_offsets) HCHECK(cudaMemsetAsync(d_sorted_offsets, 0, 8, s));
+  HCHECK(cudaStreamSynchronize(s));
+  HCHECK(cudaGetLastError());
+  if (h_out) *h_out = agg;
+  return HUSKY_OK;
+}
+
+}  // extern "C"

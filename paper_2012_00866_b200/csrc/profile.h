@@ -1,0 +1,82 @@
+// profile.h -- per-stage launch accounting for libhusky.
+//
+// Every kernel launch of the library goes through a Scope, which (a) always
+// counts the launch and (b) when profiling is enabled records a CUDA event
+// pair around it on the launching stream.  Elapsed times are harvested at the
+// library's synchronisation points (events already complete).  This is the
+// T1/T2/T3 split of PAPER.md:238-245 measured per kernel family.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <vector>
+
+namespace husky {
+
+enum Stage : int {
+  ST_ENCODE = 0, ST_HIST_SCAN, ST_RADIX, ST_RUNS_SCAN, ST_CLASSIFY, ST_FIX_SMALL, ST_FIX_MEDIUM,
+  ST_REFINE, ST_GATHER, ST_MULTI, ST_COUNT
+};
+
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  struct Pending { int stage; cudaEvent_t a, b; uint64_t elems; };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[ST_COUNT] = {};
+  uint64_t launches[ST_COUNT] = {};
+  uint64_t elems[ST_COUNT] = {};
+  uint64_t total_launches = 0;  // always counted
+
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  // harvest every pending pair (call after a stream synchronisation)
+  void flush() {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto &p : pending) {
+      float t = 0.f;
+      if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) {
+        ms[p.stage] += t;
+      }
+      pool.push_back(p.a);
+      pool.push_back(p.b);
+    }
+    pending.clear();
+  }
+};
+
+Profiler &profiler();
+
+struct Scope {
+  int stage;
+  cudaStream_t s;
+  uint64_t elems;
+  cudaEvent_t a = nullptr;
+  Scope(int st, cudaStream_t str, uint64_t m) : stage(st), s(str), elems(m) {
+    Profiler &P = profiler();
+    std::lock_guard<std::mutex> g(P.mu);
+    P.total_launches++;
+    P.launches[stage]++;
+    P.elems[stage] += m;
+    if (P.on) {
+      a = P.get();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~Scope() {
+    if (!a) return;
+    Profiler &P = profiler();
+    std::lock_guard<std::mutex> g(P.mu);
+    cudaEvent_t b = P.get();
+    cudaEventRecord(b, s);
+    P.pending.push_back({stage, a, b, elems});
+  }
+};
+
+}  // namespace husky

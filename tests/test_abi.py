@@ -1,0 +1,60 @@
+"""The C-ABI library loads and exports every symbol include/husky.h declares
+(no compute calls: this runs without a GPU), plus the host-only entry points."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    txt = open(os.path.join(ROOT, "include", "husky.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(husky_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_header_declares_the_north_star_entry_points():
+    names = _declared()
+    for must in ("husky_encode", "husky_sort", "husky_sort_multi"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2012_00866_b200 as h
+    lib = ctypes.CDLL(h.LIB_PATH)
+    missing = [n for n in _declared() if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(_declared()) == set(h.EXPORTED)
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    import paper_2012_00866_b200 as h
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", h.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_unit_bytes_and_workspace_queries():
+    import paper_2012_00866_b200 as h
+    assert h.husky_unit_bytes(0) == 1 and h.husky_unit_bytes(1) == 2 and h.husky_unit_bytes(7) == 0
+    w1 = h.husky_sort_workspace(0, 10_000_000)
+    w2 = h.husky_sort_workspace(0, 20_000_000)
+    assert 10_000_000 * 20 < w1 < w2
+    with pytest.raises(h.HuskyError) as e:
+        h.husky_sort_workspace(5, 10)
+    assert e.value.status == 1 and "coder" in h.husky_last_error()
+
+
+def test_select_splitters_host():
+    import paper_2012_00866_b200 as h
+    rng = np.random.default_rng(0)
+    s = rng.integers(0, 2**63, size=4 * 4096, dtype=np.uint64)
+    sp = h.husky_select_splitters(s, 4)
+    ss = np.sort(s)
+    assert sp.tolist() == [ss[k * s.size // 4] for k in (1, 2, 3)]
+    assert h.husky_select_splitters(s, 1).size == 0

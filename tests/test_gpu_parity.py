@@ -1,0 +1,304 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, bit-exact.
+
+Everything on the path is integer (no floating point), so the bar is bit
+equality of codes, permutation, sorted units and sorted offsets.  Sizes span
+several tiles (radix 4096, scan 2048, gather 1024) with ragged tails; the
+full BASELINE.json sizes are checked with the oracle's linear uniqueness
+verifier (bijection + strictly increasing adjacent pairs <=> equal to the
+oracle's sort, because the order is a strict total order).
+"""
+import random
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+ASCII, UNICODE = 0, 1
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    if not t.cuda.is_available():
+        pytest.skip("no GPU")
+    return t
+
+
+@pytest.fixture(scope="module")
+def h():
+    import paper_2012_00866_b200 as m
+    return m
+
+
+def to_dev(torch, w):
+    u = w.units
+    if u.dtype == np.uint16:
+        u = u.view(np.int16)
+    if u.size == 0:
+        u = np.zeros(1, dtype=u.dtype)
+    return torch.from_numpy(np.ascontiguousarray(u)).cuda(), torch.from_numpy(w.offsets).cuda()
+
+
+def run_sort(torch, h, w, with_units=True):
+    u, o = to_dev(torch, w)
+    perm, su, so, outc = h.sort(w.coder, u, o, with_units=with_units)
+    torch.cuda.synchronize()
+    perm = perm.cpu().numpy().view(np.uint32)
+    if with_units:
+        su = su.cpu().numpy()
+        if w.coder == UNICODE:
+            su = su.view(np.uint16)
+        so = so.cpu().numpy()
+    return perm, su, so, outc
+
+
+def check_against_oracle(torch, h, oracle_mod, w, with_units=True):
+    perm, su, so, outc = run_sort(torch, h, w, with_units)
+    ref = oracle_mod.sort(w.coder, w.units, w.offsets)
+    assert perm.shape == ref.shape
+    bad = np.nonzero(perm != ref)[0]
+    assert bad.size == 0, f"{w.name}: first mismatch at {bad[:5]}, got {perm[bad[:5]]} want {ref[bad[:5]]}"
+    if with_units:
+        rsu, rso = oracle_mod.gather(w.coder, w.units, w.offsets, ref)
+        assert np.array_equal(so, rso)
+        assert np.array_equal(su, rsu)
+    return outc
+
+
+def rand_wl(seed, n, alphabet, minlen, maxlen, coder=ASCII, prefix=()):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(minlen, maxlen + 1, size=n)
+    alph = np.asarray(alphabet, dtype=np.uint8 if coder == ASCII else np.uint16)
+    strings = []
+    for L in lens:
+        strings.append(list(prefix) + alph[rng.integers(0, alph.size, size=int(L))].tolist())
+    return W.from_strings(strings, coder, name=f"rand{seed}")
+
+
+# --------------------------------------------------------------------- A1
+@pytest.mark.parametrize("name,n", [("C1", 100_000), ("C2", 300_000), ("C3", 300_000), ("C4", 100_000),
+                                    ("C5", 1 << 16)])
+def test_encode_parity_configs(torch, h, oracle_mod, name, n):
+    w = W.make(name, n)
+    u, o = to_dev(torch, w)
+    codes, perfect = h.husky_encode(w.coder, u, o)
+    ref, rperf = oracle_mod.encode(w.coder, w.units, w.offsets)
+    assert np.array_equal(codes.cpu().numpy().view(np.uint64), ref)
+    assert perfect == rperf
+
+
+@pytest.mark.parametrize("coder", [ASCII, UNICODE])
+def test_encode_parity_edge_units(torch, h, oracle_mod, coder):
+    """All unit values incl. > 0x7F (Alg. 4 masks them), empty strings, every
+    length 0..20, every start alignment."""
+    rng = random.Random(1)
+    hi = 255 if coder == ASCII else 0xFFFF
+    strings = [[rng.randint(0, hi) for _ in range(L)] for L in range(21) for _ in range(40)]
+    strings += [[], [0], [hi] * 12, [0] * 12]
+    w = W.from_strings(strings, coder)
+    u, o = to_dev(torch, w)
+    codes, perfect = h.husky_encode(coder, u, o)
+    ref, rperf = oracle_mod.encode(coder, w.units, w.offsets)
+    assert np.array_equal(codes.cpu().numpy().view(np.uint64), ref)
+    assert perfect == rperf
+    # perfect flag boundary (Alg. 3): all lengths <= PL
+    pl = 9 if coder == ASCII else 3
+    w2 = W.from_strings([[0x61] * k for k in range(pl + 1)] * 50, coder)
+    _, p2 = h.husky_encode(coder, *to_dev(torch, w2))
+    assert p2 is True
+
+
+def test_encode_rejects_bad_offsets(torch, h):
+    w = W.from_strings([b"abc", b"de"], ASCII)
+    u, o = to_dev(torch, w)
+    o[1] = 5  # 0, 5, 5 ok; make it decreasing
+    o[2] = 4
+    with pytest.raises(h.HuskyError) as e:
+        h.husky_encode(ASCII, u, o)
+    assert e.value.status == 1
+
+
+# ------------------------------------------------------------ full sort
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 17, 1023, 1024, 1025, 2047, 2049, 4095, 4096, 4097, 12289, 70001])
+def test_sort_sizes_ragged(torch, h, oracle_mod, n):
+    w = rand_wl(n, n, range(0x61, 0x65), 0, 14)
+    check_against_oracle(torch, h, oracle_mod, w)
+
+
+@pytest.mark.parametrize("coder", [ASCII, UNICODE])
+@pytest.mark.parametrize("case", ["nul_ext", "all_equal", "tiny_alpha", "empties", "long_tail", "sorted",
+                                  "reverse"])
+def test_sort_degenerate(torch, h, oracle_mod, coder, case):
+    rng = random.Random(hash(case) & 0xFFFF)
+    hi = 0x7F if coder == ASCII else 0xFFFF
+    if case == "nul_ext":  # equal codes, order decided by length (short-rule, reading R6)
+        base = [[0x61], [0x61, 0], [0x61, 0, 0], [0x61, 0, 0, 0], [0x61, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0]]
+        strings = [list(rng.choice(base)) for _ in range(5000)]
+    elif case == "all_equal":
+        strings = [[0x62] * 30] * 9000
+    elif case == "tiny_alpha":
+        strings = [[rng.choice((0, 1, hi)) for _ in range(rng.randint(0, 12))] for _ in range(9000)]
+    elif case == "empties":
+        strings = [[] for _ in range(3000)] + [[1]] + [[] for _ in range(3000)]
+    elif case == "long_tail":  # long strings (> stage budget per tile for some tiles)
+        strings = [[rng.randint(1, hi) for _ in range(rng.choice((1, 5, 300, 2000)))] for _ in range(3000)]
+    elif case == "sorted":
+        strings = sorted([[rng.randint(0x61, 0x7A) for _ in range(rng.randint(1, 12))] for _ in range(9000)])
+    else:
+        strings = sorted([[rng.randint(0x61, 0x7A) for _ in range(rng.randint(1, 12))] for _ in range(9000)],
+                         reverse=True)
+    check_against_oracle(torch, h, oracle_mod, W.from_strings(strings, coder))
+
+
+@pytest.mark.parametrize("coder", [ASCII, UNICODE])
+@pytest.mark.parametrize("group", [2, 7, 32, 33, 500, 4096, 4097, 30000])
+def test_sort_dirty_runs_every_class(torch, h, oracle_mod, coder, group):
+    """Groups of strings sharing a long common prefix (equal codes) with random
+    suffixes in random order: dirty runs of every class -- warp (<=32), CTA
+    (<=4096) and giant (refinement rounds, A6)."""
+    rng = np.random.default_rng(group + 10 * coder)
+    pre = [0x41 + i % 26 for i in range(11)] if coder == ASCII else [0x4E00 + i for i in range(5)]
+    alph = np.arange(0x61, 0x64) if coder == ASCII else np.arange(0x4E00, 0x4E03)
+    strings = []
+    ngroups = max(1, 60000 // group)
+    for gi in range(ngroups):
+        p = list(pre)
+        if coder == ASCII:  # group id inside the 9-unit code window -> distinct codes per group
+            p[4], p[5], p[6] = 0x41 + gi % 26, 0x41 + (gi // 26) % 26, 0x41 + (gi // 676) % 26
+        else:  # inside the 4-unit window
+            p[1] += gi
+        for _ in range(group):
+            L = int(rng.integers(0, 10))
+            strings.append(p + alph[rng.integers(0, alph.size, size=L)].tolist())
+    order = rng.permutation(len(strings))
+    strings = [strings[i] for i in order]
+    outc = check_against_oracle(torch, h, oracle_mod, W.from_strings(strings, coder))
+    assert outc["n_runs"] > 0
+
+
+def test_sort_giant_run_c4(torch, h, oracle_mod):
+    w = W.c4(300_000)
+    outc = check_against_oracle(torch, h, oracle_mod, w)
+    assert outc["max_run"] == w.n and outc["refine_rounds"] >= 1 and outc["radix_passes"] > 0
+
+
+@pytest.mark.parametrize("name,n", [("C1", 100_000), ("C2", 1_000_000), ("C3", 1_000_000), ("C5", 1 << 20)])
+def test_sort_configs_vs_oracle(torch, h, oracle_mod, name, n):
+    check_against_oracle(torch, h, oracle_mod, W.make(name, n))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_sort_full_size_verifier(torch, h, oracle_mod, name):
+    """BASELINE.json full sizes: linear verifier (unique order) + units gather."""
+    w = W.make(name)
+    perm, su, so, outc = run_sort(torch, h, w)
+    assert oracle_mod.verify(w.coder, w.units, w.offsets, perm) == 0
+    rsu, rso = oracle_mod.gather(w.coder, w.units, w.offsets, perm)
+    assert np.array_equal(so, rso) and np.array_equal(su, rsu)
+    if name == "C2":
+        assert outc["runs_by_class"][0] == outc["n_runs"]  # every run already ordered
+
+
+def test_sort_perm_only_mode(torch, h, oracle_mod):
+    w = W.make("C1", 50_000)
+    perm, _, _, _ = run_sort(torch, h, w, with_units=False)
+    assert np.array_equal(perm, oracle_mod.sort(w.coder, w.units, w.offsets))
+
+
+def test_sort_domain_error_and_beyond_window(torch, h, oracle_mod):
+    """Unit > 0x7F inside the ASCII code window -> HUSKY_ERR_DOMAIN (reading R5);
+    beyond the window the exact byte comparator sorts it correctly."""
+    w = W.from_strings([b"abc", b"a\x80c"], ASCII)
+    with pytest.raises(h.HuskyError) as e:
+        run_sort(torch, h, w)
+    assert e.value.status == 2
+    rng = random.Random(4)
+    strings = [b"abcdefghi" + bytes(rng.randint(0, 255) for _ in range(rng.randint(0, 6))) for _ in range(5000)]
+    check_against_oracle(torch, h, oracle_mod, W.from_strings(strings, ASCII))
+
+
+def test_sort_offsets_not_starting_at_zero(torch, h, oracle_mod):
+    w = W.make("C1", 20_000)
+    pad = np.concatenate([np.full(13, 0x7A, dtype=np.uint8), w.units])
+    w2 = W.Workload("shifted", ASCII, pad, w.offsets + 13, {})
+    perm, su, so, _ = run_sort(torch, h, w2)
+    ref = oracle_mod.sort(ASCII, w.units, w.offsets)
+    assert np.array_equal(perm, ref)
+    rsu, rso = oracle_mod.gather(ASCII, w.units, w.offsets, ref)
+    assert np.array_equal(su, rsu) and np.array_equal(so, rso)
+
+
+def test_sort_host_api(torch, h, oracle_mod):
+    w = W.make("C3", 200_000)
+    n, tot = w.n, w.units.size
+    ws = torch.empty(h.husky_sort_host_workspace(w.coder, n, tot), dtype=torch.uint8, device="cuda")
+    perm = np.zeros(n, dtype=np.uint32)
+    su = np.zeros(tot, dtype=np.uint16)
+    so = np.zeros(n + 1, dtype=np.int64)
+    h.husky_sort_host(w.coder, w.units, w.offsets, perm, su, so, ws)
+    ref = oracle_mod.sort(w.coder, w.units, w.offsets)
+    assert np.array_equal(perm, ref)
+    rsu, rso = oracle_mod.gather(w.coder, w.units, w.offsets, ref)
+    assert np.array_equal(su, rsu) and np.array_equal(so, rso)
+
+
+def test_sort_repeatable_and_workspace_reuse(torch, h):
+    w = W.make("C2", 200_000)
+    u, o = to_dev(torch, w)
+    ws = torch.empty(h.husky_sort_workspace(0, w.n), dtype=torch.uint8, device="cuda")
+    ws.fill_(0xAB)  # garbage workspace contents must not matter
+    a = h.sort(0, u, o, ws=ws)[0].clone()
+    ws.fill_(0x5C)
+    b = h.sort(0, u, o, ws=ws)[0]
+    assert torch.equal(a, b)
+
+
+# ------------------------------------------------------- sharded (loopback)
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("name,n", [("C1", 60_000), ("C3", 100_000), ("C4", 50_000)])
+def test_multi_loopback_vs_oracle(torch, h, oracle_mod, world, name, n):
+    """Sample sort over `world` virtual ranks on one GPU: concatenation of the
+    shards == oracle; no equal-code run straddles shards."""
+    w = W.make(name, n)
+    u, o = to_dev(torch, w)
+    tot = w.units.size
+    ws = torch.empty(h.husky_sort_multi_loopback_workspace(w.coder, world, w.n, tot), dtype=torch.uint8,
+                     device="cuda")
+    perm = torch.empty(w.n, dtype=torch.int32, device="cuda")
+    su = torch.empty(tot + 8, dtype=u.dtype, device="cuda")
+    so = torch.empty(w.n + 1, dtype=torch.int64, device="cuda")
+    shards, outc = h.husky_sort_multi_loopback(w.coder, world, u, o, perm, su, so, ws)
+    assert sum(shards) == w.n
+    p = perm.cpu().numpy().view(np.uint32)
+    ref = oracle_mod.sort(w.coder, w.units, w.offsets)
+    assert np.array_equal(p, ref)
+    rsu, rso = oracle_mod.gather(w.coder, w.units, w.offsets, ref)
+    s_u = su[:tot].cpu().numpy()
+    if w.coder == UNICODE:
+        s_u = s_u.view(np.uint16)
+    assert np.array_equal(so.cpu().numpy(), rso) and np.array_equal(s_u, rsu)
+    # shard boundaries never split an equal-code run
+    codes, _ = oracle_mod.encode(w.coder, w.units, w.offsets)
+    sc = codes[ref]
+    b = np.cumsum(shards)[:-1]
+    b = b[(b > 0) & (b < w.n)]
+    assert not np.any(sc[b] == sc[b - 1])
+
+
+def test_multi_nccl_single_rank(torch, h, oracle_mod):
+    """The NCCL plan/exec path with a one-rank communicator."""
+    w = W.make("C1", 30_000)
+    u, o = to_dev(torch, w)
+    uid = h.husky_comm_unique_id()
+    comm = h.husky_comm_create(0, 1, uid)
+    try:
+        perm, su, so, outc = h.sort_multi(comm, w.coder, u, o, 0)
+        torch.cuda.synchronize()
+        ref = oracle_mod.sort(w.coder, w.units, w.offsets)
+        assert np.array_equal(perm.cpu().numpy().view(np.uint32), ref)
+    finally:
+        h.husky_comm_destroy(comm)
