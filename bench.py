@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the Huskysort hot path on B200 (BASELINE.json metric: strings
+sorted/sec at 1/2/4/8 B200; radix/encode HBM GB/s vs peak).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config C2] [--n N]
+
+A step = one full husky_sort (encode -> onesweep radix -> run scan/check ->
+fix-up -> gather) of one batch of synthetic strings through the C ABI, inputs
+already resident in HBM.  N = 1 runs BASELINE.json configs[1] (C2: 1e7
+English-like Zipf words); N > 1 (torchrun, one rank per GPU) runs the NCCL
+sample sort with each rank holding its own 1e7-string block (weak scaling).
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the
+reference arm of this tier: there is no reference implementation, only the
+paper) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "strings sorted/sec (M/s) at 1/2/4/8 B200; radix/encode HBM GB/s vs peak"
+UNIT = "Mstrings/s"
+DESCR = {
+    "C1": "C1: 1e5 lowercase a-z strings, len U[4,12], ASCII coder",
+    "C2": "C2: 1e7 English-like words, Zipf(1.0) over a 50,000-word synthetic vocabulary, ASCII coder",
+    "C3": "C3: 1e7 UTF-16 CJK strings (U+4E00-U+9FFF), len U[2,4], UNICODE coder",
+    "C4": "C4: 1e7 ASCII strings sharing a 16-char prefix + 8 random [0-9A-Za-z] (all codes collide)",
+    "C5": "C5: len U[8,24] [0-9A-Za-z], 1% duplicates, first 10% pre-sorted, ASCII coder",
+}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((float(f[1]), float(f[2]), f[5], f[6], f[7], f[8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        mx = max(r[1] for r in rows)
+        load = [r[0] for r in rows]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def mean_prefix(w, K):
+    L = w.offsets[1:] - w.offsets[:-1]
+    return float(np.minimum(L, K).mean()), float(L.mean())
+
+
+def cpu_baseline(name, n_sample):
+    """The oracle as it stands (single-threaded C merge sort), on the host cores."""
+    import oracle
+    oracle.build()
+    w = W.make(name, n_sample)
+    t0 = time.perf_counter()
+    oracle.sort(w.coder, w.units, w.offsets)
+    dt = time.perf_counter() - t0
+    return {"value": round(n_sample / dt / 1e6, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{name} generator, n={n_sample} strings, one oracle_sort call (top-down merge sort, "
+                      f"1 thread), {dt:.2f} s wall"}
+
+
+def make_config(args, n, coder, world):
+    return {"workload": DESCR[args.config], "n_per_gpu": n, "coder": "ascii" if coder == 0 else "unicode",
+            "outputs": "perm + sorted units + sorted offsets",
+            "l2": "256 MiB buffer written between timed steps (outside the step events)",
+            "parallelism": f"sample sort over {world} GPU(s)" if world > 1 else "1 GPU"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    n_sample = args.ref_sample
+    w = W.make(args.config, n_sample)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.sort(w.coder, w.units, w.offsets)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    value = n_sample / t / 1e6
+    sample = (f"{args.config} generator, n={n_sample} strings per step (bounded sample of the "
+              f"{W.FULL_N[args.config]}-string workload), oracle_sort, 1 thread")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8" if w.coder == 0 else "u16", "data": "synthetic",
+            "config": make_config(args, W.FULL_N[args.config] if not args.n else args.n, w.coder, 1),
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2012_00866_b200 as h
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n = args.n or W.FULL_N[args.config]
+    w = W.make(args.config, n, seed_offset=rank if world > 1 else 0)
+    K = 9 if w.coder == 0 else 4
+    p_bar, l_bar = mean_prefix(w, K)
+    ub = w.unit_bytes
+    units_np = w.units.view(np.int16) if ub == 2 else w.units
+    d_units = torch.from_numpy(np.ascontiguousarray(units_np)).to(dev)
+    d_off = torch.from_numpy(w.offsets).to(dev)
+    total_units = w.units.size
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    if world == 1:
+        ws = torch.empty(h.husky_sort_workspace(w.coder, n, total_units), dtype=torch.uint8, device=dev)
+        perm = torch.empty(n, dtype=torch.int32, device=dev)
+        su = torch.empty(total_units + 8, dtype=d_units.dtype, device=dev)
+        so = torch.empty(n + 1, dtype=torch.int64, device=dev)
+
+        def step():
+            return h.husky_sort(w.coder, d_units, d_off, perm, su, so, ws)
+    else:
+        comm = h.multi.comm_from_process_group(device=dev)
+        gbase = rank * n
+
+        def step():
+            return h.sort_multi(comm, w.coder, d_units, d_off, gbase)[3]
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        outc = step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed between steps (outside the events)
+    h.husky_profile_reset()
+    h.husky_profile_enable(True)
+    l0 = h.husky_launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            outc = step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = h.husky_launch_count() - l0
+    h.husky_profile_enable(False)
+    prof = h.husky_profile_read()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    t_local = ms / args.steps
+    if world > 1:
+        t = torch.tensor([t_local], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+    else:
+        t_step = t_local
+    value = world * n / (t_step * 1e-3) / 1e6
+
+    # ---- roofline of the dominant kernel (onesweep radix pass) and the encoder
+    peak, peak_src = peaks()
+    rp = prof["radix_pass"]
+    sorts = args.steps  # one synthesised-payload pass per sort (reads no payload)
+    radix_bytes = 24 * rp["elems"] - 4 * n * sorts if rp["launches"] else 0
+    radix_gbs = radix_bytes / (rp["ms"] * 1e-3) / 1e9 if rp["ms"] else 0.0
+    ep = prof["encode"]
+    enc_bytes = ep["elems"] * (8 + ub * p_bar + 8) + 8 * ep["launches"]
+    enc_gbs = enc_bytes / (ep["ms"] * 1e-3) / 1e9 if ep["ms"] else 0.0
+    stages = {k: {"ms_per_step": round(v["ms"] / args.steps, 4), "launches_per_step": v["launches"] / args.steps}
+              for k, v in prof.items() if v["launches"]}
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            td = json.load(open(tp)).get(args.config, {}).get("radix_pass")
+            if td:
+                traffic = int(td["bytes_per_key"] * n)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": "k_onesweep (A2 radix pass)",
+                "achieved": round(radix_gbs, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(radix_gbs / peak, 4), "traffic": traffic,
+                "bytes_alg_per_launch": int(radix_bytes / max(rp["launches"], 1)),
+                "alg_bytes_model": "24 B/key per pass (key 8 + payload 4, read + write); 20 B/key on the "
+                                   "first pass (payload synthesised)",
+                "peak_source": peak_src,
+                "encode": {"achieved": round(enc_gbs, 1), "frac": round(enc_gbs / peak, 4),
+                           "alg_bytes_model": f"16 B/string (offset + code) + {ub} B x mean min(len,{K}) "
+                                              f"= {p_bar:.2f} units"}}
+
+    # ---- end to end through the C ABI with HOST buffers (H2D/D2H inside the timed region)
+    e2e = None
+    if world == 1:
+        hu = torch.from_numpy(np.ascontiguousarray(units_np)).pin_memory()
+        ho = torch.from_numpy(w.offsets).pin_memory()
+        hp = torch.empty(n, dtype=torch.int32).pin_memory()
+        hsu = torch.empty(total_units + 8, dtype=d_units.dtype).pin_memory()
+        hso = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+        del ws
+        torch.cuda.empty_cache()
+        hws = torch.empty(h.husky_sort_host_workspace(w.coder, n, total_units), dtype=torch.uint8, device=dev)
+        for _ in range(max(1, args.warmup)):
+            h.husky_sort_host(w.coder, hu, ho, hp, hsu, hso, hws)
+        torch.cuda.synchronize()
+        e_ms = 0.0
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            h.husky_sort_host(w.coder, hu, ho, hp, hsu, hso, hws)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e_ms += a.elapsed_time(b)
+        e_ms /= args.steps
+        e2e = {"value": round(n / (e_ms * 1e-3) / 1e6, 4), "unit": UNIT,
+               "h2d_bytes_per_step": int(total_units * ub + (n + 1) * 8),
+               "d2h_bytes_per_step": int(n * 4 + total_units * ub + (n + 1) * 8),
+               "ms_per_step": round(e_ms, 3), "api": "husky_sort_host (pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, min(n, args.cpu_sample))
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u8" if ub == 1 else "u16",
+                "data": "synthetic",
+                "config": make_config(args, n, w.coder, world),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk.summary(), "stages": stages, "outcome": outc}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(DESCR))
+    ap.add_argument("--n", type=int, default=0, help="strings per GPU (default: the config's full size)")
+    ap.add_argument("--cpu-sample", type=int, default=10_000_000)
+    ap.add_argument("--ref-sample", type=int, default=4_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

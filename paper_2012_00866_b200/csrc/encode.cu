@@ -27,39 +27,25 @@ __device__ __forceinline__ uint64_t pack_ascii(uint64_t lo, uint64_t b8) {
   return (x << 7) | (b8 & 0x7F);
 }
 
+// Code of one string from the two aligned words covering its window: w0 holds
+// the byte at address `a` (sh = a & 7), w1 the next word (only read when the
+// window crosses into it).
 template <int CODER>
-__device__ __forceinline__ uint64_t encode_one(const void *units, int64_t o0, int64_t len,
-                                               uint32_t &viol) {
+__device__ __forceinline__ uint64_t encode_words(uint64_t w0, uint64_t w1, int sh, int64_t len,
+                                                 uint32_t &viol) {
   using T = CoderTraits<CODER>;
   if (len < 0) { viol |= kOffsetsBad; len = 0; }
   if (len > T::kPL) viol |= kNotPerfect;
+  uint64_t lo = sh ? ((w0 >> (8 * sh)) | (w1 << (64 - 8 * sh))) : w0;
   if (CODER == HUSKY_CODER_ASCII) {
     int m = len < 9 ? (int)len : 9;
-    uint64_t lo = 0, b8 = 0;
-    if (m > 0) {
-      uintptr_t a = (uintptr_t)((const uint8_t *)units + o0);
-      const uint64_t *w = (const uint64_t *)(a & ~(uintptr_t)7);
-      int sh = (int)(a & 7);
-      uint64_t w0 = __ldg(w);
-      uint64_t w1 = (sh + m > 8) ? __ldg(w + 1) : 0ull;
-      lo = sh ? ((w0 >> (8 * sh)) | (w1 << (64 - 8 * sh))) : w0;
-      b8 = (m == 9) ? ((w1 >> (8 * sh)) & 0xFF) : 0ull;
-      if (m < 8) lo &= (1ull << (8 * m)) - 1;
-    }
+    uint64_t b8 = (m == 9) ? ((w1 >> (8 * sh)) & 0xFF) : 0ull;
+    if (m < 8) lo &= (1ull << (8 * m)) - 1;  // m == 0 -> 0
     if ((lo & 0x8080808080808080ull) | (b8 & 0x80)) viol |= kDomainBad;
     return pack_ascii(lo, b8);
   } else {
     int m = len < 4 ? (int)len : 4;
-    uint64_t lo = 0;
-    if (m > 0) {
-      uintptr_t a = (uintptr_t)((const uint16_t *)units + o0);
-      const uint64_t *w = (const uint64_t *)(a & ~(uintptr_t)7);
-      int sh = (int)(a & 7);
-      uint64_t w0 = __ldg(w);
-      uint64_t w1 = (sh + 2 * m > 8) ? __ldg(w + 1) : 0ull;
-      lo = sh ? ((w0 >> (8 * sh)) | (w1 << (64 - 8 * sh))) : w0;
-      if (m < 4) lo &= (1ull << (16 * m)) - 1;
-    }
+    if (m < 4) lo &= (1ull << (16 * m)) - 1;
     // units u0..u3 little-endian in lo -> (u0<<48 | u1<<32 | u2<<16 | u3) >> 1
     uint64_t be = ((uint64_t)__byte_perm((uint32_t)lo, 0, 0x1032) << 32) |
                   (uint64_t)__byte_perm((uint32_t)(lo >> 32), 0, 0x1032);
@@ -78,6 +64,16 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
   }
   uint32_t viol = 0;
   const uint32_t lane = lane_id();
+  constexpr int W = CoderTraits<CODER>::kUnitBytes;
+  // Every word load is clamped into [lo_word, hi_word], the aligned words that
+  // cover units[offsets[0] .. offsets[n]); for valid offsets the words a window
+  // needs are always inside, so the loads can be issued unconditionally (all
+  // items' loads in flight at once) without ever leaving the caller's buffer.
+  const uintptr_t ub = (uintptr_t)units;
+  const int64_t ofirst = __ldg(offsets), olast = __ldg(offsets + n);
+  const bool any_units = olast > ofirst;
+  const uintptr_t lo_word = (ub + (uintptr_t)(ofirst * W)) & ~(uintptr_t)7;
+  const uintptr_t hi_word = any_units ? ((ub + (uintptr_t)(olast * W) - 1) & ~(uintptr_t)7) : lo_word;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kEncItems;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * kEncItems; base < n; base += stride) {
     int64_t o0[kEncItems], o1[kEncItems];
@@ -85,11 +81,28 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
     for (int k = 0; k < kEncItems; ++k) {
       uint64_t i = base + threadIdx.x + (uint64_t)k * blockDim.x;
       if (i < n) { o0[k] = __ldg(offsets + i); o1[k] = __ldg(offsets + i + 1); }
-      else { o0[k] = 0; o1[k] = 0; }
+      else { o0[k] = ofirst; o1[k] = ofirst; }
+    }
+    uint64_t w0[kEncItems], w1[kEncItems];
+    int sh[kEncItems];
+#pragma unroll
+    for (int k = 0; k < kEncItems; ++k) {
+      uintptr_t a = ub + (uintptr_t)(o0[k] * W);
+      sh[k] = (int)(a & 7);
+      uintptr_t aw = a & ~(uintptr_t)7;
+      aw = aw < lo_word ? lo_word : (aw > hi_word ? hi_word : aw);
+      uintptr_t aw1 = aw + 8 > hi_word ? hi_word : aw + 8;
+      if (any_units) {
+        w0[k] = __ldg((const uint64_t *)aw);
+        w1[k] = __ldg((const uint64_t *)aw1);
+      } else {
+        w0[k] = 0;
+        w1[k] = 0;
+      }
     }
     uint64_t code[kEncItems];
 #pragma unroll
-    for (int k = 0; k < kEncItems; ++k) code[k] = encode_one<CODER>(units, o0[k], o1[k] - o0[k], viol);
+    for (int k = 0; k < kEncItems; ++k) code[k] = encode_words<CODER>(w0[k], w1[k], sh[k], o1[k] - o0[k], viol);
 #pragma unroll
     for (int k = 0; k < kEncItems; ++k) {
       uint64_t i = base + threadIdx.x + (uint64_t)k * blockDim.x;

@@ -146,13 +146,21 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
                                &sorted_codes))
     return e;
 
+  // ---- A4 gather in (code, index) order.  Done BEFORE the fix-up: the order
+  // check below then reads every run's strings contiguously instead of through
+  // a second random perm -> offsets -> units walk; only spans the fix-up
+  // reorders are gathered again (rare outside all-colliding inputs).
+  if (d_sorted_units)
+    launch_gather(coder, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),
+                  S.next_counter(), S.next_epoch(), s);
+
   // ---- A3 run detection + order check, classification
   uint32_t *run_start = S.at<uint32_t>(L.run_start), *run_end = S.at<uint32_t>(L.run_end);
   uint8_t *dirty = S.at<uint8_t>(L.dirty);
   uint2 *list_sm = S.at<uint2>(L.list_sm), *list_g = S.at<uint2>(L.list_g);
   HCHECK(cudaMemsetAsync(dirty, 0, L.cap_sm, s));
   launch_runs_scan(coder, 0, sorted_codes, n, d_perm, d_units, d_offsets, 0, run_start, run_end, dirty, st,
-                   S.lb_scan(), S.next_counter(), S.next_epoch(), s);
+                   S.lb_scan(), S.next_counter(), S.next_epoch(), s, d_sorted_units, d_sorted_offsets);
   launch_runs_classify(run_start, run_end, dirty, st, list_sm, L.cap_sm, list_g, true, S.sms, s);
   uint32_t n_giant = 0;
   HCHECK(cudaMemcpyAsync(&n_giant, &st->n_giant, 4, cudaMemcpyDeviceToHost, s));
@@ -162,10 +170,12 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // ---- A6 giant-run refinement (rare: runs > 4096 strings with an inversion)
   struct Seg { uint32_t start, len, from; };
   std::vector<Seg> queue;
+  std::vector<uint2> giant_spans;  // top-level giant runs: re-gathered at the end
   if (n_giant) {
     std::vector<uint2> g(n_giant);
     HCHECK(cudaMemcpy(g.data(), list_g, n_giant * sizeof(uint2), cudaMemcpyDeviceToHost));
     for (auto &x : g) queue.push_back({x.x, x.y, (uint32_t)(coder == HUSKY_CODER_ASCII ? 9 : 3)});
+    giant_spans = g;
   }
   const uint32_t win = coder == HUSKY_CODER_ASCII ? 7 : 3;
   for (size_t qi = 0; qi < queue.size(); ++qi) {
@@ -210,10 +220,14 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   launch_fix_small(coder, list_sm, st, d_perm, d_units, d_offsets, S.sms, s);
   launch_fix_medium(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s);
 
-  // ---- A4 gather
-  if (d_sorted_units)
-    launch_gather(coder, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),
-                  S.next_counter(), S.next_epoch(), s);
+  // ---- A4 (again) for the spans whose order the fix-up changed
+  if (d_sorted_units) {
+    launch_regather_runs(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, d_sorted_units,
+                         d_sorted_offsets, S.sms, s);
+    for (auto &g : giant_spans)
+      launch_gather(coder, d_perm + g.x, g.y, d_units, d_offsets, d_sorted_units, d_sorted_offsets + g.x,
+                    S.lb_scan(), S.next_counter(), S.next_epoch(), s, d_sorted_offsets + g.x);
+  }
 
   DevState hs;
   HCHECK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, s));

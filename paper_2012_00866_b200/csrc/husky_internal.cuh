@@ -184,6 +184,17 @@ __device__ __forceinline__ int cmp_units_from(const void *units, int64_t oa, int
 // length, then index); otherwise units [0, S) are equal and the comparison
 // starts at unit `from` (>= S when the caller knows a longer common prefix).
 template <int CODER>
+__device__ __forceinline__ int cmp_equal_code_ol(const void *units, int64_t oa, int64_t la, uint32_t ia,
+                                                 int64_t ob, int64_t lb, uint32_t ib, int64_t from) {
+  using T = CoderTraits<CODER>;
+  int c;
+  if (la <= T::kPL || lb <= T::kPL) c = (la < lb) ? -1 : (la > lb ? 1 : 0);
+  else c = cmp_units_from<CODER>(units, oa, la, ob, lb, from);
+  if (c) return c;
+  return ia < ib ? -1 : (ia > ib ? 1 : 0);
+}
+
+template <int CODER>
 __device__ __forceinline__ int cmp_equal_code(const void *units, const int64_t *offsets, uint32_t ia,
                                               uint32_t ib, int64_t from) {
   using T = CoderTraits<CODER>;

@@ -7,12 +7,16 @@
 namespace husky {
 
 // A1 encode
-constexpr int kEncThreads = 512, kEncItems = 4, kEncBlocksPerSM = 2;
+constexpr int kEncThreads = 512, kEncItems = 4, kEncBlocksPerSM = 3;
 void launch_encode(int coder, bool hist, const void *units, const int64_t *offsets, uint64_t n,
                    uint64_t *codes, DevState *st, int num_sms, cudaStream_t s);
 
 // A2 onesweep radix
-constexpr int kRadixThreads = 256, kRadixItems = 16, kRadixTile = kRadixThreads * kRadixItems;
+// 256 threads x 8 keys = 2048-key tiles, 24 KB smem, <= 64 registers -> 4 CTAs
+// (32 warps) per SM so the key loads and the look-back of one tile overlap the
+// ranking of others.
+constexpr int kRadixThreads = 256, kRadixItems = 8, kRadixTile = kRadixThreads * kRadixItems;
+constexpr int kRadixMinBlocks = 4;
 inline uint64_t radix_tiles(uint64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
 void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s);
 // One stable LSD pass on digit `digit` (bits 8*digit..8*digit+7).  vals_in == NULL
@@ -31,7 +35,8 @@ inline uint64_t scan_tiles(uint64_t n) { return (n + kScanTile - 1) / kScanTile;
 void launch_runs_scan(int coder, int mode, const uint64_t *keys, uint64_t n, const uint32_t *perm,
                       const void *units, const int64_t *offsets, uint32_t base, uint32_t *run_start,
                       uint32_t *run_end, uint8_t *dirty, DevState *st, unsigned long long *lb,
-                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
+                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s,
+                      const void *sorted_units = nullptr, const int64_t *sorted_offsets = nullptr);
 void launch_runs_classify(const uint32_t *run_start, const uint32_t *run_end, const uint8_t *dirty,
                           DevState *st, uint2 *list_sm, uint64_t cap_sm, uint2 *list_g,
                           bool count_stats, int num_sms, cudaStream_t s);
@@ -54,8 +59,14 @@ void launch_seg_key2(int coder, const uint32_t *perm_seg, uint64_t len, const vo
 constexpr int kGatherThreads = 256, kGatherItems = 4, kGatherTile = kGatherThreads * kGatherItems;
 constexpr int kGatherStage = 32 * 1024;
 inline uint64_t gather_tiles(uint64_t n) { return (n + kGatherTile - 1) / kGatherTile; }
+// base_ptr (nullable): device pointer to the first output offset of a span
+// re-gather (positions start there); NULL = 0.
 void launch_gather(int coder, const uint32_t *perm, uint64_t n, const void *units,
                    const int64_t *offsets, void *sorted_units, int64_t *sorted_offsets,
-                   unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
+                   unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s,
+                   const int64_t *base_ptr = nullptr);
+void launch_regather_runs(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
+                          const uint32_t *perm, const void *units, const int64_t *offsets,
+                          void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s);
 
 }  // namespace husky

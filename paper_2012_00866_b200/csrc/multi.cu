@@ -249,7 +249,7 @@ struct Plan {
     HCHECK(cudaMemsetAsync(st(), 0, sizeof(DevState), s));
     HCHECK(S.reset_lookback());
     launch_encode(coder, false, units, offsets, n, at<uint64_t>(M.L.keysA), st(), S.sms, s);
-    { Scope sc_(ST_MULTI, s, 0); }
+    HUSKY_SCOPE(ST_MULTI, s, 0);
     k_sample<<<1, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, at<uint64_t>(M.samples) + (size_t)rank * kSampleStride,
                                st());
     HCHECK(cudaGetLastError());
@@ -287,7 +287,7 @@ struct Plan {
     HCHECK(cudaMemsetAsync(st()->hist, 0, sizeof(st()->hist), s));
     if (n) {
       unsigned blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)S.sms * 4);
-      { Scope sc_(ST_MULTI, s, 0); }
+      HUSKY_SCOPE(ST_MULTI, s, 0);
       k_bucket<<<blocks, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, at<uint64_t>(M.splitters), world - 1, world,
                                       offsets, at<uint64_t>(M.L.keysB), st(), at<unsigned long long>(M.counts));
       launch_hist_scan(n, st(), s);
@@ -320,7 +320,7 @@ struct Plan {
     if (husky_status e = S.radix(at<uint64_t>(M.L.keysB), nullptr, n, 0xFEu, at<uint32_t>(M.send_perm),
                                  at<uint32_t>(M.L.vals), &sorted_keys))
       return e;
-    { Scope sc_(ST_MULTI, s, 0); }
+    HUSKY_SCOPE(ST_MULTI, s, 0);
     k_send_meta<<<grid_for(n), 256, 0, s>>>(at<uint32_t>(M.send_perm), n, offsets, (uint32_t)gbase,
                                             at<uint32_t>(M.send_gidx), at<uint32_t>(M.send_lens));
     launch_gather(coder, at<uint32_t>(M.send_perm), n, units, offsets, at<void>(M.send_units),
@@ -339,16 +339,27 @@ struct Plan {
     }
     HCHECK(cudaMemsetAsync(rws + R.lb, 0, scan_tiles(n_out) * 8 + 8, s));
     HCHECK(cudaMemsetAsync(&st()->tile_counter[63], 0, 4, s));
-    { Scope sc_(ST_MULTI, s, 0); }
+    HUSKY_SCOPE(ST_MULTI, s, 0);
     k_lens_to_offsets<<<(unsigned)scan_tiles(n_out), kScanThreads, 0, s>>>(
         (const uint32_t *)(rws + R.lens), n_out, (int64_t *)(rws + R.offsets), (unsigned long long *)(rws + R.lb),
         &st()->tile_counter[63], 1, 0);
     HCHECK(cudaGetLastError());
+    if (debug_sync()) {
+      int64_t ends[2] = {-1, -1};
+      uint32_t l0[4] = {0, 0, 0, 0};
+      HCHECK(cudaStreamSynchronize(s));
+      HCHECK(cudaMemcpy(&ends[0], rws + R.offsets, 8, cudaMemcpyDeviceToHost));
+      HCHECK(cudaMemcpy(&ends[1], (int64_t *)(rws + R.offsets) + n_out, 8, cudaMemcpyDeviceToHost));
+      HCHECK(cudaMemcpy(l0, rws + R.lens, 16, cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[husky] rank %d recv n=%llu units=%llu offsets[0]=%lld offsets[n]=%lld lens %u %u %u %u\n",
+              rank, (unsigned long long)n_out, (unsigned long long)units_out, (long long)ends[0],
+              (long long)ends[1], l0[0], l0[1], l0[2], l0[3]);
+    }
     husky_status e = sort_impl(coder, rws + R.units, (const int64_t *)(rws + R.offsets), n_out, d_perm_out,
                                d_sorted_units_out, d_sorted_offsets_out, rws + R.sort_ws,
                                make_layout(n_out).total, h_out, s);
     if (e) return e;
-    { Scope sc_(ST_MULTI, s, 0); }
+    HUSKY_SCOPE(ST_MULTI, s, 0);
     k_remap<<<grid_for(n_out), 256, 0, s>>>(d_perm_out, n_out, (const uint32_t *)(rws + R.gidx));
     HCHECK(cudaGetLastError());
     return HUSKY_OK;
@@ -675,9 +686,10 @@ husky_status husky_sort_multi_loopback(int coder, int world, const void *d_units
     int64_t *so_out = (d_sorted_offsets && dst.n_out) ? d_sorted_offsets + out_n : nullptr;
     // offsets slot out_n is shared with the previous shard's end: write it first
     if (husky_status e = dst.phase4(rws_all, R, d_perm + out_n, su_out, so_out, &o)) return e;
-    if (so_out && out_u && dst.n_out)
-      { Scope sc_(ST_MULTI, s, 0); }
+    if (so_out && out_u && dst.n_out) {
+      HUSKY_SCOPE(ST_MULTI, s, 0);
       k_add_base<<<grid_for(dst.n_out + 1), 256, 0, s>>>(so_out, dst.n_out + 1, (int64_t)out_u);
+    }
     if (h_shard_n) h_shard_n[r] = dst.n_out;
     agg.perfect &= o.perfect; agg.domain_ok &= o.domain_ok;
     agg.n_runs += o.n_runs; agg.n_in_runs += o.n_in_runs;

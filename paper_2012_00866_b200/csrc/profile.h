@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -53,6 +55,14 @@ struct Profiler {
 
 Profiler &profiler();
 
+inline bool debug_sync() {
+  static const bool on = [] {
+    const char *v = getenv("HUSKY_DEBUG_SYNC");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 struct Scope {
   int stage;
   cudaStream_t s;
@@ -70,6 +80,13 @@ struct Scope {
     }
   }
   ~Scope() {
+    if (debug_sync()) {  // HUSKY_DEBUG_SYNC=1: localise device faults per launch
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess)
+        fprintf(stderr, "[husky] device error after stage %d launch (%llu elems): %s\n", stage,
+                (unsigned long long)elems, cudaGetErrorString(e));
+    }
     if (!a) return;
     Profiler &P = profiler();
     std::lock_guard<std::mutex> g(P.mu);
@@ -78,5 +95,9 @@ struct Scope {
     P.pending.push_back({stage, a, b, elems});
   }
 };
+
+#define HUSKY_CAT2(a, b) a##b
+#define HUSKY_CAT(a, b) HUSKY_CAT2(a, b)
+#define HUSKY_SCOPE(stage, stream, elems) ::husky::Scope HUSKY_CAT(husky_scope_, __COUNTER__)(stage, stream, elems)
 
 }  // namespace husky

@@ -42,7 +42,7 @@ constexpr int kRadixWarps = kRadixThreads / 32;
 constexpr int kExchangeBytes = kRadixTile * (8 + 4);
 
 template <bool SYNTH_VALS>
-__global__ void __launch_bounds__(kRadixThreads, 2)
+__global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     k_onesweep(const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint64_t n, int shift,
                const uint32_t *__restrict__ digit_start, unsigned long long *lb, uint32_t *tile_counter,

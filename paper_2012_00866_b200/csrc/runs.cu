@@ -23,7 +23,8 @@ __global__ void __launch_bounds__(kScanThreads)
     k_runs_scan(const uint64_t *__restrict__ keys, uint64_t n, const uint32_t *__restrict__ perm,
                 const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t base,
                 uint32_t *__restrict__ run_start, uint32_t *__restrict__ run_end, uint8_t *__restrict__ dirty,
-                DevState *st, unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch) {
+                DevState *st, unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch,
+                const void *__restrict__ sunits, const int64_t *__restrict__ soffs) {
   using T = CoderTraits<CODER>;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_wt[kScanThreads / 32 + 1];
@@ -85,6 +86,11 @@ __global__ void __launch_bounds__(kScanThreads)
       bool bad;
       if (MODE == 0) {
         bad = cmp_equal_code<CODER>(units, offsets, __ldg(perm + p), __ldg(perm + p + 1), T::kS) > 0;
+      } else if (MODE == 2) {
+        // strings already gathered in sorted order: contiguous reads
+        int64_t oa = __ldg(soffs + p), ob = __ldg(soffs + p + 1), oe = __ldg(soffs + p + 2);
+        bad = cmp_equal_code_ol<CODER>(sunits, oa, ob - oa, __ldg(perm + p), ob, oe - ob, __ldg(perm + p + 1),
+                                       T::kS) > 0;
       } else {
         constexpr uint64_t tagmask = CODER == HUSKY_CODER_ASCII ? 0xFFull : 0xFFFFull;
         bad = (c[j + 1] & tagmask) == (uint64_t)(16 + T::kTagCap);
@@ -97,16 +103,21 @@ __global__ void __launch_bounds__(kScanThreads)
 void launch_runs_scan(int coder, int mode, const uint64_t *keys, uint64_t n, const uint32_t *perm,
                       const void *units, const int64_t *offsets, uint32_t base, uint32_t *run_start,
                       uint32_t *run_end, uint8_t *dirty, DevState *st, unsigned long long *lb,
-                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s) {
+                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, const void *sunits,
+                      const int64_t *soffs) {
   if (n == 0) return;
   Scope sc_(ST_RUNS_SCAN, s, n);
   dim3 g((unsigned)scan_tiles(n)), b(kScanThreads);
-#define RS_ARGS keys, n, perm, units, offsets, base, run_start, run_end, dirty, st, lb, tile_counter, epoch
+#define RS_ARGS \
+  keys, n, perm, units, offsets, base, run_start, run_end, dirty, st, lb, tile_counter, epoch, sunits, soffs
+  if (mode == 0 && sunits) mode = 2;
   if (coder == HUSKY_CODER_ASCII) {
     if (mode == 0) k_runs_scan<HUSKY_CODER_ASCII, 0><<<g, b, 0, s>>>(RS_ARGS);
+    else if (mode == 2) k_runs_scan<HUSKY_CODER_ASCII, 2><<<g, b, 0, s>>>(RS_ARGS);
     else k_runs_scan<HUSKY_CODER_ASCII, 1><<<g, b, 0, s>>>(RS_ARGS);
   } else {
     if (mode == 0) k_runs_scan<HUSKY_CODER_UNICODE, 0><<<g, b, 0, s>>>(RS_ARGS);
+    else if (mode == 2) k_runs_scan<HUSKY_CODER_UNICODE, 2><<<g, b, 0, s>>>(RS_ARGS);
     else k_runs_scan<HUSKY_CODER_UNICODE, 1><<<g, b, 0, s>>>(RS_ARGS);
   }
 #undef RS_ARGS

@@ -1,0 +1,103 @@
+"""The N>1 sample-sort path on CPU: world_size-2 gloo process groups.
+
+The data-path kernels need a GPU, so here the per-rank steps that run on the
+device are stood in for by the oracle (test infrastructure), while the
+cross-rank logic is exercised for real across processes: regular sampling (the
+k_sample rule codes[i*n/s]), the library's host splitter selection
+(husky_select_splitters, C ABI), bucket = #splitters <= code, the count
+exchange, the string exchange in source-rank order, and the rank-order
+concatenation.  Checks: concatenation == oracle global sort; no equal-code run
+straddles ranks; shard sizes add up.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+S = 4096  # kSamplesPerRank in csrc/multi.cu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, name, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import paper_2012_00866_b200 as h
+        import workloads as W
+        wl = W.make(name, n) if name != "empty_rank" else W.make("C1", n)
+        N = wl.n
+        base = [0, N] if name == "empty_rank" else [N * r // world for r in range(world + 1)]
+        if name == "empty_rank":
+            base = [0] + [N] * world  # rank 0 holds everything, the others nothing
+        lo, hi = base[rank], base[rank + 1]
+        off = wl.offsets[lo:hi + 1]
+        units = wl.units
+        codes, _ = oracle.encode(wl.coder, units, off) if hi > lo else (np.zeros(0, np.uint64), True)
+        nl = hi - lo
+        smp = np.array([codes[i * nl // S] for i in range(S)] if nl else [2**64 - 1] * S, dtype=np.uint64)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, smp)
+        allsmp = np.concatenate(gathered)
+        allsmp = allsmp[allsmp != np.uint64(2**64 - 1)]
+        spl = h.husky_select_splitters(allsmp, world)
+        bucket = np.searchsorted(spl, codes, side="right")
+        # stable partition -> per destination (units, lengths, global indices)
+        send = []
+        for d in range(world):
+            idx = np.nonzero(bucket == d)[0]
+            strs = [units[off[i]:off[i + 1]] for i in idx]
+            send.append((strs, (lo + idx).astype(np.int64)))
+        recv = [None] * world
+        for src in range(world):
+            obj = [send] if src == rank else [None]
+            dist.broadcast_object_list(obj, src=src)
+            recv[src] = obj[0][rank]
+        strs = [s for r in recv for s in r[0]]
+        gidx = np.concatenate([r[1] for r in recv]) if strs else np.zeros(0, np.int64)
+        assert np.all(np.diff(gidx) > 0)  # source-rank order == ascending global index
+        lw = W.from_strings([list(s) for s in strs], wl.coder)
+        lperm = oracle.sort(wl.coder, lw.units, lw.offsets) if strs else np.zeros(0, np.uint32)
+        shard = gidx[lperm] if strs else np.zeros(0, np.int64)
+        shard_codes = codes[0:0]
+        if strs:
+            shard_codes, _ = oracle.encode(wl.coder, lw.units, lw.offsets)
+            shard_codes = shard_codes[lperm]
+        out = [None] * world
+        dist.all_gather_object(out, (shard, shard_codes))
+        if rank == 0:
+            cat = np.concatenate([o[0] for o in out])
+            ref = oracle.sort(wl.coder, wl.units, wl.offsets).astype(np.int64)
+            ok = np.array_equal(cat, ref)
+            straddle = any(len(out[r][1]) and len(out[r + 1][1]) and out[r][1][-1] == out[r + 1][1][0]
+                           for r in range(world - 1))
+            q.put((ok, straddle, [len(o[0]) for o in out]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,n", [("C1", 30_000), ("C3", 30_000), ("C4", 5_000), ("empty_rank", 5_000)])
+def test_sample_sort_world2_gloo(name, n):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, name, n, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(300)
+        assert p.exitcode == 0
+    ok, straddle, sizes = q.get(timeout=10)
+    assert ok, "concatenation of shards != oracle global sort"
+    assert not straddle, "an equal-code run straddles two ranks"
+    assert sum(sizes) == n
