@@ -56,8 +56,11 @@ __device__ __forceinline__ uint64_t encode_words(uint64_t w0, uint64_t w1, int s
 template <int CODER, bool HIST>
 __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__ units,
                                                         const int64_t *__restrict__ offsets, uint64_t n,
-                                                        uint64_t *__restrict__ codes, DevState *st) {
+                                                        uint64_t *__restrict__ codes, DevState *st,
+                                                        uint32_t *__restrict__ packed) {
   __shared__ uint32_t sh_hist[HIST ? 8 * 256 : 1];
+  __shared__ int64_t s_off[kEncTile + 1];
+  __shared__ uint64_t s_stage[kEncStageWords + 2];
   if (HIST) {
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) sh_hist[i] = 0;
     __syncthreads();
@@ -65,23 +68,35 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
   uint32_t viol = 0;
   const uint32_t lane = lane_id();
   constexpr int W = CoderTraits<CODER>::kUnitBytes;
-  // Every word load is clamped into [lo_word, hi_word], the aligned words that
-  // cover units[offsets[0] .. offsets[n]); for valid offsets the words a window
-  // needs are always inside, so the loads can be issued unconditionally (all
-  // items' loads in flight at once) without ever leaving the caller's buffer.
+  // Global word loads (fallback path) are clamped into [lo_word, hi_word], the
+  // aligned words that cover units[offsets[0] .. offsets[n]): for valid offsets
+  // the words a window needs are always inside, so they can be issued
+  // unconditionally without ever leaving the caller's buffer.
   const uintptr_t ub = (uintptr_t)units;
   const int64_t ofirst = __ldg(offsets), olast = __ldg(offsets + n);
   const bool any_units = olast > ofirst;
   const uintptr_t lo_word = (ub + (uintptr_t)(ofirst * W)) & ~(uintptr_t)7;
   const uintptr_t hi_word = any_units ? ((ub + (uintptr_t)(olast * W) - 1) & ~(uintptr_t)7) : lo_word;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kEncItems;
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * kEncItems; base < n; base += stride) {
+  for (uint64_t base = (uint64_t)blockIdx.x * kEncTile; base < n; base += (uint64_t)gridDim.x * kEncTile) {
+    // ---- stage the tile: its offsets, then its contiguous unit span, with
+    // fully coalesced loads (each byte of the span is read once)
+    const uint32_t cnt = (uint32_t)((n - base) < (uint64_t)kEncTile ? (n - base) : kEncTile);
+    for (uint32_t i = threadIdx.x; i <= cnt; i += blockDim.x) s_off[i] = __ldg(offsets + base + i);
+    __syncthreads();
+    const int64_t tstart = s_off[0], tend = s_off[cnt];
+    const uintptr_t aw0 = (ub + (uintptr_t)(tstart * W)) & ~(uintptr_t)7;
+    const int64_t nwords = tend > tstart ? (int64_t)(((ub + (uintptr_t)(tend * W)) - aw0 + 7) >> 3) : 0;
+    const bool staged = nwords <= kEncStageWords;
+    if (staged)
+      for (int64_t wd = threadIdx.x; wd < nwords; wd += blockDim.x) s_stage[wd] = __ldg((const uint64_t *)aw0 + wd);
+    __syncthreads();
+
     int64_t o0[kEncItems], o1[kEncItems];
 #pragma unroll
     for (int k = 0; k < kEncItems; ++k) {
-      uint64_t i = base + threadIdx.x + (uint64_t)k * blockDim.x;
-      if (i < n) { o0[k] = __ldg(offsets + i); o1[k] = __ldg(offsets + i + 1); }
-      else { o0[k] = ofirst; o1[k] = ofirst; }
+      uint32_t li = threadIdx.x + k * blockDim.x;
+      if (li < cnt) { o0[k] = s_off[li]; o1[k] = s_off[li + 1]; }
+      else { o0[k] = tstart; o1[k] = tstart; }
     }
     uint64_t w0[kEncItems], w1[kEncItems];
     int sh[kEncItems];
@@ -89,10 +104,14 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
     for (int k = 0; k < kEncItems; ++k) {
       uintptr_t a = ub + (uintptr_t)(o0[k] * W);
       sh[k] = (int)(a & 7);
-      uintptr_t aw = a & ~(uintptr_t)7;
-      aw = aw < lo_word ? lo_word : (aw > hi_word ? hi_word : aw);
-      uintptr_t aw1 = aw + 8 > hi_word ? hi_word : aw + 8;
-      if (any_units) {
+      if (staged && o0[k] >= tstart && o1[k] <= tend && o0[k] <= o1[k]) {
+        uint64_t rel = (uint64_t)((a & ~(uintptr_t)7) - aw0) >> 3;
+        w0[k] = s_stage[rel];
+        w1[k] = s_stage[rel + 1];
+      } else if (any_units) {  // long spans or invalid offsets: clamped global loads
+        uintptr_t aw = a & ~(uintptr_t)7;
+        aw = aw < lo_word ? lo_word : (aw > hi_word ? hi_word : aw);
+        uintptr_t aw1 = aw + 8 > hi_word ? hi_word : aw + 8;
         w0[k] = __ldg((const uint64_t *)aw);
         w1[k] = __ldg((const uint64_t *)aw1);
       } else {
@@ -106,8 +125,15 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
 #pragma unroll
     for (int k = 0; k < kEncItems; ++k) {
       uint64_t i = base + threadIdx.x + (uint64_t)k * blockDim.x;
-      bool valid = i < n;
-      if (valid) codes[i] = code[k];
+      bool valid = threadIdx.x + k * blockDim.x < cnt;
+      if (valid) {
+        codes[i] = code[k];
+        // initial radix payload: index | min(len, 15) << 28 (n <= 2^28 only)
+        if (packed) {
+          int64_t L = o1[k] - o0[k];
+          packed[i] = (uint32_t)i | ((uint32_t)(L < 0 ? 0 : (L > 15 ? 15 : L)) << 28);
+        }
+      }
       if (HIST) {
         uint32_t vmask = __ballot_sync(0xFFFFFFFFu, valid);
         if (vmask == 0) continue;
@@ -124,6 +150,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
         }
       }
     }
+    __syncthreads();  // s_off / s_stage are reused by the next tile
   }
   // reduce violation bits: one atomic per warp that saw any
   viol = __reduce_or_sync(0xFFFFFFFFu, viol);
@@ -137,20 +164,19 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
 }
 
 void launch_encode(int coder, bool hist, const void *units, const int64_t *offsets, uint64_t n,
-                   uint64_t *codes, DevState *st, int num_sms, cudaStream_t s) {
+                   uint64_t *codes, DevState *st, int num_sms, cudaStream_t s, uint32_t *packed) {
   if (n == 0) return;
   Scope sc_(ST_ENCODE, s, n);
-  uint64_t per_block = (uint64_t)kEncThreads * kEncItems;
-  uint64_t blocks = (n + per_block - 1) / per_block;
+  uint64_t blocks = (n + kEncTile - 1) / kEncTile;
   uint64_t cap = (uint64_t)num_sms * kEncBlocksPerSM;
   if (blocks > cap) blocks = cap;
   dim3 g((unsigned)blocks), b(kEncThreads);
   if (coder == HUSKY_CODER_ASCII) {
-    if (hist) k_encode<HUSKY_CODER_ASCII, true><<<g, b, 0, s>>>(units, offsets, n, codes, st);
-    else k_encode<HUSKY_CODER_ASCII, false><<<g, b, 0, s>>>(units, offsets, n, codes, st);
+    if (hist) k_encode<HUSKY_CODER_ASCII, true><<<g, b, 0, s>>>(units, offsets, n, codes, st, packed);
+    else k_encode<HUSKY_CODER_ASCII, false><<<g, b, 0, s>>>(units, offsets, n, codes, st, packed);
   } else {
-    if (hist) k_encode<HUSKY_CODER_UNICODE, true><<<g, b, 0, s>>>(units, offsets, n, codes, st);
-    else k_encode<HUSKY_CODER_UNICODE, false><<<g, b, 0, s>>>(units, offsets, n, codes, st);
+    if (hist) k_encode<HUSKY_CODER_UNICODE, true><<<g, b, 0, s>>>(units, offsets, n, codes, st, packed);
+    else k_encode<HUSKY_CODER_UNICODE, false><<<g, b, 0, s>>>(units, offsets, n, codes, st, packed);
   }
 }
 

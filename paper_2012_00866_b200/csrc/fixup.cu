@@ -51,6 +51,10 @@ __global__ void __launch_bounds__(1024)
   for (uint32_t e = blockIdx.x; e < nmed; e += gridDim.x) {
     uint2 ent = list[cap - 1 - e];
     const uint32_t start = ent.x, len = ent.y;
+#ifdef HUSKY_TRACE
+    if (threadIdx.x == 0) printf("[husky trace] fix_medium entry %u/%u: start %u len %u cap %llu\n", e, nmed, start, len,
+                                 (unsigned long long)cap);
+#endif
     uint32_t P = 1;
     while (P < len) P <<= 1;
     for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < len ? perm[start + i] : 0xFFFFFFFFu;

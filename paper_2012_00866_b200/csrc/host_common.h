@@ -16,7 +16,7 @@ namespace husky {
 // Workspace layout of husky_sort for n strings (byte offsets, 256-aligned).
 struct Layout {
   uint64_t n = 0, tiles_r = 0, tiles_s = 0, cap_sm = 0, cap_g = 0;
-  size_t state = 0, keysA = 0, keysB = 0, vals = 0, lb_radix = 0, lb_scan = 0, run_start = 0,
+  size_t state = 0, keysA = 0, keysB = 0, vals = 0, vals2 = 0, lb_radix = 0, lb_scan = 0, run_start = 0,
          run_end = 0, dirty = 0, list_sm = 0, list_g = 0, total = 0;
 };
 Layout make_layout(uint64_t n);

@@ -64,6 +64,7 @@ Layout make_layout(uint64_t n) {
   L.keysA = take(n * 8);
   L.keysB = take(n * 8);
   L.vals = take(n * 4);
+  L.vals2 = take(n * 4);  // packed initial payload (index | len << 28) when n <= 2^28
   L.lb_radix = take(L.tiles_r * 256 * 8);
   L.lb_scan = take(L.tiles_s * 8);
   L.run_start = take(L.cap_sm * 4);
@@ -73,6 +74,32 @@ Layout make_layout(uint64_t n) {
   L.list_g = take(L.cap_g * 8);
   L.total = off;
   return L;
+}
+
+// HUSKY_DEBUG_SYNC only: verify that perm[0..n) is a permutation (bitmap count)
+__global__ void k_debug_perm(const uint32_t *perm, uint64_t n, uint32_t *bitmap, unsigned long long *bad) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t v = perm[i];
+    if (v >= n) { atomicAdd(bad, 1ull); continue; }
+    uint32_t old = atomicOr(&bitmap[v >> 5], 1u << (v & 31));
+    if (old & (1u << (v & 31))) atomicAdd(bad, 1ull);
+  }
+}
+
+static void debug_check_perm(const uint32_t *perm, uint64_t n, const char *tag, cudaStream_t s) {
+  if (!debug_sync()) return;
+  uint32_t *bm = nullptr;
+  unsigned long long *bad = nullptr, hb = 0;
+  cudaStreamSynchronize(s);
+  cudaMalloc(&bm, (n / 32 + 1) * 4);
+  cudaMalloc(&bad, 8);
+  cudaMemset(bm, 0, (n / 32 + 1) * 4);
+  cudaMemset(bad, 0, 8);
+  k_debug_perm<<<1024, 256>>>(perm, n, bm, bad);
+  cudaMemcpy(&hb, bad, 8, cudaMemcpyDeviceToHost);
+  if (hb) fprintf(stderr, "[husky] perm check after %s: %llu bad entries (n=%llu)\n", tag, hb, (unsigned long long)n);
+  cudaFree(bm);
+  cudaFree(bad);
 }
 
 struct HostSnap {  // small prefix of DevState read back at sync points
@@ -130,7 +157,11 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   HCHECK(S.reset_lookback());
 
   // ---- A1 encode (+ digit histograms, flags) and the histogram scan
-  launch_encode(coder, true, d_units, d_offsets, n, S.keysA(), st, S.sms, s);
+  // n <= 2^28: the payload carries min(len, 15) in its top 4 bits, so the
+  // gather rebuilds strings of length <= PL from their code (no random reads)
+  const bool packed = n <= kPackMaxN;
+  uint32_t *packed_payload = packed ? S.at<uint32_t>(L.vals2) : nullptr;
+  launch_encode(coder, true, d_units, d_offsets, n, S.keysA(), st, S.sms, s, packed_payload);
   launch_hist_scan(n, st, s);
   HostSnap snap;
   HCHECK(cudaMemcpyAsync(&snap, &st->trivial_mask, sizeof snap, cudaMemcpyDeviceToHost, s));
@@ -142,9 +173,10 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
 
   // ---- A2 key sort: (code, index) -> sorted codes, perm
   uint64_t *sorted_codes = nullptr;
-  if (husky_status e = S.radix(S.keysA(), nullptr, n, snap.trivial_mask, d_perm, S.at<uint32_t>(L.vals),
+  if (husky_status e = S.radix(S.keysA(), packed_payload, n, snap.trivial_mask, d_perm, S.at<uint32_t>(L.vals),
                                &sorted_codes))
     return e;
+  if (packed && !d_sorted_units) launch_unpack_perm(d_perm, n, s);  // the gather unpacks otherwise
 
   // ---- A4 gather in (code, index) order.  Done BEFORE the fix-up: the order
   // check below then reads every run's strings contiguously instead of through
@@ -152,7 +184,8 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // reorders are gathered again (rare outside all-colliding inputs).
   if (d_sorted_units)
     launch_gather(coder, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),
-                  S.next_counter(), S.next_epoch(), s);
+                  S.next_counter(), S.next_epoch(), s, nullptr, packed ? sorted_codes : nullptr);
+  debug_check_perm(d_perm, n, "key sort", s);
 
   // ---- A3 run detection + order check, classification
   uint32_t *run_start = S.at<uint32_t>(L.run_start), *run_end = S.at<uint32_t>(L.run_end);
@@ -200,6 +233,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
     if (husky_status e = S.radix(S.keysA(), perm_seg, seg.len, snap.trivial_mask, perm_seg,
                                  S.at<uint32_t>(L.vals), &sorted_key2))
       return e;
+    debug_check_perm(d_perm, n, "refine radix", s);
     // sub-runs of equal key with tag == cap are still ambiguous
     HCHECK(cudaMemsetAsync(dirty, 0, seg.len / 2 + 1, s));
     HCHECK(cudaMemsetAsync(&st->n_giant, 0, 4, s));
@@ -219,14 +253,31 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // ---- A5 fix-up of small / medium dirty runs (counts read on device)
   launch_fix_small(coder, list_sm, st, d_perm, d_units, d_offsets, S.sms, s);
   launch_fix_medium(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s);
+  debug_check_perm(d_perm, n, "fix-up", s);
 
   // ---- A4 (again) for the spans whose order the fix-up changed
   if (d_sorted_units) {
-    launch_regather_runs(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, d_sorted_units,
-                         d_sorted_offsets, S.sms, s);
+    auto dbg_so = [&](const char *tag) {
+      if (!debug_sync()) return;
+      int64_t v[2] = {0, 0};
+      cudaStreamSynchronize(s);
+      cudaMemcpy(v, d_sorted_offsets, 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(v + 1, d_sorted_offsets + n, 8, cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[husky] %s: sorted_offsets[0]=%lld [n]=%lld giants=%zu first=(%u,%u)\n", tag, (long long)v[0],
+              (long long)v[1], giant_spans.size(), giant_spans.empty() ? 0u : giant_spans[0].x,
+              giant_spans.empty() ? 0u : giant_spans[0].y);
+    };
+    // Giant spans first: the refinement reordered them wholesale, so the
+    // offsets inside them (and hence the bases of the small/medium sub-runs it
+    // produced) are only valid after the whole span is gathered again.  The
+    // span's own base and length never change.
     for (auto &g : giant_spans)
       launch_gather(coder, d_perm + g.x, g.y, d_units, d_offsets, d_sorted_units, d_sorted_offsets + g.x,
                     S.lb_scan(), S.next_counter(), S.next_epoch(), s, d_sorted_offsets + g.x);
+    dbg_so("after giant re-gather");
+    launch_regather_runs(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, d_sorted_units,
+                         d_sorted_offsets, S.sms, s);
+    dbg_so("after run re-gather");
   }
 
   DevState hs;

@@ -98,6 +98,68 @@ __device__ __forceinline__ unsigned long long lookback(const unsigned long long 
   return excl;
 }
 
+// Windowed look-back for one value per thread: loads W predecessor words at
+// once (nearest first) and consumes them in order; an unpublished word stops
+// the window and is re-read.  One round trip covers up to W tiles.
+template <int W>
+__device__ __forceinline__ unsigned long long lookback_window(const unsigned long long *flags, uint32_t tile,
+                                                              uint32_t stride, uint32_t epoch) {
+  unsigned long long excl = 0;
+  int64_t j = (int64_t)tile - 1;
+  while (j >= 0) {
+    unsigned long long w[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+      w[q] = (j - q >= 0) ? ld_relaxed_u64(flags + (uint64_t)(j - q) * stride) : make_flag(kFlagInc, epoch, 0);
+    int used = 0;
+    bool done = false;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      if (done || used != q) break;
+      unsigned long long x = w[q];
+      bool ok = ((uint32_t)(x >> 54) & 0xFF) == epoch && (x & (3ull << 62)) != 0;
+      if (!ok) break;
+      excl += x & kValMask;
+      used = q + 1;
+      if ((x & (3ull << 62)) == kFlagInc) done = true;
+    }
+    if (done) break;
+    j -= used;
+  }
+  return excl;
+}
+
+// Warp-cooperative look-back (all 32 lanes call it): lane l reads the word of
+// tile (base - l); the nearest inclusive word ends the walk.  Returns the
+// exclusive prefix of `tile` in every lane.
+__device__ __forceinline__ unsigned long long warp_lookback(const unsigned long long *flags, uint32_t tile,
+                                                            uint32_t epoch) {
+  const uint32_t lane = threadIdx.x & 31;
+  unsigned long long excl = 0;
+  int64_t base = (int64_t)tile - 1;
+  while (base >= 0) {
+    int64_t j = base - (int64_t)lane;
+    unsigned long long x = j >= 0 ? ld_relaxed_u64(flags + j) : make_flag(kFlagInc, epoch, 0);
+    bool valid = ((uint32_t)(x >> 54) & 0xFF) == epoch && (x & (3ull << 62)) != 0;
+    bool inc = valid && (x & (3ull << 62)) == kFlagInc;
+    uint32_t vmask = __ballot_sync(0xFFFFFFFFu, valid), imask = __ballot_sync(0xFFFFFFFFu, inc);
+    uint32_t take;  // number of leading lanes consumed this round
+    bool stop;
+    uint32_t first_invalid = __ffs(~vmask) - 1;  // 32 if all valid (ffs(0) = 0 -> 0xFFFFFFFF -> wrap)
+    if (vmask == 0xFFFFFFFFu) first_invalid = 32;
+    uint32_t first_inc = imask ? (uint32_t)(__ffs(imask) - 1) : 32u;
+    if (first_inc < first_invalid) { take = first_inc + 1; stop = true; }
+    else { take = first_invalid; stop = false; }
+    unsigned long long v = lane < take ? (x & kValMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    excl += v;
+    if (stop) break;
+    base -= take;
+  }
+  return excl;
+}
+
 // Warp inclusive scan (Kogge-Stone over shuffles).
 template <typename T>
 __device__ __forceinline__ T warp_inclusive_scan(T v) {

@@ -7,9 +7,15 @@
 namespace husky {
 
 // A1 encode
-constexpr int kEncThreads = 512, kEncItems = 4, kEncBlocksPerSM = 3;
+// tile of 1024 strings per CTA iteration; its unit span (<= 16 KB) is staged in smem
+constexpr int kEncThreads = 256, kEncItems = 4, kEncTile = kEncThreads * kEncItems, kEncBlocksPerSM = 4;
+constexpr int kEncStageWords = 2048;
+// packed (nullable, n <= 2^28): also writes the initial radix payload
+// index | min(len, 15) << 28, so the gather knows short strings' lengths
+// without a random offsets read.
+constexpr uint64_t kPackMaxN = 1ull << 28;
 void launch_encode(int coder, bool hist, const void *units, const int64_t *offsets, uint64_t n,
-                   uint64_t *codes, DevState *st, int num_sms, cudaStream_t s);
+                   uint64_t *codes, DevState *st, int num_sms, cudaStream_t s, uint32_t *packed = nullptr);
 
 // A2 onesweep radix
 // 256 threads x 8 keys = 2048-key tiles, 24 KB smem, <= 64 registers -> 4 CTAs
@@ -61,10 +67,13 @@ constexpr int kGatherStage = 32 * 1024;
 inline uint64_t gather_tiles(uint64_t n) { return (n + kGatherTile - 1) / kGatherTile; }
 // base_ptr (nullable): device pointer to the first output offset of a span
 // re-gather (positions start there); NULL = 0.
-void launch_gather(int coder, const uint32_t *perm, uint64_t n, const void *units,
-                   const int64_t *offsets, void *sorted_units, int64_t *sorted_offsets,
-                   unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s,
-                   const int64_t *base_ptr = nullptr);
+// packed_codes (nullable): perm holds index | min(len,15) << 28; strings of
+// length <= PL are rebuilt from these sorted codes and perm is unpacked in place.
+void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, const int64_t *offsets,
+                   void *sorted_units, int64_t *sorted_offsets, unsigned long long *lb,
+                   uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, const int64_t *base_ptr = nullptr,
+                   const uint64_t *packed_codes = nullptr);
+void launch_unpack_perm(uint32_t *perm, uint64_t n, cudaStream_t s);
 void launch_regather_runs(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                           const uint32_t *perm, const void *units, const int64_t *offsets,
                           void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s);

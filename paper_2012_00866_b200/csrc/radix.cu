@@ -39,7 +39,7 @@ void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s) {
 }
 
 constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kExchangeBytes = kRadixTile * (8 + 4);
+constexpr int kExchangeBytes = kRadixTile * (8 + 4) + kRadixWarps * 256 * 4;
 
 template <bool SYNTH_VALS>
 __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
@@ -48,10 +48,10 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
                const uint32_t *__restrict__ digit_start, unsigned long long *lb, uint32_t *tile_counter,
                uint32_t epoch) {
   extern __shared__ __align__(16) uint8_t smem[];
-  // phase 1: per-warp digit counters [warps][256]; phase 2: key/value exchange
-  uint32_t *cnt = reinterpret_cast<uint32_t *>(smem);
+  // key/value exchange buffer, then per-warp digit counters [warps][256]
   uint64_t *xk = reinterpret_cast<uint64_t *>(smem);
   uint32_t *xv = reinterpret_cast<uint32_t *>(smem + kRadixTile * 8);
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(smem + kRadixTile * 12);
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_local_start[256];
   __shared__ uint32_t s_gbase[256];
@@ -94,7 +94,9 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   }
   __syncthreads();
 
-  // ---- per digit (thread tid = digit): warp prefixes, tile count, look-back
+  // ---- per digit (thread tid = digit): warp prefixes, tile count; the tile's
+  // counts are published (aggregate) before anything else so successors can
+  // consume them without waiting for this tile's own look-back.
   const uint32_t dg = tid;
   uint32_t tot = 0;
 #pragma unroll
@@ -110,26 +112,24 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   else st_relaxed_u64(my_flag, make_flag(kFlagAgg, epoch, tot));
   uint32_t block_total;
   uint32_t local_start = block_exclusive_scan<uint32_t, kRadixThreads>(tot, &block_total, s_wt);
-  unsigned long long excl = tile == 0 ? (unsigned long long)digit_start[dg]
-                                      : lookback(lb + dg, tile, 256, epoch);
-  if (tile != 0) st_relaxed_u64(my_flag, make_flag(kFlagInc, epoch, excl + tot));
   s_local_start[dg] = local_start;
-  s_gbase[dg] = (uint32_t)excl - local_start;  // modular; global = gbase + local position
   __syncthreads();
 
-  // ---- local positions, then exchange through shared memory
-  uint32_t pos[kRadixItems];
+  // ---- exchange through shared memory into tile-local digit order (frees the
+  // key/value registers before the look-back)
 #pragma unroll
   for (int r = 0; r < kRadixItems; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & 0xFF;
-    pos[r] = s_local_start[d] + wc[d] + rank[r];
+    uint32_t pos = s_local_start[d] + wc[d] + rank[r];
+    xk[pos] = k[r];
+    xv[pos] = v[r];
   }
-  __syncthreads();  // counters are dead; reuse smem for the exchange
-#pragma unroll
-  for (int r = 0; r < kRadixItems; ++r) {
-    xk[pos[r]] = k[r];
-    xv[pos[r]] = v[r];
-  }
+
+  // ---- windowed decoupled look-back (8 predecessor tiles per round trip)
+  unsigned long long excl = tile == 0 ? (unsigned long long)digit_start[dg]
+                                      : lookback_window<8>(lb + dg, tile, 256, epoch);
+  if (tile != 0) st_relaxed_u64(my_flag, make_flag(kFlagInc, epoch, excl + tot));
+  s_gbase[dg] = (uint32_t)excl - local_start;  // modular; global = gbase + local position
   __syncthreads();
 
   // ---- scatter: consecutive local positions of a digit -> consecutive addresses

@@ -54,19 +54,37 @@ __global__ void __launch_bounds__(kScanThreads)
   }
   uint32_t tile_total;
   uint32_t excl_t = block_exclusive_scan<uint32_t, kScanThreads>(cnt, &tile_total, s_wt);
-  if (tid == 0) {
-    unsigned long long *f = lb + tile;
-    unsigned long long ex;
-    if (tile == 0) {
-      ex = 0;
-      st_relaxed_u64(f, make_flag(kFlagInc, epoch, tile_total));
-    } else {
-      st_relaxed_u64(f, make_flag(kFlagAgg, epoch, tile_total));
-      ex = lookback(lb, tile, 1, epoch);
-      st_relaxed_u64(f, make_flag(kFlagInc, epoch, ex + tile_total));
+  if (tid == 0) st_relaxed_u64(lb + tile, make_flag(tile == 0 ? kFlagInc : kFlagAgg, epoch, tile_total));
+
+  // order check of the adjacent pairs inside runs (independent of the look-back)
+  uint32_t badm = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    uint64_t p = p0 + j;
+    if ((eqn >> j) & 1) {
+      bool bad;
+      if (MODE == 0) {
+        bad = cmp_equal_code<CODER>(units, offsets, __ldg(perm + p), __ldg(perm + p + 1), T::kS) > 0;
+      } else if (MODE == 2) {
+        // strings already gathered in sorted order: contiguous reads
+        int64_t oa = __ldg(soffs + p), ob = __ldg(soffs + p + 1), oe = __ldg(soffs + p + 2);
+        bad = cmp_equal_code_ol<CODER>(sunits, oa, ob - oa, __ldg(perm + p), ob, oe - ob, __ldg(perm + p + 1),
+                                       T::kS) > 0;
+      } else {
+        constexpr uint64_t tagmask = CODER == HUSKY_CODER_ASCII ? 0xFFull : 0xFFFFull;
+        bad = (c[j + 1] & tagmask) == (uint64_t)(16 + T::kTagCap);
+      }
+      badm |= (uint32_t)bad << j;
     }
-    s_excl = ex;
-    if ((uint64_t)(tile + 1) * kScanTile >= n) st->n_runs = (uint32_t)(ex + tile_total);
+  }
+
+  if ((tid >> 5) == 0) {  // warp-wide look-back: 32 predecessor tiles per round trip
+    unsigned long long ex = tile == 0 ? 0ull : warp_lookback(lb, tile, epoch);
+    if (lane_id() == 0) {
+      if (tile != 0) st_relaxed_u64(lb + tile, make_flag(kFlagInc, epoch, ex + tile_total));
+      s_excl = ex;
+      if ((uint64_t)(tile + 1) * kScanTile >= n) st->n_runs = (uint32_t)(ex + tile_total);
+    }
   }
   __syncthreads();
   if ((eqp | eqn) == 0) return;
@@ -82,21 +100,7 @@ __global__ void __launch_bounds__(kScanThreads)
       run_start[rid] = base + (uint32_t)p;
     }
     if (ep && !en) run_end[rid] = base + (uint32_t)p;
-    if (en) {
-      bool bad;
-      if (MODE == 0) {
-        bad = cmp_equal_code<CODER>(units, offsets, __ldg(perm + p), __ldg(perm + p + 1), T::kS) > 0;
-      } else if (MODE == 2) {
-        // strings already gathered in sorted order: contiguous reads
-        int64_t oa = __ldg(soffs + p), ob = __ldg(soffs + p + 1), oe = __ldg(soffs + p + 2);
-        bad = cmp_equal_code_ol<CODER>(sunits, oa, ob - oa, __ldg(perm + p), ob, oe - ob, __ldg(perm + p + 1),
-                                       T::kS) > 0;
-      } else {
-        constexpr uint64_t tagmask = CODER == HUSKY_CODER_ASCII ? 0xFFull : 0xFFFFull;
-        bad = (c[j + 1] & tagmask) == (uint64_t)(16 + T::kTagCap);
-      }
-      if (bad) dirty[rid] = 1;
-    }
+    if ((badm >> j) & 1) dirty[rid] = 1;
   }
 }
 
