@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
                                                         uint64_t *__restrict__ codes, DevState *st,
                                                         uint32_t *__restrict__ packed) {
   __shared__ uint32_t sh_hist[HIST ? 8 * 256 : 1];
-  __shared__ int64_t s_off[kEncTile + 1];
+  __shared__ int64_t s_off[2][kEncTile + 1];
   __shared__ uint64_t s_stage[kEncStageWords + 2];
   if (HIST) {
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) sh_hist[i] = 0;
@@ -77,25 +77,42 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
   const bool any_units = olast > ofirst;
   const uintptr_t lo_word = (ub + (uintptr_t)(ofirst * W)) & ~(uintptr_t)7;
   const uintptr_t hi_word = any_units ? ((ub + (uintptr_t)(olast * W) - 1) & ~(uintptr_t)7) : lo_word;
-  for (uint64_t base = (uint64_t)blockIdx.x * kEncTile; base < n; base += (uint64_t)gridDim.x * kEncTile) {
-    // ---- stage the tile: its offsets, then its contiguous unit span, with
-    // fully coalesced loads (each byte of the span is read once)
+  const uint64_t stride = (uint64_t)gridDim.x * kEncTile;
+  auto issue_offsets = [&](uint64_t b, int64_t *dst) {
+    uint32_t c = (uint32_t)((n - b) < (uint64_t)kEncTile ? (n - b) : kEncTile);
+    for (uint32_t i = threadIdx.x; i <= c; i += blockDim.x) cp_async8(&dst[i], offsets + b + i);
+    cp_async_commit();
+  };
+  int buf = 0;
+  if ((uint64_t)blockIdx.x * kEncTile < n) issue_offsets((uint64_t)blockIdx.x * kEncTile, s_off[0]);
+  for (uint64_t base = (uint64_t)blockIdx.x * kEncTile; base < n; base += stride, buf ^= 1) {
+    // ---- stage the tile: its offsets (prefetched one tile ahead), then its
+    // contiguous unit span, with coalesced async copies (each byte read once)
     const uint32_t cnt = (uint32_t)((n - base) < (uint64_t)kEncTile ? (n - base) : kEncTile);
-    for (uint32_t i = threadIdx.x; i <= cnt; i += blockDim.x) s_off[i] = __ldg(offsets + base + i);
+    const int64_t *so = s_off[buf];
+    cp_async_wait_all();
     __syncthreads();
-    const int64_t tstart = s_off[0], tend = s_off[cnt];
+    const int64_t tstart = so[0], tend = so[cnt];
     const uintptr_t aw0 = (ub + (uintptr_t)(tstart * W)) & ~(uintptr_t)7;
     const int64_t nwords = tend > tstart ? (int64_t)(((ub + (uintptr_t)(tend * W)) - aw0 + 7) >> 3) : 0;
     const bool staged = nwords <= kEncStageWords;
-    if (staged)
-      for (int64_t wd = threadIdx.x; wd < nwords; wd += blockDim.x) s_stage[wd] = __ldg((const uint64_t *)aw0 + wd);
+    if (staged) {
+      for (int64_t wd = threadIdx.x; wd < nwords; wd += blockDim.x) cp_async8(&s_stage[wd], (const uint64_t *)aw0 + wd);
+      cp_async_commit();
+    }
+    const bool has_next = base + stride < n;
+    if (has_next) issue_offsets(base + stride, s_off[buf ^ 1]);
+    if (staged) {
+      if (has_next) cp_async_wait_group<1>();
+      else cp_async_wait_all();
+    }
     __syncthreads();
 
     int64_t o0[kEncItems], o1[kEncItems];
 #pragma unroll
     for (int k = 0; k < kEncItems; ++k) {
       uint32_t li = threadIdx.x + k * blockDim.x;
-      if (li < cnt) { o0[k] = s_off[li]; o1[k] = s_off[li + 1]; }
+      if (li < cnt) { o0[k] = so[li]; o1[k] = so[li + 1]; }
       else { o0[k] = tstart; o1[k] = tstart; }
     }
     uint64_t w0[kEncItems], w1[kEncItems];

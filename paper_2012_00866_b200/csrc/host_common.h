@@ -53,7 +53,7 @@ struct Sorter {
   unsigned long long *lb_scan() const { return at<unsigned long long>(L.lb_scan); }
 
   cudaError_t reset_lookback() {
-    cudaError_t e = cudaMemsetAsync(ws + L.lb_radix, 0, L.tiles_r * 256 * 8, s);
+    cudaError_t e = cudaMemsetAsync(ws + L.lb_radix, 0, radix_lb_words(L.n) * 8, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(ws + L.lb_scan, 0, L.tiles_s * 8, s);
     return e;
   }

@@ -65,7 +65,7 @@ Layout make_layout(uint64_t n) {
   L.keysB = take(n * 8);
   L.vals = take(n * 4);
   L.vals2 = take(n * 4);  // packed initial payload (index | len << 28) when n <= 2^28
-  L.lb_radix = take(L.tiles_r * 256 * 8);
+  L.lb_radix = take(radix_lb_words(n) * 8);
   L.lb_scan = take(L.tiles_s * 8);
   L.run_start = take(L.cap_sm * 4);
   L.run_end = take(L.cap_sm * 4);

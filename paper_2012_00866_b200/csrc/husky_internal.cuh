@@ -103,10 +103,12 @@ __device__ __forceinline__ unsigned long long lookback(const unsigned long long 
 // the window and is re-read.  One round trip covers up to W tiles.
 template <int W>
 __device__ __forceinline__ unsigned long long lookback_window(const unsigned long long *flags, uint32_t tile,
-                                                              uint32_t stride, uint32_t epoch) {
+                                                              uint32_t stride, uint32_t epoch,
+                                                              uint32_t *stats = nullptr) {
   unsigned long long excl = 0;
   int64_t j = (int64_t)tile - 1;
   while (j >= 0) {
+    if (stats) stats[0]++;
     unsigned long long w[W];
 #pragma unroll
     for (int q = 0; q < W; ++q)
@@ -125,6 +127,69 @@ __device__ __forceinline__ unsigned long long lookback_window(const unsigned lon
     }
     if (done) break;
     j -= used;
+    if (used == 0) {
+      // the nearest predecessor has not published yet: poll just that word,
+      // backing off so the spinning warp leaves issue slots to working warps
+      unsigned ns = 32;
+      for (;;) {
+        unsigned long long x = ld_relaxed_u64(flags + (uint64_t)j * stride);
+        if (((uint32_t)(x >> 54) & 0xFF) == epoch && (x & (3ull << 62)) != 0) break;
+        if (stats) stats[1]++;
+        __nanosleep(ns);
+        if (ns < 512) ns <<= 1;
+      }
+    }
+  }
+  return excl;
+}
+
+__device__ __forceinline__ void ld_relaxed_v2u64(const unsigned long long *p, unsigned long long &a,
+                                                 unsigned long long &b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+// Look-back over a TRANSPOSED flag row (row[t] = word of tile t for one digit):
+// one round trip reads the 16 nearest predecessors with 8 aligned 16-byte
+// loads, so the inclusive-prefix frontier keeps up with the tile arrival rate
+// (a window of 1-8 tiles per round trip falls behind on a 148-SM part).
+__device__ __forceinline__ unsigned long long lookback_row16(const unsigned long long *row, uint32_t tile,
+                                                             uint32_t epoch) {
+  unsigned long long excl = 0;
+  int64_t j = (int64_t)tile - 1;
+  const unsigned long long inc0 = make_flag(kFlagInc, epoch, 0);
+  while (j >= 0) {
+    const int64_t lo = (j & 1) ? j - 15 : j - 14;  // even: 16-byte aligned pairs; covers lo..j (j <= lo+15)
+    unsigned long long w[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      int64_t i = lo + 2 * q;
+      if (i >= 0) ld_relaxed_v2u64(row + i, w[2 * q], w[2 * q + 1]);
+      else { w[2 * q] = inc0; w[2 * q + 1] = inc0; }
+    }
+    int used = 0;
+    bool done = false, blocked = false;
+#pragma unroll
+    for (int q = 15; q >= 0; --q) {
+      if (done || blocked) continue;
+      if (lo + q > j) continue;  // the word past the nearest predecessor
+      unsigned long long x = w[q];
+      bool ok = ((uint32_t)(x >> 54) & 0xFF) == epoch && (x & (3ull << 62)) != 0;
+      if (!ok) { blocked = true; continue; }
+      excl += x & kValMask;
+      ++used;
+      if ((x & (3ull << 62)) == kFlagInc) done = true;
+    }
+    if (done) break;
+    j -= used;
+    if (blocked) {  // poll just the blocking word, backing off
+      unsigned ns = 32;
+      for (;;) {
+        unsigned long long x = ld_relaxed_u64(row + j);
+        if (((uint32_t)(x >> 54) & 0xFF) == epoch && (x & (3ull << 62)) != 0) break;
+        __nanosleep(ns);
+        if (ns < 512) ns <<= 1;
+      }
+    }
   }
   return excl;
 }
@@ -156,6 +221,7 @@ __device__ __forceinline__ unsigned long long warp_lookback(const unsigned long 
     excl += v;
     if (stop) break;
     base -= take;
+    if (take == 0) __nanosleep(64);  // nearest predecessor unpublished: back off
   }
   return excl;
 }
@@ -193,6 +259,21 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T *total, T *warp_tot) {
   *total = warp_tot[NW];
   return r;
 }
+
+// Asynchronous global -> shared copies (LDGSTS): many in flight per thread, no
+// register round trip.  cp_async_wait_all() + __syncthreads() before reading.
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gmem_src) {
+  uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *smem_dst, const void *gmem_src) {
+  uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // Unaligned little-endian load of 8 bytes at byte address p, reading only the
 // aligned 8-byte words that contain bytes [p, p + need) (need in 1..8), so it

@@ -18,12 +18,18 @@ void launch_encode(int coder, bool hist, const void *units, const int64_t *offse
                    uint64_t *codes, DevState *st, int num_sms, cudaStream_t s, uint32_t *packed = nullptr);
 
 // A2 onesweep radix
-// 256 threads x 8 keys = 2048-key tiles, 24 KB smem, <= 64 registers -> 4 CTAs
-// (32 warps) per SM so the key loads and the look-back of one tile overlap the
-// ranking of others.
-constexpr int kRadixThreads = 256, kRadixItems = 8, kRadixTile = kRadixThreads * kRadixItems;
-constexpr int kRadixMinBlocks = 4;
+// 512 threads x 8 keys = 4096-key tiles, 64 KB smem, <= 64 registers -> 2 CTAs
+// (32 warps) per SM.  Large tiles keep the number of tiles in flight low: each
+// look-back round trip queues behind the SM's bulk DRAM loads (~1 us under
+// load), so the walk length (tiles between a tile and the inclusive-prefix
+// frontier) is what bounds the pass; measured per-tile phases in DESIGN.md.
+constexpr int kRadixThreads = 512, kRadixItems = 8, kRadixTile = kRadixThreads * kRadixItems;
+constexpr int kRadixMinBlocks = 2;
 inline uint64_t radix_tiles(uint64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
+// look-back words are stored transposed, [digit][tile], rows of an even length
+// (16-byte aligned pair loads); the buffer holds 256 rows
+inline uint64_t radix_lb_stride(uint64_t n) { return (radix_tiles(n) + 1) & ~1ull; }
+inline uint64_t radix_lb_words(uint64_t n) { return radix_lb_stride(n) * 256 + 2; }
 void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s);
 // One stable LSD pass on digit `digit` (bits 8*digit..8*digit+7).  vals_in == NULL
 // synthesises payload = index.  lb: radix_tiles(n)*256 look-back words.

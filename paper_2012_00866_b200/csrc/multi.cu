@@ -177,7 +177,7 @@ static MultiLayout make_multi_layout(int coder, uint64_t n, uint64_t units, int 
   L.keysA = take(n * 8 + 8);
   L.keysB = take(n * 8 + 8);
   L.vals = take(n * 4 + 4);
-  L.lb_radix = take(L.tiles_r * 256 * 8 + 8);
+  L.lb_radix = take(radix_lb_words(n) * 8);
   L.lb_scan = take(L.tiles_s * 8 + 8);
   M.send_perm = take(n * 4 + 4);
   M.samples = take((size_t)world * kSampleStride * 8);

@@ -39,6 +39,24 @@ void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s) {
 }
 
 constexpr int kRadixWarps = kRadixThreads / 32;
+#ifndef RADIX_LB_W
+#define RADIX_LB_W 16
+#endif
+
+#ifdef HUSKY_TIMING
+// per-tile phase timestamps of the last onesweep launch (instrumented builds only)
+constexpr int kTimingTiles = 8192;
+__device__ unsigned long long g_tile_times[kTimingTiles][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define HT(tile, i) \
+  do { if (threadIdx.x == 0 && (tile) < kTimingTiles) g_tile_times[tile][i] = gtimer(); } while (0)
+#else
+#define HT(tile, i) do { } while (0)
+#endif
 constexpr int kExchangeBytes = kRadixTile * (8 + 4) + kRadixWarps * 256 * 4;
 
 template <bool SYNTH_VALS>
@@ -46,7 +64,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     k_onesweep(const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint64_t n, int shift,
                const uint32_t *__restrict__ digit_start, unsigned long long *lb, uint32_t *tile_counter,
-               uint32_t epoch) {
+               uint32_t epoch, uint64_t lb_stride) {
   extern __shared__ __align__(16) uint8_t smem[];
   // key/value exchange buffer, then per-warp digit counters [warps][256]
   uint64_t *xk = reinterpret_cast<uint64_t *>(smem);
@@ -63,6 +81,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint64_t tile_base = (uint64_t)tile * kRadixTile;
+  HT(tile, 0);
 
   // ---- load (warp-striped: element = tile_base + warp*512 + r*32 + lane)
   uint64_t k[kRadixItems];
@@ -86,6 +105,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   for (int r = 0; r < kRadixItems; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & 0xFF;
     uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+    if (r == 0) HT(tile, 1);
     uint32_t pre = wc[d];
     rank[r] = pre + __popc(peers & lanemask_lt());
     __syncwarp();
@@ -93,27 +113,36 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     __syncwarp();
   }
   __syncthreads();
+  HT(tile, 2);
 
   // ---- per digit (thread tid = digit): warp prefixes, tile count; the tile's
   // counts are published (aggregate) before anything else so successors can
   // consume them without waiting for this tile's own look-back.
-  const uint32_t dg = tid;
+  // threads 0..255 own one digit each (the CTA may have more threads)
+  const bool is_dg = tid < 256;
+  const uint32_t dg = tid & 255;
   uint32_t tot = 0;
+  if (is_dg) {
 #pragma unroll
-  for (int w = 0; w < kRadixWarps; ++w) {
-    uint32_t c = cnt[w * 256 + dg];
-    cnt[w * 256 + dg] = tot;
-    tot += c;
+    for (int w = 0; w < kRadixWarps; ++w) {
+      uint32_t c = cnt[w * 256 + dg];
+      cnt[w * 256 + dg] = tot;
+      tot += c;
+    }
   }
   uint64_t tile_end = tile_base + kRadixTile;
-  if (dg == 255 && tile_end > n) tot -= (uint32_t)(tile_end - n);  // padding keys
+  if (is_dg && dg == 255 && tile_end > n) tot -= (uint32_t)(tile_end - n);  // padding keys
   unsigned long long *my_flag = lb + (uint64_t)tile * 256 + dg;
-  if (tile == 0) st_relaxed_u64(my_flag, make_flag(kFlagInc, epoch, (unsigned long long)digit_start[dg] + tot));
-  else st_relaxed_u64(my_flag, make_flag(kFlagAgg, epoch, tot));
+  (void)lb_stride;
+  if (is_dg) {
+    if (tile == 0) st_relaxed_u64(my_flag, make_flag(kFlagInc, epoch, (unsigned long long)digit_start[dg] + tot));
+    else st_relaxed_u64(my_flag, make_flag(kFlagAgg, epoch, tot));
+  }
   uint32_t block_total;
   uint32_t local_start = block_exclusive_scan<uint32_t, kRadixThreads>(tot, &block_total, s_wt);
-  s_local_start[dg] = local_start;
+  if (is_dg) s_local_start[dg] = local_start;
   __syncthreads();
+  HT(tile, 3);
 
   // ---- exchange through shared memory into tile-local digit order (frees the
   // key/value registers before the look-back)
@@ -125,12 +154,23 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     xv[pos] = v[r];
   }
 
-  // ---- windowed decoupled look-back (8 predecessor tiles per round trip)
-  unsigned long long excl = tile == 0 ? (unsigned long long)digit_start[dg]
-                                      : lookback_window<8>(lb + dg, tile, 256, epoch);
-  if (tile != 0) st_relaxed_u64(my_flag, make_flag(kFlagInc, epoch, excl + tot));
-  s_gbase[dg] = (uint32_t)excl - local_start;  // modular; global = gbase + local position
+  // ---- decoupled look-back, RADIX_LB_W predecessor tiles per round trip
+  if (is_dg) {
+#ifdef HUSKY_TIMING
+    uint32_t lbst[2] = {0, 0};
+    unsigned long long excl = tile == 0 ? (unsigned long long)digit_start[dg]
+                                        : lookback_window<RADIX_LB_W>(lb + dg, tile, 256, epoch, lbst);
+    if (tid == 0 && tile < kTimingTiles) g_tile_times[tile][7] = lbst[0] | ((unsigned long long)lbst[1] << 32);
+#else
+    unsigned long long excl = tile == 0 ? (unsigned long long)digit_start[dg]
+                                        : lookback_window<RADIX_LB_W>(lb + dg, tile, 256, epoch);
+#endif
+    if (tile != 0) st_relaxed_u64(my_flag, make_flag(kFlagInc, epoch, excl + tot));
+    if (tid == 0) HT(tile, 4);  // thread 0's own look-back done
+    s_gbase[dg] = (uint32_t)excl - local_start;  // modular; global = gbase + local position
+  }
   __syncthreads();
+  HT(tile, 5);
 
   // ---- scatter: consecutive local positions of a digit -> consecutive addresses
   uint32_t n_valid = (uint32_t)((n - tile_base) < (uint64_t)kRadixTile ? (n - tile_base) : kRadixTile);
@@ -142,6 +182,21 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     keys_out[g] = key;
     vals_out[g] = xv[i];
   }
+  HT(tile, 6);
+}
+
+// instrumented builds: copy the per-tile phase timestamps of the last pass
+extern "C" int husky_debug_tile_times(unsigned long long *out, int max_tiles) {
+#ifdef HUSKY_TIMING
+  int k = max_tiles < kTimingTiles ? max_tiles : kTimingTiles;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_tile_times, (size_t)k * 8 * sizeof(unsigned long long));
+  return k;
+#else
+  (void)out;
+  (void)max_tiles;
+  return 0;
+#endif
 }
 
 void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,
@@ -157,12 +212,13 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
   Scope sc_(ST_RADIX, s, n);
   dim3 g((unsigned)radix_tiles(n)), b(kRadixThreads);
   const uint32_t *ds = st->digit_start[digit];
+  const uint64_t stride = radix_lb_stride(n);
   if (vals_in == nullptr)
     k_onesweep<true><<<g, b, kExchangeBytes, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                  tile_counter, epoch);
+                                                  tile_counter, epoch, stride);
   else
     k_onesweep<false><<<g, b, kExchangeBytes, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                   tile_counter, epoch);
+                                                   tile_counter, epoch, stride);
 }
 
 __global__ void k_iota(uint32_t *perm, uint64_t n) {

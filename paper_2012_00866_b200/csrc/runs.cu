@@ -26,6 +26,14 @@ __global__ void __launch_bounds__(kScanThreads)
                 DevState *st, unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch,
                 const void *__restrict__ sunits, const int64_t *__restrict__ soffs) {
   using T = CoderTraits<CODER>;
+  // Tile staging in smem (coalesced async copies).  Each thread then works on
+  // kScanItems consecutive positions; the arrays are padded (one pad element
+  // every 8 u64 / 32 u32) so that blocked per-thread reads do not bank-conflict.
+  constexpr int KP = kScanTile + 2 + (kScanTile + 2) / 8 + 1;
+  constexpr bool SO = MODE == 2;
+  __shared__ uint64_t s_keys[KP];                                  // keys[tile_base - 1 + i]
+  __shared__ int64_t s_soff[SO ? KP : 1];                          // soffs[tile_base + i]
+  __shared__ uint32_t s_perm[SO ? kScanTile + 2 + (kScanTile + 2) / 32 + 1 : 1];  // perm[tile_base + i]
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_wt[kScanThreads / 32 + 1];
   __shared__ unsigned long long s_excl;
@@ -33,14 +41,28 @@ __global__ void __launch_bounds__(kScanThreads)
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint64_t p0 = (uint64_t)tile * kScanTile + (uint64_t)tid * kScanItems;
+  const uint64_t tb = (uint64_t)tile * kScanTile;
+  const uint64_t p0 = tb + (uint64_t)tid * kScanItems;
+  for (uint32_t i = tid; i < kScanTile + 2; i += kScanThreads) {
+    int64_t p = (int64_t)tb + (int64_t)i - 1;
+    if (p >= 0 && (uint64_t)p < n) cp_async8(&s_keys[i + i / 8], keys + p);
+    if (SO) {
+      uint64_t q = tb + i;
+      if (q <= n) cp_async8(&s_soff[i + i / 8], soffs + q);
+      if (q < n) cp_async4(&s_perm[i + i / 32], perm + q);
+    }
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
 
-  // keys at p0-1 .. p0+kScanItems (neighbours come from L1)
+  // keys at p0-1 .. p0+kScanItems
   uint64_t c[kScanItems + 2];
 #pragma unroll
   for (int j = 0; j < kScanItems + 2; ++j) {
     int64_t p = (int64_t)p0 + j - 1;
-    c[j] = (p >= 0 && (uint64_t)p < n) ? __ldg(keys + p) : 0ull;
+    uint32_t i = tid * kScanItems + j;
+    c[j] = (p >= 0 && (uint64_t)p < n) ? s_keys[i + i / 8] : 0ull;
   }
   uint32_t eqp = 0, eqn = 0, cnt = 0;  // bit j: eq_prev / eq_next of position p0+j
 #pragma unroll
@@ -66,10 +88,12 @@ __global__ void __launch_bounds__(kScanThreads)
       if (MODE == 0) {
         bad = cmp_equal_code<CODER>(units, offsets, __ldg(perm + p), __ldg(perm + p + 1), T::kS) > 0;
       } else if (MODE == 2) {
-        // strings already gathered in sorted order: contiguous reads
-        int64_t oa = __ldg(soffs + p), ob = __ldg(soffs + p + 1), oe = __ldg(soffs + p + 2);
-        bad = cmp_equal_code_ol<CODER>(sunits, oa, ob - oa, __ldg(perm + p), ob, oe - ob, __ldg(perm + p + 1),
-                                       T::kS) > 0;
+        // strings already gathered in sorted order: offsets / indices from smem,
+        // units (only for pairs longer than PL) contiguous in sorted_units
+        uint32_t i = tid * kScanItems + j;
+        int64_t oa = s_soff[i + i / 8], ob = s_soff[(i + 1) + (i + 1) / 8], oe = s_soff[(i + 2) + (i + 2) / 8];
+        uint32_t ia = s_perm[i + i / 32], ib = s_perm[(i + 1) + (i + 1) / 32];
+        bad = cmp_equal_code_ol<CODER>(sunits, oa, ob - oa, ia, ob, oe - ob, ib, T::kS) > 0;
       } else {
         constexpr uint64_t tagmask = CODER == HUSKY_CODER_ASCII ? 0xFFull : 0xFFFFull;
         bad = (c[j + 1] & tagmask) == (uint64_t)(16 + T::kTagCap);
