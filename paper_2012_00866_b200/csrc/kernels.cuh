@@ -6,6 +6,8 @@
 
 namespace husky {
 
+int device_sm_count();  // husky.cu
+
 // A1 encode
 // tile of 1024 strings per CTA iteration; its unit span (<= 16 KB) is staged in smem
 constexpr int kEncThreads = 256, kEncItems = 4, kEncTile = kEncThreads * kEncItems, kEncBlocksPerSM = 4;

@@ -1,4 +1,4 @@
-// radix.cu -- A2: stable onesweep LSD radix sort of (64-bit key, 32-bit payload).
+// radix.cu -- A2: stable LSD radix sort of (64-bit key, 32-bit payload).
 //
 // Role in the paper: step 2 of Alg. 1, "Sort array longs ... in such a way that
 // when elements i, j of longs are exchanged, then elements i, j of xs are also
@@ -7,15 +7,21 @@
 // co-swap is the payload scatter.  Being stable, it leaves equal codes in index
 // order (R7), which the fix-up (A5) relies on.
 //
-// Per pass (one launch): a tile of 4096 keys (256 threads x 16, warp-striped so
-// every load/store instruction is a coalesced 256-B access) is ranked in shared
-// memory with warp-level match (__match_any_sync) + popc ranking into per-warp
-// digit counters; the tile's digit counts are published to a per-(tile, digit)
-// decoupled look-back array; the global digit base comes from the histograms the
-// encoder fused into A1 (exclusive-scanned by k_hist_scan).  Keys are then
-// exchanged through shared memory into digit order and written out as runs of
-// consecutive addresses.  Tile ids come from an atomic counter, so every
-// predecessor a tile waits on is already resident (forward progress).
+// A pass (one 8-bit digit) works on tiles of 4096 keys (512 threads x 8,
+// warp-striped so every load/store instruction is a coalesced 256-B access).
+// Each tile is ranked in shared memory with warp-level match (__match_any_sync)
+// + popc into per-warp digit counters, exchanged through shared memory into
+// digit order, and written out as runs of consecutive addresses.  The tile's
+// global base per digit comes from one of two schemes:
+//   * onesweep (HUSKY_RADIX=onesweep): per-(tile, digit) decoupled look-back
+//     (Adinets & Merrill), global digit starts from the histograms the encoder
+//     fused into A1.  One read of the keys per pass, but the look-back is a chain
+//     of dependent L2 round trips (~1 us each with the memory system saturated;
+//     measured per-tile phases in DESIGN.md).
+//   * reduce-then-scan (default): an upsweep writes each tile's digit counts
+//     (8 B/key read), a digit-parallel scan turns them into per-tile bases, and
+//     the downsweep ranks/exchanges/scatters with no inter-tile dependency.
+// Digits whose histogram puts all keys in one bucket are skipped by the caller.
 #include "husky_internal.cuh"
 #include "kernels.cuh"
 
@@ -40,11 +46,11 @@ void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s) {
 
 constexpr int kRadixWarps = kRadixThreads / 32;
 #ifndef RADIX_LB_W
-#define RADIX_LB_W 16
+#define RADIX_LB_W 8
 #endif
 
 #ifdef HUSKY_TIMING
-// per-tile phase timestamps of the last onesweep launch (instrumented builds only)
+// per-tile phase timestamps of the last radix launch (instrumented builds only)
 constexpr int kTimingTiles = 8192;
 __device__ unsigned long long g_tile_times[kTimingTiles][8];
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -59,12 +65,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 constexpr int kExchangeBytes = kRadixTile * (8 + 4) + kRadixWarps * 256 * 4;
 
-template <bool SYNTH_VALS>
+// One pass over one tile.  LOOKBACK: decoupled look-back on `lb` (onesweep);
+// otherwise the tile's per-digit bases are read from `prefix` ([digit][tile],
+// written by k_rs_scan) and nothing waits on other tiles.
+template <bool SYNTH_VALS, bool LOOKBACK>
 __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     k_onesweep(const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint64_t n, int shift,
                const uint32_t *__restrict__ digit_start, unsigned long long *lb, uint32_t *tile_counter,
-               uint32_t epoch, uint64_t lb_stride) {
+               uint32_t epoch, const uint32_t *__restrict__ prefix, uint32_t num_tiles) {
   extern __shared__ __align__(16) uint8_t smem[];
   // key/value exchange buffer, then per-warp digit counters [warps][256]
   uint64_t *xk = reinterpret_cast<uint64_t *>(smem);
@@ -76,14 +85,16 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   __shared__ uint32_t s_wt[kRadixWarps + 1];
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  if (LOOKBACK) {  // dynamic tile ids: every predecessor a tile waits on is resident
+    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  }
   for (int i = tid; i < kRadixWarps * 256; i += kRadixThreads) cnt[i] = 0;
   __syncthreads();
-  const uint32_t tile = s_tile;
+  const uint32_t tile = LOOKBACK ? s_tile : blockIdx.x;
   const uint64_t tile_base = (uint64_t)tile * kRadixTile;
   HT(tile, 0);
 
-  // ---- load (warp-striped: element = tile_base + warp*512 + r*32 + lane)
+  // ---- load (warp-striped: element = tile_base + warp*256 + r*32 + lane)
   uint64_t k[kRadixItems];
   uint32_t v[kRadixItems];
 #pragma unroll
@@ -97,6 +108,11 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
       v[r] = 0;
     }
   }
+  // ---- the tile's bases (reduce-then-scan): independent of everything above
+  const bool is_dg = tid < 256;  // threads 0..255 own one digit each
+  const uint32_t dg = tid & 255;
+  uint32_t pre_base = 0;
+  if (!LOOKBACK && is_dg) pre_base = __ldg(prefix + (uint64_t)dg * num_tiles + tile);
 
   // ---- warp-level match ranking into per-warp counters (stable: (r, lane) order)
   uint32_t *wc = cnt + warp * 256;
@@ -115,12 +131,8 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   __syncthreads();
   HT(tile, 2);
 
-  // ---- per digit (thread tid = digit): warp prefixes, tile count; the tile's
-  // counts are published (aggregate) before anything else so successors can
-  // consume them without waiting for this tile's own look-back.
-  // threads 0..255 own one digit each (the CTA may have more threads)
-  const bool is_dg = tid < 256;
-  const uint32_t dg = tid & 255;
+  // ---- per digit: warp prefixes and the tile count; with look-back the tile's
+  // aggregate is published before anything else so successors can consume it
   uint32_t tot = 0;
   if (is_dg) {
 #pragma unroll
@@ -133,8 +145,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   uint64_t tile_end = tile_base + kRadixTile;
   if (is_dg && dg == 255 && tile_end > n) tot -= (uint32_t)(tile_end - n);  // padding keys
   unsigned long long *my_flag = lb + (uint64_t)tile * 256 + dg;
-  (void)lb_stride;
-  if (is_dg) {
+  if (LOOKBACK && is_dg) {
     if (tile == 0) st_relaxed_u64(my_flag, make_flag(kFlagInc, epoch, (unsigned long long)digit_start[dg] + tot));
     else st_relaxed_u64(my_flag, make_flag(kFlagAgg, epoch, tot));
   }
@@ -144,8 +155,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   __syncthreads();
   HT(tile, 3);
 
-  // ---- exchange through shared memory into tile-local digit order (frees the
-  // key/value registers before the look-back)
+  // ---- exchange through shared memory into tile-local digit order
 #pragma unroll
   for (int r = 0; r < kRadixItems; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & 0xFF;
@@ -154,19 +164,23 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     xv[pos] = v[r];
   }
 
-  // ---- decoupled look-back, RADIX_LB_W predecessor tiles per round trip
+  // ---- global base of each digit
   if (is_dg) {
+    unsigned long long excl;
+    if (LOOKBACK) {
 #ifdef HUSKY_TIMING
-    uint32_t lbst[2] = {0, 0};
-    unsigned long long excl = tile == 0 ? (unsigned long long)digit_start[dg]
-                                        : lookback_window<RADIX_LB_W>(lb + dg, tile, 256, epoch, lbst);
-    if (tid == 0 && tile < kTimingTiles) g_tile_times[tile][7] = lbst[0] | ((unsigned long long)lbst[1] << 32);
+      uint32_t lbst[2] = {0, 0};
+      excl = tile == 0 ? (unsigned long long)digit_start[dg]
+                       : lookback_window<RADIX_LB_W>(lb + dg, tile, 256, epoch, lbst);
+      if (tid == 0 && tile < kTimingTiles) g_tile_times[tile][7] = lbst[0] | ((unsigned long long)lbst[1] << 32);
 #else
-    unsigned long long excl = tile == 0 ? (unsigned long long)digit_start[dg]
-                                        : lookback_window<RADIX_LB_W>(lb + dg, tile, 256, epoch);
+      excl = tile == 0 ? (unsigned long long)digit_start[dg] : lookback_window<RADIX_LB_W>(lb + dg, tile, 256, epoch);
 #endif
-    if (tile != 0) st_relaxed_u64(my_flag, make_flag(kFlagInc, epoch, excl + tot));
-    if (tid == 0) HT(tile, 4);  // thread 0's own look-back done
+      if (tile != 0) st_relaxed_u64(my_flag, make_flag(kFlagInc, epoch, excl + tot));
+    } else {
+      excl = pre_base;
+    }
+    if (tid == 0) HT(tile, 4);
     s_gbase[dg] = (uint32_t)excl - local_start;  // modular; global = gbase + local position
   }
   __syncthreads();
@@ -183,6 +197,55 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     vals_out[g] = xv[i];
   }
   HT(tile, 6);
+}
+
+// ------------------------------------------------------- reduce-then-scan
+// Upsweep: counts[digit][tile] of one tile (warp-striped loads, match-aggregated
+// shared-memory histogram).
+constexpr int kUpThreads = 256, kUpItems = kRadixTile / kUpThreads;
+
+__global__ void __launch_bounds__(kUpThreads)
+    k_rs_upsweep(const uint64_t *__restrict__ keys, uint64_t n, int shift, uint32_t *__restrict__ counts,
+                 uint32_t num_tiles) {
+  __shared__ uint32_t hist[256];
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  hist[tid] = 0;
+  const uint32_t tile = blockIdx.x;
+  const uint64_t tb = (uint64_t)tile * kRadixTile;
+  uint64_t k[kUpItems];
+#pragma unroll
+  for (int r = 0; r < kUpItems; ++r) {
+    uint64_t idx = tb + warp * (kUpItems * 32) + r * 32 + lane;
+    k[r] = idx < n ? __ldg(keys + idx) : ~0ull;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kUpItems; ++r) {
+    uint64_t idx = tb + warp * (kUpItems * 32) + r * 32 + lane;
+    uint32_t d = idx < n ? (uint32_t)(k[r] >> shift) & 0xFF : 256u;
+    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+    if (d < 256 && lane == 31 - __clz(peers)) atomicAdd(&hist[d], (uint32_t)__popc(peers));
+  }
+  __syncthreads();
+  counts[(uint64_t)tid * num_tiles + tile] = hist[tid];
+}
+
+// Scan: one CTA per digit turns counts[d][*] into bases digit_start[d] + sum of
+// the counts of earlier tiles (in place).
+__global__ void __launch_bounds__(1024)
+    k_rs_scan(uint32_t *__restrict__ counts, uint32_t num_tiles, const uint32_t *__restrict__ digit_start) {
+  __shared__ uint32_t wt[33];
+  uint32_t *row = counts + (uint64_t)blockIdx.x * num_tiles;
+  uint32_t running = digit_start[blockIdx.x];
+  for (uint32_t c = 0; c < num_tiles; c += 1024) {
+    uint32_t i = c + threadIdx.x;
+    uint32_t v = i < num_tiles ? row[i] : 0u;
+    uint32_t total;
+    uint32_t ex = block_exclusive_scan<uint32_t, 1024>(v, &total, wt);
+    if (i < num_tiles) row[i] = running + ex;
+    running += total;
+    __syncthreads();
+  }
 }
 
 // instrumented builds: copy the per-tile phase timestamps of the last pass
@@ -205,20 +268,39 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
   if (n == 0) return;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
-    cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
+    cudaFuncSetAttribute(k_onesweep<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
+    cudaFuncSetAttribute(k_onesweep<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
+    cudaFuncSetAttribute(k_onesweep<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
+    cudaFuncSetAttribute(k_onesweep<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
     configured = true;
   }
+  static const bool onesweep = [] {
+    const char *v = getenv("HUSKY_RADIX");
+    return !(v && v[0] == 'r');  // default onesweep; HUSKY_RADIX=rts: reduce-then-scan variant
+  }();
   Scope sc_(ST_RADIX, s, n);
-  dim3 g((unsigned)radix_tiles(n)), b(kRadixThreads);
   const uint32_t *ds = st->digit_start[digit];
-  const uint64_t stride = radix_lb_stride(n);
+  const uint32_t tiles = (uint32_t)radix_tiles(n);
+  dim3 g(tiles), b(kRadixThreads);
+  if (onesweep) {
+    if (vals_in == nullptr)
+      k_onesweep<true, true><<<g, b, kExchangeBytes, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds,
+                                                          lb, tile_counter, epoch, nullptr, tiles);
+    else
+      k_onesweep<false, true><<<g, b, kExchangeBytes, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds,
+                                                           lb, tile_counter, epoch, nullptr, tiles);
+    return;
+  }
+  // reduce-then-scan: the look-back buffer (tiles*256 u64) holds counts[256][tiles] u32
+  uint32_t *counts = reinterpret_cast<uint32_t *>(lb);
+  k_rs_upsweep<<<tiles, kUpThreads, 0, s>>>(keys_in, n, 8 * digit, counts, tiles);
+  k_rs_scan<<<256, 1024, 0, s>>>(counts, tiles, ds);
   if (vals_in == nullptr)
-    k_onesweep<true><<<g, b, kExchangeBytes, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                  tile_counter, epoch, stride);
+    k_onesweep<true, false><<<g, b, kExchangeBytes, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds, lb,
+                                                         tile_counter, epoch, counts, tiles);
   else
-    k_onesweep<false><<<g, b, kExchangeBytes, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                   tile_counter, epoch, stride);
+    k_onesweep<false, false><<<g, b, kExchangeBytes, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds, lb,
+                                                          tile_counter, epoch, counts, tiles);
 }
 
 __global__ void k_iota(uint32_t *perm, uint64_t n) {
