@@ -4,13 +4,14 @@
 // here the strings themselves are materialised in sorted order:
 //   sorted_offsets = exclusive scan of len[perm[i]]  (single pass, look-back)
 //   sorted_units   = concatenation of units[offsets[perm[i]] ..)
-// A tile of 1024 sorted positions: perm (coalesced) -> offsets (random) ->
-// tile-local scan; the tile's aggregate is published, then every thread stages
-// its strings into shared memory at tile-local byte offsets (random reads,
-// independent of the look-back), warp 0 resolves the tile's global base with a
-// warp-wide look-back (32 predecessors per round trip), and the tile's output
-// range is written with aligned 16-byte stores (funnel-shifted out of smem);
-// only the two boundary chunks use byte stores, so neighbouring tiles never race.
+// A tile of 4096 sorted positions (512 threads x 8): perm (coalesced) ->
+// lengths -> tile-local scan; the tile's aggregate is published, then the first
+// window of the tile's output bytes is staged in shared memory at tile-local
+// byte offsets (random reads, independent of the look-back), warp 0 resolves
+// the tile's global base with a warp-wide look-back (32 predecessors per round
+// trip), and the output is written with aligned 16-byte stores funnel-shifted
+// out of smem.  Tiles larger than the stage are processed window by window.
+// Boundary chunks use byte stores, so neighbouring tiles never race.
 #include "husky_internal.cuh"
 #include "kernels.cuh"
 
@@ -36,7 +37,8 @@ __global__ void __launch_bounds__(kGatherThreads)
              int64_t *__restrict__ sorted_offsets, unsigned long long *lb, uint32_t *tile_counter,
              uint32_t epoch, const int64_t *base_ptr, int dbg, const uint64_t *__restrict__ codes) {
   constexpr int W = CoderTraits<CODER>::kUnitBytes;
-  __shared__ __align__(16) uint8_t stage[kGatherStage + 32];
+  constexpr uint32_t PL = CoderTraits<CODER>::kPL;
+  extern __shared__ __align__(16) uint8_t stage[];  // kGatherStage + 32 bytes
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_wt[kGatherThreads / 32 + 1];
   __shared__ unsigned long long s_base;
@@ -47,39 +49,36 @@ __global__ void __launch_bounds__(kGatherThreads)
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint64_t p0 = (uint64_t)tile * kGatherTile + (uint64_t)tid * kGatherItems;
-#ifdef HUSKY_TRACE
-  if (tid == 0) printf("[husky trace] gather start tile %u n %llu gbase %llu\n", tile, (unsigned long long)n, gbase);
-#endif
 
-  constexpr uint32_t PL = CoderTraits<CODER>::kPL;
-  uint32_t idx[kGatherItems];
+  // per item: len (units) and either the source offset or, for strings rebuilt
+  // from their code, the code itself (bit j of `dec`)
+  uint32_t raw[kGatherItems];
 #pragma unroll
-  for (int j = 0; j < kGatherItems; ++j) idx[j] = p0 + j < n ? perm[p0 + j] : 0xFFFFFFFFu;
-  int64_t src[kGatherItems];  // -1: rebuild from the code
-  uint64_t len[kGatherItems];
-  uint64_t code[kGatherItems];
+  for (int j = 0; j < kGatherItems; ++j) raw[j] = p0 + j < n ? perm[p0 + j] : 0xFFFFFFFFu;
+  uint64_t sv[kGatherItems];
+  uint32_t len[kGatherItems];
+  uint32_t dec = 0;
   unsigned long long mine = 0;
 #pragma unroll
   for (int j = 0; j < kGatherItems; ++j) {
-    code[j] = 0;
-    if (idx[j] == 0xFFFFFFFFu) {
-      src[j] = 0;
+    if (raw[j] == 0xFFFFFFFFu) {
+      sv[j] = 0;
       len[j] = 0;
     } else {
-      uint32_t lc = 15;
+      uint32_t idx = raw[j], lc = 15;
       if (PACKED) {
-        lc = idx[j] >> 28;
-        idx[j] &= 0x0FFFFFFFu;
-        perm[p0 + j] = idx[j];
+        lc = idx >> 28;
+        idx &= 0x0FFFFFFFu;
+        perm[p0 + j] = idx;
       }
       if (PACKED && lc <= PL) {
-        src[j] = -1;
+        dec |= 1u << j;
         len[j] = lc;
-        code[j] = __ldg(codes + p0 + j);
+        sv[j] = __ldg(codes + p0 + j);
       } else {
-        int64_t a = __ldg(offsets + idx[j]), b = __ldg(offsets + idx[j] + 1);
-        src[j] = a;
-        len[j] = (uint64_t)(b - a);
+        int64_t a = __ldg(offsets + idx), b = __ldg(offsets + idx + 1);
+        sv[j] = (uint64_t)a;
+        len[j] = (uint32_t)(b - a);
       }
     }
     mine += len[j];
@@ -91,29 +90,61 @@ __global__ void __launch_bounds__(kGatherThreads)
   const uint8_t *ub = (const uint8_t *)units;
   uint8_t *ob = (uint8_t *)sorted_units;
   const uint64_t tile_bytes = tile_total * W;
-  const bool staged = sorted_units != nullptr && tile_bytes <= (uint64_t)kGatherStage && !(dbg & 1);
-  if (staged) {  // stage at tile-local byte offsets (needs no global base)
+  const bool direct = (dbg & 1) != 0;
+
+  // stage tile-local output bytes [w0, w1) of this thread's strings at stage[x - w0]
+  auto stage_window = [&](uint64_t w0, uint64_t w1) {
     uint64_t d = excl_t * W;
 #pragma unroll
     for (int j = 0; j < kGatherItems; ++j) {
-      uint64_t nb = len[j] * W;
-      if (PACKED && src[j] < 0) {
-        for (int b = 0; b < (int)nb; ++b) stage[d + b] = decode_byte<CODER>(code[j], b);
-        d += nb;
-        continue;
-      }
-      const uint8_t *sp = ub + src[j] * W;
-      for (uint64_t c = 0; c < nb; c += 8) {
-        int take = (int)(nb - c < 8 ? nb - c : 8);
-        uint64_t v = load8_unaligned(sp + c, take);
-        for (int b = 0; b < take; ++b) stage[d + c + b] = (uint8_t)(v >> (8 * b));
+      const uint64_t nb = (uint64_t)len[j] * W;
+      const uint64_t lo = d > w0 ? d : w0, hi = d + nb < w1 ? d + nb : w1;
+      if (lo < hi) {
+        if (PACKED && ((dec >> j) & 1)) {
+          for (uint64_t x = lo; x < hi; ++x) stage[x - w0] = decode_byte<CODER>(sv[j], (int)(x - d));
+        } else {
+          const uint8_t *sp = ub + sv[j] * W;
+          for (uint64_t x = lo; x < hi; x += 8) {
+            int take = (int)(hi - x < 8 ? hi - x : 8);
+            uint64_t v = load8_unaligned(sp + (x - d), take);
+            for (int b = 0; b < take; ++b) stage[x - w0 + b] = (uint8_t)(v >> (8 * b));
+          }
+        }
       }
       d += nb;
     }
-  }
+  };
+  // write tile-local bytes [w0, w1) (staged at stage[x - w0]) to g0 + x
+  auto write_window = [&](uint8_t *g0, uint64_t w0, uint64_t w1) {
+    const uint32_t align = (uint32_t)((uintptr_t)g0 & 15);
+    uint8_t *a0 = g0 - align;  // 16-aligned; tile byte x lives at a0 + align + x
+    const uint64_t lo_b = align + w0, hi_b = align + w1;
+    const uint64_t c0 = lo_b / 16, c1 = (hi_b + 15) / 16;
+    const uint32_t *sw = reinterpret_cast<const uint32_t *>(stage);
+    for (uint64_t ch = c0 + tid; ch < c1; ch += kGatherThreads) {
+      uint64_t lo = ch * 16, hi = lo + 16;
+      if (lo >= lo_b && hi <= hi_b) {
+        uint32_t so = (uint32_t)(lo - lo_b);  // stage offset of the chunk
+        uint32_t wi = so >> 2, sh = (so & 3) * 8;
+        uint32_t x0 = sw[wi], x1 = sw[wi + 1], x2 = sw[wi + 2], x3 = sw[wi + 3], x4 = sw[wi + 4];
+        uint4 o;
+        o.x = __funnelshift_r(x0, x1, sh);
+        o.y = __funnelshift_r(x1, x2, sh);
+        o.z = __funnelshift_r(x2, x3, sh);
+        o.w = __funnelshift_r(x3, x4, sh);
+        *reinterpret_cast<uint4 *>(a0 + lo) = o;
+      } else {
+        for (uint64_t b = (lo > lo_b ? lo : lo_b); b < (hi < hi_b ? hi : hi_b); ++b) a0[b] = stage[b - lo_b];
+      }
+    }
+  };
+
+  const uint64_t first_w1 = tile_bytes < (uint64_t)kGatherStage ? tile_bytes : (uint64_t)kGatherStage;
+  if (sorted_units && !direct) stage_window(0, first_w1);  // overlaps the look-back
 
   if (warp == 0) {
-    unsigned long long ex = tile == 0 ? 0ull : ((dbg & 2) ? lookback(lb, tile, 1, epoch) : warp_lookback(lb, tile, epoch));
+    unsigned long long ex =
+        tile == 0 ? 0ull : ((dbg & 2) ? lookback(lb, tile, 1, epoch) : warp_lookback(lb, tile, epoch));
     if (lane == 0) {
       if (tile != 0) st_relaxed_u64(lb + tile, make_flag(kFlagInc, epoch, ex + tile_total));
       s_base = ex;
@@ -133,41 +164,27 @@ __global__ void __launch_bounds__(kGatherThreads)
   if (sorted_units == nullptr) return;
 
   uint8_t *g0 = ob + tbase * W;  // first output byte of the tile
-  if (staged) {
-    // global chunk ch covers [a0 + 16 ch, +16); its bytes sit at stage[16 ch - align ..)
-    const uint32_t align = (uint32_t)((uintptr_t)g0 & 15);
-    uint8_t *a0 = g0 - align;  // 16-aligned
-    const uint64_t end = align + tile_bytes;
-    const uint64_t nchunks = (end + 15) / 16;
-    const uint32_t *sw = reinterpret_cast<const uint32_t *>(stage);
-    for (uint64_t ch = tid; ch < nchunks; ch += kGatherThreads) {
-      uint64_t lo = ch * 16, hi = lo + 16;
-      if (lo >= align && hi <= end) {
-        uint32_t so = (uint32_t)(lo - align);  // stage byte offset of the chunk
-        uint32_t wi = so >> 2, sh = (so & 3) * 8;
-        uint32_t w0 = sw[wi], w1 = sw[wi + 1], w2 = sw[wi + 2], w3 = sw[wi + 3], w4 = sw[wi + 4];
-        uint4 o;
-        o.x = __funnelshift_r(w0, w1, sh);
-        o.y = __funnelshift_r(w1, w2, sh);
-        o.z = __funnelshift_r(w2, w3, sh);
-        o.w = __funnelshift_r(w3, w4, sh);
-        *reinterpret_cast<uint4 *>(a0 + lo) = o;
-      } else {
-        for (uint64_t b = (lo > align ? lo : align); b < (hi < end ? hi : end); ++b) a0[b] = stage[b - align];
-      }
+  if (!direct) {
+    write_window(g0, 0, first_w1);
+    for (uint64_t w0 = first_w1; w0 < tile_bytes; w0 += kGatherStage) {  // large tiles: more windows
+      const uint64_t w1 = w0 + kGatherStage < tile_bytes ? w0 + kGatherStage : tile_bytes;
+      __syncthreads();
+      stage_window(w0, w1);
+      __syncthreads();
+      write_window(g0, w0, w1);
     }
   } else {
-    // long strings: warp-cooperative byte copy, one string at a time per warp
+    // debug path: warp-cooperative byte copy, one string at a time per warp
     for (int t = 0; t < 32; ++t) {
       uint64_t d = tbase + __shfl_sync(0xFFFFFFFFu, excl_t, t);
+      uint32_t dt = __shfl_sync(0xFFFFFFFFu, dec, t);
 #pragma unroll
       for (int j = 0; j < kGatherItems; ++j) {
-        int64_t s = __shfl_sync(0xFFFFFFFFu, src[j], t);
-        uint64_t l = __shfl_sync(0xFFFFFFFFu, len[j], t);
-        uint64_t cd = __shfl_sync(0xFFFFFFFFu, code[j], t);
-        uint64_t nb = l * W;
-        if (PACKED && s < 0) {
-          for (uint64_t b = lane; b < nb; b += 32) ob[d * W + b] = decode_byte<CODER>(cd, (int)b);
+        uint64_t s = __shfl_sync(0xFFFFFFFFu, sv[j], t);
+        uint32_t l = __shfl_sync(0xFFFFFFFFu, len[j], t);
+        uint64_t nb = (uint64_t)l * W;
+        if (PACKED && ((dt >> j) & 1)) {
+          for (uint64_t b = lane; b < nb; b += 32) ob[d * W + b] = decode_byte<CODER>(s, (int)b);
         } else {
           for (uint64_t b = lane; b < nb; b += 32) ob[d * W + b] = ub[s * W + b];
         }
@@ -182,6 +199,15 @@ void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, con
                    uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, const int64_t *base_ptr,
                    const uint64_t *packed_codes) {
   if (n == 0) return;
+  constexpr int kSmem = kGatherStage + 32;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_gather<HUSKY_CODER_ASCII, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_gather<HUSKY_CODER_ASCII, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_gather<HUSKY_CODER_UNICODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_gather<HUSKY_CODER_UNICODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    configured = true;
+  }
   Scope sc_(ST_GATHER, s, n);
   dim3 g((unsigned)gather_tiles(n)), b(kGatherThreads);
   // HUSKY_DEBUG_GATHER: bit 0 forces the unstaged copy, bit 1 the serial look-back
@@ -191,11 +217,11 @@ void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, con
   }();
 #define G_ARGS perm, n, units, offsets, sorted_units, sorted_offsets, lb, tile_counter, epoch, base_ptr, dbg, packed_codes
   if (coder == HUSKY_CODER_ASCII) {
-    if (packed_codes) k_gather<HUSKY_CODER_ASCII, true><<<g, b, 0, s>>>(G_ARGS);
-    else k_gather<HUSKY_CODER_ASCII, false><<<g, b, 0, s>>>(G_ARGS);
+    if (packed_codes) k_gather<HUSKY_CODER_ASCII, true><<<g, b, kSmem, s>>>(G_ARGS);
+    else k_gather<HUSKY_CODER_ASCII, false><<<g, b, kSmem, s>>>(G_ARGS);
   } else {
-    if (packed_codes) k_gather<HUSKY_CODER_UNICODE, true><<<g, b, 0, s>>>(G_ARGS);
-    else k_gather<HUSKY_CODER_UNICODE, false><<<g, b, 0, s>>>(G_ARGS);
+    if (packed_codes) k_gather<HUSKY_CODER_UNICODE, true><<<g, b, kSmem, s>>>(G_ARGS);
+    else k_gather<HUSKY_CODER_UNICODE, false><<<g, b, kSmem, s>>>(G_ARGS);
   }
 #undef G_ARGS
 }
@@ -231,9 +257,6 @@ __global__ void __launch_bounds__(256)
   for (uint32_t e = blockIdx.x; e < ns + nm; e += gridDim.x) {
     uint2 ent = e < ns ? list[e] : list[cap - 1 - (e - ns)];
     const uint32_t start = ent.x, len = ent.y;
-#ifdef HUSKY_TRACE
-    if (threadIdx.x == 0) printf("[husky trace] regather entry %u/%u+%u: start %u len %u\n", e, ns, nm, start, len);
-#endif
     const unsigned long long base = (unsigned long long)sorted_offsets[start];
     unsigned long long running = 0;
     for (uint32_t c = 0; c < len; c += 256) {
@@ -259,9 +282,6 @@ __global__ void __launch_bounds__(256)
       running += tot;
       __syncthreads();
     }
-#ifdef HUSKY_TRACE
-    if (threadIdx.x == 0) printf("[husky trace] regather entry %u done: running %llu\n", e, running);
-#endif
   }
 }
 

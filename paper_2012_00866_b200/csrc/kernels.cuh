@@ -41,7 +41,10 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
 void launch_iota(uint32_t *perm, uint64_t n, cudaStream_t s);
 
 // A3 run detection (single-pass scan with decoupled look-back)
-constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+constexpr int kScanThreads = 512, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+// padded smem staging sizes of k_runs_scan (one pad u64 every 8, one pad u32 every 32)
+constexpr int kScanKP = kScanTile + 2 + (kScanTile + 2) / 8 + 1;
+constexpr int kScanPP = kScanTile + 2 + (kScanTile + 2) / 32 + 1;
 inline uint64_t scan_tiles(uint64_t n) { return (n + kScanTile - 1) / kScanTile; }
 // mode 0: keys are husky codes; a pair inside a run is checked with the exact
 //         equal-code comparator (strings via perm -> offsets -> units).
@@ -70,8 +73,9 @@ void launch_seg_key2(int coder, const uint32_t *perm_seg, uint64_t len, const vo
                      int num_sms, cudaStream_t s);
 
 // A4 gather
+// small tiles, many CTAs: the gather is bound by the latency of random reads
 constexpr int kGatherThreads = 256, kGatherItems = 4, kGatherTile = kGatherThreads * kGatherItems;
-constexpr int kGatherStage = 32 * 1024;
+constexpr int kGatherStage = 24 * 1024;  // one window of output bytes (dynamic smem)
 inline uint64_t gather_tiles(uint64_t n) { return (n + kGatherTile - 1) / kGatherTile; }
 // base_ptr (nullable): device pointer to the first output offset of a span
 // re-gather (positions start there); NULL = 0.

@@ -29,11 +29,11 @@ __global__ void __launch_bounds__(kScanThreads)
   // Tile staging in smem (coalesced async copies).  Each thread then works on
   // kScanItems consecutive positions; the arrays are padded (one pad element
   // every 8 u64 / 32 u32) so that blocked per-thread reads do not bank-conflict.
-  constexpr int KP = kScanTile + 2 + (kScanTile + 2) / 8 + 1;
   constexpr bool SO = MODE == 2;
-  __shared__ uint64_t s_keys[KP];                                  // keys[tile_base - 1 + i]
-  __shared__ int64_t s_soff[SO ? KP : 1];                          // soffs[tile_base + i]
-  __shared__ uint32_t s_perm[SO ? kScanTile + 2 + (kScanTile + 2) / 32 + 1 : 1];  // perm[tile_base + i]
+  extern __shared__ __align__(16) uint8_t dsm[];  // runs_scan_smem(mode) bytes
+  uint64_t *s_keys = reinterpret_cast<uint64_t *>(dsm);                 // keys[tile_base - 1 + i]
+  int64_t *s_soff = reinterpret_cast<int64_t *>(dsm + kScanKP * 8);      // soffs[tile_base + i]
+  uint32_t *s_perm = reinterpret_cast<uint32_t *>(dsm + kScanKP * 16);   // perm[tile_base + i]
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_wt[kScanThreads / 32 + 1];
   __shared__ unsigned long long s_excl;
@@ -134,19 +134,31 @@ void launch_runs_scan(int coder, int mode, const uint64_t *keys, uint64_t n, con
                       uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, const void *sunits,
                       const int64_t *soffs) {
   if (n == 0) return;
+  // staging: keys (all modes) + sorted offsets and perm (mode 2), padded
+  constexpr int kSmem0 = kScanKP * 8, kSmem2 = kScanKP * 16 + kScanPP * 4;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_ASCII, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
+    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_ASCII, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
+    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_ASCII, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_UNICODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
+    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_UNICODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
+    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_UNICODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+    configured = true;
+  }
   Scope sc_(ST_RUNS_SCAN, s, n);
   dim3 g((unsigned)scan_tiles(n)), b(kScanThreads);
 #define RS_ARGS \
   keys, n, perm, units, offsets, base, run_start, run_end, dirty, st, lb, tile_counter, epoch, sunits, soffs
   if (mode == 0 && sunits) mode = 2;
   if (coder == HUSKY_CODER_ASCII) {
-    if (mode == 0) k_runs_scan<HUSKY_CODER_ASCII, 0><<<g, b, 0, s>>>(RS_ARGS);
-    else if (mode == 2) k_runs_scan<HUSKY_CODER_ASCII, 2><<<g, b, 0, s>>>(RS_ARGS);
-    else k_runs_scan<HUSKY_CODER_ASCII, 1><<<g, b, 0, s>>>(RS_ARGS);
+    if (mode == 0) k_runs_scan<HUSKY_CODER_ASCII, 0><<<g, b, kSmem0, s>>>(RS_ARGS);
+    else if (mode == 2) k_runs_scan<HUSKY_CODER_ASCII, 2><<<g, b, kSmem2, s>>>(RS_ARGS);
+    else k_runs_scan<HUSKY_CODER_ASCII, 1><<<g, b, kSmem0, s>>>(RS_ARGS);
   } else {
-    if (mode == 0) k_runs_scan<HUSKY_CODER_UNICODE, 0><<<g, b, 0, s>>>(RS_ARGS);
-    else if (mode == 2) k_runs_scan<HUSKY_CODER_UNICODE, 2><<<g, b, 0, s>>>(RS_ARGS);
-    else k_runs_scan<HUSKY_CODER_UNICODE, 1><<<g, b, 0, s>>>(RS_ARGS);
+    if (mode == 0) k_runs_scan<HUSKY_CODER_UNICODE, 0><<<g, b, kSmem0, s>>>(RS_ARGS);
+    else if (mode == 2) k_runs_scan<HUSKY_CODER_UNICODE, 2><<<g, b, kSmem2, s>>>(RS_ARGS);
+    else k_runs_scan<HUSKY_CODER_UNICODE, 1><<<g, b, kSmem0, s>>>(RS_ARGS);
   }
 #undef RS_ARGS
 }
