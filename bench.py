@@ -133,7 +133,8 @@ def make_config(args, n, coder, world):
     return {"workload": DESCR[args.config], "n_per_gpu": n, "coder": "ascii" if coder == 0 else "unicode",
             "outputs": "perm + sorted units + sorted offsets",
             "l2": "256 MiB buffer written between timed steps (outside the step events)",
-            "parallelism": f"sample sort over {world} GPU(s)" if world > 1 else "1 GPU"}
+            "parallelism": (f"sample sort over {world} GPU(s)" if world > 1 or getattr(args, "force_multi", False)
+                            else "1 GPU")}
 
 
 def run_reference(args):
@@ -191,7 +192,7 @@ def run_ours(args):
     total_units = w.units.size
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    if world == 1:
+    if world == 1 and not args.force_multi:
         ws = torch.empty(h.husky_sort_workspace(w.coder, n, total_units), dtype=torch.uint8, device=dev)
         perm = torch.empty(n, dtype=torch.int32, device=dev)
         su = torch.empty(total_units + 8, dtype=d_units.dtype, device=dev)
@@ -200,7 +201,11 @@ def run_ours(args):
         def step():
             return h.husky_sort(w.coder, d_units, d_off, perm, su, so, ws)
     else:
-        comm = h.multi.comm_from_process_group(device=dev)
+        if world > 1:
+            comm = h.multi.comm_from_process_group(device=dev)
+        else:  # --force-multi on one GPU: the NCCL sample-sort path with a 1-rank communicator
+            comm = h.husky_comm_create(0, 1, h.husky_comm_unique_id())
+            h.multi._WORLD[comm.value] = 1
         gbase = rank * n
 
         def step():
@@ -281,7 +286,7 @@ def run_ours(args):
         hp = torch.empty(n, dtype=torch.int32).pin_memory()
         hsu = torch.empty(total_units + 8, dtype=d_units.dtype).pin_memory()
         hso = torch.empty(n + 1, dtype=torch.int64).pin_memory()
-        del ws
+        ws = None  # free the device workspace before the host-API workspace
         torch.cuda.empty_cache()
         hws = torch.empty(h.husky_sort_host_workspace(w.coder, n, total_units), dtype=torch.uint8, device=dev)
         for _ in range(max(1, args.warmup)):
@@ -332,6 +337,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=10_000_000)
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-multi", action="store_true",
+                    help="run the NCCL sample-sort path even on one GPU (validation)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
