@@ -21,12 +21,13 @@ namespace husky {
 template <int CODER>
 __global__ void __launch_bounds__(256)
     k_fix_small(const uint2 *__restrict__ list, const DevState *st, uint32_t *perm,
-                const void *__restrict__ units, const int64_t *__restrict__ offsets) {
+                const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t first) {
   using T = CoderTraits<CODER>;
+  if (st->violations & kOffsetsBad) return;
   const uint32_t lane = lane_id();
   const uint32_t nsmall = st->n_small;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < nsmall; e += warps) {
+  for (uint32_t e = first + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < nsmall; e += warps) {
     uint2 ent = list[e];
     const uint32_t start = ent.x, len = ent.y;
     uint32_t my = lane < len ? perm[start + lane] : 0xFFFFFFFFu;
@@ -44,11 +45,12 @@ __global__ void __launch_bounds__(256)
 template <int CODER>
 __global__ void __launch_bounds__(1024)
     k_fix_medium(const uint2 *__restrict__ list, uint64_t cap, const DevState *st, uint32_t *perm,
-                 const void *__restrict__ units, const int64_t *__restrict__ offsets) {
+                 const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t first) {
   using T = CoderTraits<CODER>;
   __shared__ uint32_t s[kMediumMax];
+  if (st->violations & kOffsetsBad) return;
   const uint32_t nmed = st->n_medium;
-  for (uint32_t e = blockIdx.x; e < nmed; e += gridDim.x) {
+  for (uint32_t e = first + blockIdx.x; e < nmed; e += gridDim.x) {
     uint2 ent = list[cap - 1 - e];
     const uint32_t start = ent.x, len = ent.y;
 #ifdef HUSKY_TRACE
@@ -82,22 +84,24 @@ __global__ void __launch_bounds__(1024)
 }
 
 void launch_fix_small(int coder, const uint2 *list_sm, const DevState *st, uint32_t *perm,
-                      const void *units, const int64_t *offsets, int num_sms, cudaStream_t s) {
+                      const void *units, const int64_t *offsets, int num_sms, cudaStream_t s, uint32_t first) {
   Scope sc_(ST_FIX_SMALL, s, 0);
   dim3 g(num_sms * 4), b(256);
-  if (coder == HUSKY_CODER_ASCII) k_fix_small<HUSKY_CODER_ASCII><<<g, b, 0, s>>>(list_sm, st, perm, units, offsets);
-  else k_fix_small<HUSKY_CODER_UNICODE><<<g, b, 0, s>>>(list_sm, st, perm, units, offsets);
+  if (coder == HUSKY_CODER_ASCII)
+    k_fix_small<HUSKY_CODER_ASCII><<<g, b, 0, s>>>(list_sm, st, perm, units, offsets, first);
+  else
+    k_fix_small<HUSKY_CODER_UNICODE><<<g, b, 0, s>>>(list_sm, st, perm, units, offsets, first);
 }
 
 void launch_fix_medium(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                        uint32_t *perm, const void *units, const int64_t *offsets, int num_sms,
-                       cudaStream_t s) {
+                       cudaStream_t s, uint32_t first) {
   Scope sc_(ST_FIX_MEDIUM, s, 0);
   dim3 g(num_sms), b(1024);
   if (coder == HUSKY_CODER_ASCII)
-    k_fix_medium<HUSKY_CODER_ASCII><<<g, b, 0, s>>>(list_sm, cap_sm, st, perm, units, offsets);
+    k_fix_medium<HUSKY_CODER_ASCII><<<g, b, 0, s>>>(list_sm, cap_sm, st, perm, units, offsets, first);
   else
-    k_fix_medium<HUSKY_CODER_UNICODE><<<g, b, 0, s>>>(list_sm, cap_sm, st, perm, units, offsets);
+    k_fix_medium<HUSKY_CODER_UNICODE><<<g, b, 0, s>>>(list_sm, cap_sm, st, perm, units, offsets, first);
 }
 
 // ------------------------------------------------------------------ A6

@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(kGatherThreads)
     k_gather(uint32_t *__restrict__ perm, uint64_t n, const void *__restrict__ units,
              const int64_t *__restrict__ offsets, void *__restrict__ sorted_units,
              int64_t *__restrict__ sorted_offsets, unsigned long long *lb, uint32_t *tile_counter,
-             uint32_t epoch, const int64_t *base_ptr, int dbg, const uint64_t *__restrict__ codes) {
+             uint32_t epoch, const int64_t *base_ptr, int dbg, const uint64_t *__restrict__ codes,
+             const DevState *st) {
   constexpr int W = CoderTraits<CODER>::kUnitBytes;
   constexpr uint32_t PL = CoderTraits<CODER>::kPL;
   extern __shared__ __align__(16) uint8_t stage[];  // kGatherStage + 32 bytes
@@ -43,6 +44,10 @@ __global__ void __launch_bounds__(kGatherThreads)
   __shared__ unsigned long long s_wt[kGatherThreads / 32 + 1];
   __shared__ unsigned long long s_base;
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  if (st) {
+    if (st->violations & kOffsetsBad) return;  // invalid input: reported by the caller
+    if (PACKED && codes == nullptr) codes = reinterpret_cast<const uint64_t *>(st->sorted_keys);
+  }
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   // re-gather of a span: output positions start at *base_ptr (unchanged by us)
   const unsigned long long gbase = base_ptr ? (unsigned long long)*base_ptr : 0ull;
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(kGatherThreads)
 void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, const int64_t *offsets,
                    void *sorted_units, int64_t *sorted_offsets, unsigned long long *lb,
                    uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, const int64_t *base_ptr,
-                   const uint64_t *packed_codes) {
+                   bool packed, const uint64_t *packed_codes, const DevState *st) {
   if (n == 0) return;
   constexpr int kSmem = kGatherStage + 32;
   static bool configured = false;
@@ -215,12 +220,13 @@ void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, con
     const char *v = getenv("HUSKY_DEBUG_GATHER");
     return v ? atoi(v) : 0;
   }();
-#define G_ARGS perm, n, units, offsets, sorted_units, sorted_offsets, lb, tile_counter, epoch, base_ptr, dbg, packed_codes
+#define G_ARGS \
+  perm, n, units, offsets, sorted_units, sorted_offsets, lb, tile_counter, epoch, base_ptr, dbg, packed_codes, st
   if (coder == HUSKY_CODER_ASCII) {
-    if (packed_codes) k_gather<HUSKY_CODER_ASCII, true><<<g, b, kSmem, s>>>(G_ARGS);
+    if (packed) k_gather<HUSKY_CODER_ASCII, true><<<g, b, kSmem, s>>>(G_ARGS);
     else k_gather<HUSKY_CODER_ASCII, false><<<g, b, kSmem, s>>>(G_ARGS);
   } else {
-    if (packed_codes) k_gather<HUSKY_CODER_UNICODE, true><<<g, b, kSmem, s>>>(G_ARGS);
+    if (packed) k_gather<HUSKY_CODER_UNICODE, true><<<g, b, kSmem, s>>>(G_ARGS);
     else k_gather<HUSKY_CODER_UNICODE, false><<<g, b, kSmem, s>>>(G_ARGS);
   }
 #undef G_ARGS
@@ -248,14 +254,16 @@ __global__ void __launch_bounds__(256)
     k_regather_runs(const uint2 *__restrict__ list, uint64_t cap, const DevState *st,
                     const uint32_t *__restrict__ perm, const void *__restrict__ units,
                     const int64_t *__restrict__ offsets, void *__restrict__ sorted_units,
-                    int64_t *__restrict__ sorted_offsets) {
+                    int64_t *__restrict__ sorted_offsets, uint32_t first_small, uint32_t first_medium) {
   constexpr int W = CoderTraits<CODER>::kUnitBytes;
   __shared__ unsigned long long s_wt[256 / 32 + 1];
-  const uint32_t ns = st->n_small, nm = st->n_medium;
+  if (st->violations & kOffsetsBad) return;
+  // entries [first_small, n_small) of the small list, then [first_medium, n_medium) of the medium list
+  const uint32_t ns = st->n_small - first_small, nm = st->n_medium - first_medium;
   const uint8_t *ub = (const uint8_t *)units;
   uint8_t *ob = (uint8_t *)sorted_units;
   for (uint32_t e = blockIdx.x; e < ns + nm; e += gridDim.x) {
-    uint2 ent = e < ns ? list[e] : list[cap - 1 - (e - ns)];
+    uint2 ent = e < ns ? list[first_small + e] : list[cap - 1 - (first_medium + e - ns)];
     const uint32_t start = ent.x, len = ent.y;
     const unsigned long long base = (unsigned long long)sorted_offsets[start];
     unsigned long long running = 0;
@@ -287,15 +295,16 @@ __global__ void __launch_bounds__(256)
 
 void launch_regather_runs(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                           const uint32_t *perm, const void *units, const int64_t *offsets,
-                          void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s) {
+                          void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s,
+                          uint32_t first_small, uint32_t first_medium) {
   Scope sc_(ST_FIX_SMALL, s, 0);
   dim3 g(num_sms * 4), b(256);
   if (coder == HUSKY_CODER_ASCII)
     k_regather_runs<HUSKY_CODER_ASCII><<<g, b, 0, s>>>(list_sm, cap_sm, st, perm, units, offsets, sorted_units,
-                                                       sorted_offsets);
+                                                       sorted_offsets, first_small, first_medium);
   else
     k_regather_runs<HUSKY_CODER_UNICODE><<<g, b, 0, s>>>(list_sm, cap_sm, st, perm, units, offsets, sorted_units,
-                                                         sorted_offsets);
+                                                         sorted_offsets, first_small, first_medium);
 }
 
 }  // namespace husky

@@ -6,9 +6,10 @@
 //   determine whether our encoding was perfect")  ->  fix-up
 //   of dirty runs (A5, the cleanup of Alg. 1 line 5 restricted to where
 //   inversions can be) with giant-run refinement (A6)  ->  gather (A4).
-// Host<->device synchronisation points: after the histogram scan (trivial-pass
-// mask, input violations), after run classification (giant-run count), once per
-// giant refinement round, and at the end (outcome).
+// Host<->device synchronisation: ONE per sort on the common path (the outcome,
+// read after the re-gather); the radix pass plan is made on device and input
+// violations turn later kernels into no-ops.  Only inputs with giant dirty runs
+// (A6) add one synchronisation per refinement round.
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -118,6 +119,9 @@ static husky_status cuda_check(const char *where) {
     if (e_ != cudaSuccess) return fail(HUSKY_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
   } while (0)
 
+static husky_status refine_giants(Sorter &S, const DevState &hs0, void *d_sorted_units, int64_t *d_sorted_offsets,
+                                  DevState *out);
+
 husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
                        uint32_t *d_perm, void *d_sorted_units, int64_t *d_sorted_offsets, void *d_ws,
                        size_t ws_bytes, husky_outcome *h_out, cudaStream_t s) {
@@ -163,19 +167,19 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   uint32_t *packed_payload = packed ? S.at<uint32_t>(L.vals2) : nullptr;
   launch_encode(coder, true, d_units, d_offsets, n, S.keysA(), st, S.sms, s, packed_payload);
   launch_hist_scan(n, st, s);
-  HostSnap snap;
-  HCHECK(cudaMemcpyAsync(&snap, &st->trivial_mask, sizeof snap, cudaMemcpyDeviceToHost, s));
-  HCHECK(cudaStreamSynchronize(s));
-  if (husky_status e = cuda_check("encode")) return e;
-  if (snap.violations & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing");
-  if (coder == HUSKY_CODER_ASCII && (snap.violations & kDomainBad))
-    return fail(HUSKY_ERR_DOMAIN, "ASCII coder: a unit > 0x7F inside a code prefix (Alg. 4 mask is not monotone there)");
 
-  // ---- A2 key sort: (code, index) -> sorted codes, perm
-  uint64_t *sorted_codes = nullptr;
-  if (husky_status e = S.radix(S.keysA(), packed_payload, n, snap.trivial_mask, d_perm, S.at<uint32_t>(L.vals),
-                               &sorted_codes))
-    return e;
+  // ---- A2 key sort: (code, index) -> sorted codes, perm.  The pass plan (which
+  // digits are not shared by all keys) is made on device, so the host enqueues
+  // all 8 pass slots without waiting; slots beyond the plan exit at once.  Input
+  // violations (bad offsets, ASCII domain) make every later kernel a no-op and
+  // are reported at the single synchronisation below.
+  uint64_t *keysA = S.keysA(), *keysB = S.keysB();
+  uint32_t *vals_tmp = S.at<uint32_t>(L.vals);
+  launch_radix_plan(st, keysA, keysB, s);
+  for (int slot = 0; slot < 8; ++slot)
+    launch_onesweep_slot(slot, keysA, keysB, packed_payload, d_perm, vals_tmp, n, st, S.lb_radix(),
+                         S.next_counter(), S.next_epoch(), s);
+  launch_radix_finalize(st, packed_payload, d_perm, n, s);
   if (packed && !d_sorted_units) launch_unpack_perm(d_perm, n, s);  // the gather unpacks otherwise
 
   // ---- A4 gather in (code, index) order.  Done BEFORE the fix-up: the order
@@ -184,27 +188,81 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // reorders are gathered again (rare outside all-colliding inputs).
   if (d_sorted_units)
     launch_gather(coder, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),
-                  S.next_counter(), S.next_epoch(), s, nullptr, packed ? sorted_codes : nullptr);
+                  S.next_counter(), S.next_epoch(), s, nullptr, packed, nullptr, st);
   debug_check_perm(d_perm, n, "key sort", s);
 
-  // ---- A3 run detection + order check, classification
+  // ---- A3 run detection + order check (keys: DevState::sorted_keys), classification
   uint32_t *run_start = S.at<uint32_t>(L.run_start), *run_end = S.at<uint32_t>(L.run_end);
   uint8_t *dirty = S.at<uint8_t>(L.dirty);
   uint2 *list_sm = S.at<uint2>(L.list_sm), *list_g = S.at<uint2>(L.list_g);
   HCHECK(cudaMemsetAsync(dirty, 0, L.cap_sm, s));
-  launch_runs_scan(coder, 0, sorted_codes, n, d_perm, d_units, d_offsets, 0, run_start, run_end, dirty, st,
+  launch_runs_scan(coder, 0, nullptr, n, d_perm, d_units, d_offsets, 0, run_start, run_end, dirty, st,
                    S.lb_scan(), S.next_counter(), S.next_epoch(), s, d_sorted_units, d_sorted_offsets);
   launch_runs_classify(run_start, run_end, dirty, st, list_sm, L.cap_sm, list_g, true, S.sms, s);
-  uint32_t n_giant = 0;
-  HCHECK(cudaMemcpyAsync(&n_giant, &st->n_giant, 4, cudaMemcpyDeviceToHost, s));
+
+  // ---- A5 fix-up of small / medium dirty runs (counts read on device), then
+  // A4 again for the spans it reordered.  Enqueued optimistically before the
+  // host knows whether there are giant runs: giant runs are disjoint from the
+  // small/medium ones, so their refinement below only appends list entries.
+  launch_fix_small(coder, list_sm, st, d_perm, d_units, d_offsets, S.sms, s);
+  launch_fix_medium(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s);
+  if (d_sorted_units)
+    launch_regather_runs(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, d_sorted_units,
+                         d_sorted_offsets, S.sms, s);
+  DevState hs;
+  HCHECK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, s));
   HCHECK(cudaStreamSynchronize(s));
-  if (husky_status e = cuda_check("radix/runs")) return e;
+  if (husky_status e = cuda_check("sort")) return e;
+  if (hs.violations & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing");
+  if (coder == HUSKY_CODER_ASCII && (hs.violations & kDomainBad))
+    return fail(HUSKY_ERR_DOMAIN, "ASCII coder: a unit > 0x7F inside a code prefix (Alg. 4 mask is not monotone there)");
+  S.radix_passes = hs.np;
+  debug_check_perm(d_perm, n, "fix-up", s);
 
   // ---- A6 giant-run refinement (rare: runs > 4096 strings with an inversion)
+  const uint32_t n_giant = hs.n_giant;
+  if (n_giant) {
+    if (husky_status e = refine_giants(S, hs, d_sorted_units, d_sorted_offsets, &hs)) return e;
+  }
+  if (h_out) {
+    h_out->perfect = !(hs.violations & kNotPerfect);
+    h_out->domain_ok = !(hs.violations & kDomainBad) || coder != HUSKY_CODER_ASCII;
+    h_out->n_in_runs = hs.n_in_runs;
+    h_out->max_run = hs.max_run;
+    for (int c = 0; c < 4; ++c) h_out->runs_by_class[c] = hs.runs_by_class[c];
+    h_out->n_runs = hs.runs_total;
+    h_out->refine_rounds = S.refine_rounds;
+    h_out->radix_passes = S.radix_passes;
+  }
+  return HUSKY_OK;
+}
+
+// A6: refine the giant dirty runs found by the main scan (host-driven loop, one
+// synchronisation per round), fix the small/medium sub-runs it appends to the
+// lists, and re-gather the affected spans.  hs: DevState after the main pass;
+// *out: DevState at the end.
+static husky_status refine_giants(Sorter &S, const DevState &hs0, void *d_sorted_units, int64_t *d_sorted_offsets,
+                                  DevState *out) {
+  const int coder = S.coder;
+  const Layout &L = S.L;
+  DevState *st = S.st;
+  cudaStream_t s = S.s;
+  const void *d_units = S.units;
+  const int64_t *d_offsets = S.offsets;
+  uint32_t *d_perm = S.perm;
+  const uint64_t n = S.n;
+  uint32_t *run_start = S.at<uint32_t>(L.run_start), *run_end = S.at<uint32_t>(L.run_end);
+  uint8_t *dirty = S.at<uint8_t>(L.dirty);
+  uint2 *list_sm = S.at<uint2>(L.list_sm), *list_g = S.at<uint2>(L.list_g);
+  // small/medium entries already fixed (and re-gathered) by the main pass
+  const uint32_t s0 = hs0.n_small, m0 = hs0.n_medium;
+  uint32_t n_giant = hs0.n_giant;
+  HostSnap snap;
+
   struct Seg { uint32_t start, len, from; };
   std::vector<Seg> queue;
   std::vector<uint2> giant_spans;  // top-level giant runs: re-gathered at the end
-  if (n_giant) {
+  {
     std::vector<uint2> g(n_giant);
     HCHECK(cudaMemcpy(g.data(), list_g, n_giant * sizeof(uint2), cudaMemcpyDeviceToHost));
     for (auto &x : g) queue.push_back({x.x, x.y, (uint32_t)(coder == HUSKY_CODER_ASCII ? 9 : 3)});
@@ -250,10 +308,10 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
     }
   }
 
-  // ---- A5 fix-up of small / medium dirty runs (counts read on device)
-  launch_fix_small(coder, list_sm, st, d_perm, d_units, d_offsets, S.sms, s);
-  launch_fix_medium(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s);
-  debug_check_perm(d_perm, n, "fix-up", s);
+  // ---- A5 fix-up of the small / medium sub-runs the refinement appended
+  launch_fix_small(coder, list_sm, st, d_perm, d_units, d_offsets, S.sms, s, s0);
+  launch_fix_medium(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s, m0);
+  debug_check_perm(d_perm, n, "refine fix-up", s);
 
   // ---- A4 (again) for the spans whose order the fix-up changed
   if (d_sorted_units) {
@@ -276,24 +334,13 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
                     S.lb_scan(), S.next_counter(), S.next_epoch(), s, d_sorted_offsets + g.x);
     dbg_so("after giant re-gather");
     launch_regather_runs(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, d_sorted_units,
-                         d_sorted_offsets, S.sms, s);
+                         d_sorted_offsets, S.sms, s, s0, m0);
     dbg_so("after run re-gather");
   }
 
-  DevState hs;
-  HCHECK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, s));
+  HCHECK(cudaMemcpyAsync(out, st, sizeof *out, cudaMemcpyDeviceToHost, s));
   HCHECK(cudaStreamSynchronize(s));
-  if (husky_status e = cuda_check("fixup/gather")) return e;
-  if (h_out) {
-    h_out->perfect = !(hs.violations & kNotPerfect);
-    h_out->domain_ok = !(hs.violations & kDomainBad) || coder != HUSKY_CODER_ASCII;
-    h_out->n_in_runs = hs.n_in_runs;
-    h_out->max_run = hs.max_run;
-    for (int c = 0; c < 4; ++c) h_out->runs_by_class[c] = hs.runs_by_class[c];
-    h_out->n_runs = hs.runs_total;
-    h_out->refine_rounds = S.refine_rounds;
-    h_out->radix_passes = S.radix_passes;
-  }
+  if (husky_status e = cuda_check("refine/fixup/gather")) return e;
   return HUSKY_OK;
 }
 

@@ -52,7 +52,12 @@ struct DevState {
   uint32_t seg_L;             // refinement: common-prefix length of the segment
   uint32_t seg_has_short;     // refinement: segment contains a string with len <= PL
   unsigned long long runs_total; // runs found by the main (code) scan
-  uint32_t pad[28];
+  // device-side radix plan (k_radix_plan): the non-trivial digits in pass order
+  // and which ping-pong key buffer ends up holding the sorted codes
+  uint32_t np;
+  uint32_t pass_digit[8];
+  unsigned long long sorted_keys;  // uint64_t* of the sorted keys
+  uint32_t pad[16];
 };
 
 // ----------------------------------------------------------- small helpers

@@ -39,6 +39,16 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
                      uint32_t *vals_out, uint64_t n, int digit, DevState *st,
                      unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
 void launch_iota(uint32_t *perm, uint64_t n, cudaStream_t s);
+// Device-planned passes (no host sync): k_radix_plan turns the trivial-digit
+// mask into DevState::np / pass_digit / sorted_keys; slots 0..7 are launched
+// unconditionally and resolve their digit and ping-pong buffers on device (the
+// last planned pass writes vals_final); finalize copies the payload when np == 0.
+void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, cudaStream_t s);
+void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint32_t *vals_init,
+                          uint32_t *vals_final, uint32_t *vals_tmp, uint64_t n, DevState *st,
+                          unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
+void launch_radix_finalize(const DevState *st, const uint32_t *vals_init, uint32_t *vals_final, uint64_t n,
+                           cudaStream_t s);
 
 // A3 run detection (single-pass scan with decoupled look-back)
 constexpr int kScanThreads = 512, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
@@ -59,11 +69,12 @@ void launch_runs_classify(const uint32_t *run_start, const uint32_t *run_end, co
                           bool count_stats, int num_sms, cudaStream_t s);
 
 // A5 fix-up of dirty runs (lists filled by classify; counts read on device)
+// entries [first, count) of each list (first > 0: the round after a refinement)
 void launch_fix_small(int coder, const uint2 *list_sm, const DevState *st, uint32_t *perm,
-                      const void *units, const int64_t *offsets, int num_sms, cudaStream_t s);
+                      const void *units, const int64_t *offsets, int num_sms, cudaStream_t s, uint32_t first = 0);
 void launch_fix_medium(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                        uint32_t *perm, const void *units, const int64_t *offsets, int num_sms,
-                       cudaStream_t s);
+                       cudaStream_t s, uint32_t first = 0);
 
 // A6 giant-run refinement
 void launch_seg_prep(int coder, const uint32_t *perm_seg, uint64_t len, const void *units,
@@ -79,15 +90,17 @@ constexpr int kGatherStage = 24 * 1024;  // one window of output bytes (dynamic 
 inline uint64_t gather_tiles(uint64_t n) { return (n + kGatherTile - 1) / kGatherTile; }
 // base_ptr (nullable): device pointer to the first output offset of a span
 // re-gather (positions start there); NULL = 0.
-// packed_codes (nullable): perm holds index | min(len,15) << 28; strings of
-// length <= PL are rebuilt from these sorted codes and perm is unpacked in place.
+// packed: perm holds index | min(len,15) << 28; strings of length <= PL are
+// rebuilt from the sorted codes (packed_codes, or DevState::sorted_keys when
+// NULL) and perm is unpacked in place.  st (nullable): violation guard.
 void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, const int64_t *offsets,
                    void *sorted_units, int64_t *sorted_offsets, unsigned long long *lb,
                    uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, const int64_t *base_ptr = nullptr,
-                   const uint64_t *packed_codes = nullptr);
+                   bool packed = false, const uint64_t *packed_codes = nullptr, const DevState *st = nullptr);
 void launch_unpack_perm(uint32_t *perm, uint64_t n, cudaStream_t s);
 void launch_regather_runs(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                           const uint32_t *perm, const void *units, const int64_t *offsets,
-                          void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s);
+                          void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s,
+                          uint32_t first_small = 0, uint32_t first_medium = 0);
 
 }  // namespace husky

@@ -65,15 +65,53 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 constexpr int kExchangeBytes = kRadixTile * (8 + 4) + kRadixWarps * 256 * 4;
 
+// Device-side pass plan: lets the host launch all 8 pass slots without
+// reading the trivial-digit mask back (no host synchronisation).
+__global__ void k_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB) {
+  uint32_t m = st->trivial_mask, np = 0;
+  for (int d = 0; d < 8; ++d)
+    if (!((m >> d) & 1)) st->pass_digit[np++] = d;
+  st->np = np;
+  st->sorted_keys = (unsigned long long)((np & 1) ? keysB : keysA);
+}
+
+// all digits trivial: the permutation is the payload as it stands
+__global__ void k_radix_finalize(const DevState *st, const uint32_t *v_init, uint32_t *v_final, uint64_t n) {
+  if (st->np != 0) return;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    v_final[i] = v_init ? v_init[i] : (uint32_t)i;
+}
+
+// Buffers of a planned pass slot, resolved on device from DevState::np.
+struct SlotPtrs {
+  uint64_t *kA, *kB;
+  const uint32_t *v_init;  // NULL: payload = index (synthesised by slot 0)
+  uint32_t *v_final, *v_tmp;
+};
+
 // One pass over one tile.  LOOKBACK: decoupled look-back on `lb` (onesweep);
 // otherwise the tile's per-digit bases are read from `prefix` ([digit][tile],
-// written by k_rs_scan) and nothing waits on other tiles.
+// written by k_rs_scan) and nothing waits on other tiles.  plan != NULL: this
+// is pass slot `slot` of the device-side plan (buffers, digit resolved here;
+// slots beyond the plan exit at once).
 template <bool SYNTH_VALS, bool LOOKBACK>
 __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     k_onesweep(const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint64_t n, int shift,
                const uint32_t *__restrict__ digit_start, unsigned long long *lb, uint32_t *tile_counter,
-               uint32_t epoch, const uint32_t *__restrict__ prefix, uint32_t num_tiles) {
+               uint32_t epoch, const uint32_t *__restrict__ prefix, uint32_t num_tiles, const DevState *plan,
+               int slot, SlotPtrs sp) {
+  if (plan) {
+    const uint32_t np = plan->np;
+    if ((uint32_t)slot >= np) return;
+    const uint32_t digit = plan->pass_digit[slot];
+    shift = 8 * digit;
+    digit_start = plan->digit_start[digit];
+    keys_in = (slot & 1) ? sp.kB : sp.kA;
+    keys_out = (slot & 1) ? sp.kA : sp.kB;
+    vals_in = slot == 0 ? sp.v_init : (((np - slot) & 1) == 0 ? sp.v_final : sp.v_tmp);
+    vals_out = ((np - 1 - slot) & 1) == 0 ? sp.v_final : sp.v_tmp;
+  }
   extern __shared__ __align__(16) uint8_t smem[];
   // key/value exchange buffer, then per-warp digit counters [warps][256]
   uint64_t *xk = reinterpret_cast<uint64_t *>(smem);
@@ -285,10 +323,10 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
   if (onesweep) {
     if (vals_in == nullptr)
       k_onesweep<true, true><<<g, b, kExchangeBytes, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds,
-                                                          lb, tile_counter, epoch, nullptr, tiles);
+                                                          lb, tile_counter, epoch, nullptr, tiles, nullptr, 0, SlotPtrs{});
     else
       k_onesweep<false, true><<<g, b, kExchangeBytes, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds,
-                                                           lb, tile_counter, epoch, nullptr, tiles);
+                                                           lb, tile_counter, epoch, nullptr, tiles, nullptr, 0, SlotPtrs{});
     return;
   }
   // reduce-then-scan: the look-back buffer (tiles*256 u64) holds counts[256][tiles] u32
@@ -297,10 +335,47 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
   k_rs_scan<<<256, 1024, 0, s>>>(counts, tiles, ds);
   if (vals_in == nullptr)
     k_onesweep<true, false><<<g, b, kExchangeBytes, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                         tile_counter, epoch, counts, tiles);
+                                                         tile_counter, epoch, counts, tiles, nullptr, 0, SlotPtrs{});
   else
     k_onesweep<false, false><<<g, b, kExchangeBytes, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                          tile_counter, epoch, counts, tiles);
+                                                          tile_counter, epoch, counts, tiles, nullptr, 0, SlotPtrs{});
+}
+
+void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, cudaStream_t s) {
+  Scope sc_(ST_HIST_SCAN, s, 0);
+  k_radix_plan<<<1, 1, 0, s>>>(st, keysA, keysB);
+}
+
+// Pass slot `slot` (0..7) of the device-side plan, onesweep variant.  Launched
+// unconditionally; the kernel resolves digit and buffers from DevState.
+void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint32_t *vals_init,
+                          uint32_t *vals_final, uint32_t *vals_tmp, uint64_t n, DevState *st,
+                          unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s) {
+  if (n == 0) return;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_onesweep<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
+    cudaFuncSetAttribute(k_onesweep<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
+    configured = true;
+  }
+  Scope sc_(ST_RADIX, s, n);
+  const uint32_t tiles = (uint32_t)radix_tiles(n);
+  SlotPtrs sp{keysA, keysB, vals_init, vals_final, vals_tmp};
+  if (slot == 0 && vals_init == nullptr)
+    k_onesweep<true, true><<<tiles, kRadixThreads, kExchangeBytes, s>>>(
+        nullptr, nullptr, nullptr, nullptr, n, 0, nullptr, lb, tile_counter, epoch, nullptr, tiles, st, slot, sp);
+  else
+    k_onesweep<false, true><<<tiles, kRadixThreads, kExchangeBytes, s>>>(
+        nullptr, nullptr, nullptr, nullptr, n, 0, nullptr, lb, tile_counter, epoch, nullptr, tiles, st, slot, sp);
+}
+
+void launch_radix_finalize(const DevState *st, const uint32_t *vals_init, uint32_t *vals_final, uint64_t n,
+                           cudaStream_t s) {
+  if (n == 0) return;
+  Scope sc_(ST_RADIX, s, 0);
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 2048) blocks = 2048;
+  k_radix_finalize<<<(unsigned)blocks, 256, 0, s>>>(st, vals_init, vals_final, n);
 }
 
 __global__ void k_iota(uint32_t *perm, uint64_t n) {

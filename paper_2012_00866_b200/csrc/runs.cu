@@ -38,6 +38,8 @@ __global__ void __launch_bounds__(kScanThreads)
   __shared__ uint32_t s_wt[kScanThreads / 32 + 1];
   __shared__ unsigned long long s_excl;
   const uint32_t tid = threadIdx.x;
+  if (st->violations & kOffsetsBad) return;  // invalid input: reported by the caller
+  if (keys == nullptr) keys = reinterpret_cast<const uint64_t *>(st->sorted_keys);  // device-planned radix
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
