@@ -71,7 +71,10 @@ typedef struct {
   uint64_t runs_by_class[4];/* [0] already ordered (check only)  [1] warp-sorted (<=32)
                                [2] CTA-sorted (<=4096)           [3] giant (refined)     */
   uint32_t refine_rounds;   /* giant-run refinement rounds (re-key + segment radix)      */
-  uint32_t radix_passes;    /* non-trivial 8-bit LSD passes executed (0..8)              */
+  uint32_t radix_passes;    /* key-sort partition passes: MSD levels (default key sort) or
+                               non-trivial 8-bit LSD passes (HUSKY_KEYSORT=lsd), 0..8    */
+  uint64_t keys_partitioned;/* keys moved by those passes, summed over passes            */
+  uint64_t keys_local;      /* keys sorted in shared memory by the MSD local sort        */
 } husky_outcome;
 
 /* 1 for ASCII, 2 for UNICODE, 0 for an unknown coder. */

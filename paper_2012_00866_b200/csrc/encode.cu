@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
     __syncthreads();
   }
   uint32_t viol = 0;
+  unsigned long long kor = 0, knand = 0;  // OR and NOT-AND of the codes (MSD level 0)
   const uint32_t lane = lane_id();
   constexpr int W = CoderTraits<CODER>::kUnitBytes;
   // Global word loads (fallback path) are clamped into [lo_word, hi_word], the
@@ -145,6 +146,8 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
       bool valid = threadIdx.x + k * blockDim.x < cnt;
       if (valid) {
         codes[i] = code[k];
+        kor |= code[k];
+        knand |= ~code[k];
         // initial radix payload: index | min(len, 15) << 28 (n <= 2^28 only)
         if (packed) {
           int64_t L = o1[k] - o0[k];
@@ -172,6 +175,22 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
   // reduce violation bits: one atomic per warp that saw any
   viol = __reduce_or_sync(0xFFFFFFFFu, viol);
   if (lane == 0 && viol) atomicOr(&st->violations, viol);
+  {
+    __shared__ unsigned long long s_ao[2][kEncThreads / 32];
+    uint32_t a = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)kor), b = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)(kor >> 32));
+    uint32_t c = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)knand), d = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)(knand >> 32));
+    if (lane == 0) {
+      s_ao[0][threadIdx.x >> 5] = ((unsigned long long)b << 32) | a;
+      s_ao[1][threadIdx.x >> 5] = ((unsigned long long)d << 32) | c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long x = 0, y = 0;
+      for (int w = 0; w < kEncThreads / 32; ++w) { x |= s_ao[0][w]; y |= s_ao[1][w]; }
+      if (x) atomicOr(&st->key_or, x);
+      if (y) atomicOr(&st->key_nand, y);
+    }
+  }
   if (HIST) {
     __syncthreads();
     uint32_t *g = &st->hist[0][0];

@@ -18,6 +18,10 @@ struct Layout {
   uint64_t n = 0, tiles_r = 0, tiles_s = 0, cap_sm = 0, cap_g = 0;
   size_t state = 0, keysA = 0, keysB = 0, vals = 0, vals2 = 0, lb_radix = 0, lb_scan = 0, run_start = 0,
          run_end = 0, dirty = 0, list_sm = 0, list_g = 0, total = 0;
+  uint64_t lb_radix_words = 0;
+  // MSD key sort (msd.cu)
+  size_t keysC = 0, vals3 = 0, segs[2] = {0, 0}, tile_seg[2] = {0, 0}, hist = 0, seg_or = 0, seg_nand = 0,
+         cont = 0, win_lo = 0, win_hi = 0;
 };
 Layout make_layout(uint64_t n);
 
@@ -53,7 +57,7 @@ struct Sorter {
   unsigned long long *lb_scan() const { return at<unsigned long long>(L.lb_scan); }
 
   cudaError_t reset_lookback() {
-    cudaError_t e = cudaMemsetAsync(ws + L.lb_radix, 0, radix_lb_words(L.n) * 8, s);
+    cudaError_t e = cudaMemsetAsync(ws + L.lb_radix, 0, L.lb_radix_words * 8, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(ws + L.lb_scan, 0, L.tiles_s * 8, s);
     return e;
   }

@@ -46,6 +46,13 @@ int device_sm_count() {
   return sms > 0 ? sms : 148;
 }
 
+// Key sort variant: LSD onesweep (default) or HUSKY_KEYSORT=msd, the MSD hybrid
+// of msd.cu (measured slower on every config so far: DESIGN.md section 6.2).
+bool keysort_msd() {
+  const char *v = getenv("HUSKY_KEYSORT");
+  return v && v[0] == 'm';
+}
+
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 Layout make_layout(uint64_t n) {
@@ -66,13 +73,31 @@ Layout make_layout(uint64_t n) {
   L.keysB = take(n * 8);
   L.vals = take(n * 4);
   L.vals2 = take(n * 4);  // packed initial payload (index | len << 28) when n <= 2^28
-  L.lb_radix = take(radix_lb_words(n) * 8);
+  {
+    // the LSD passes and the MSD levels share the look-back words (and their epochs)
+    uint64_t w = radix_lb_words(n), wm = msd_max_tiles(n) * 256 + 2;
+    L.lb_radix_words = w > wm ? w : wm;
+  }
+  L.lb_radix = take(L.lb_radix_words * 8);
   L.lb_scan = take(L.tiles_s * 8);
   L.run_start = take(L.cap_sm * 4);
   L.run_end = take(L.cap_sm * 4);
   L.dirty = take(L.cap_sm);
   L.list_sm = take(L.cap_sm * 8);
   L.list_g = take(L.cap_g * 8);
+  const uint64_t ms = msd_max_segs(n), mt = msd_max_tiles(n), nw = msd_windows(n);
+  L.keysC = take(n * 8);
+  L.vals3 = take(n * 4);
+  for (int i = 0; i < 2; ++i) {
+    L.segs[i] = take(ms * sizeof(MsdSeg));
+    L.tile_seg[i] = take(mt * 4);
+  }
+  L.hist = take(ms * 256 * 4);
+  L.seg_or = take(ms * 8);
+  L.seg_nand = take(ms * 8);
+  L.cont = take(ms * 8 * 4);
+  L.win_lo = take(nw * 4);
+  L.win_hi = take(nw * 4);
   L.total = off;
   return L;
 }
@@ -165,21 +190,49 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // gather rebuilds strings of length <= PL from their code (no random reads)
   const bool packed = n <= kPackMaxN;
   uint32_t *packed_payload = packed ? S.at<uint32_t>(L.vals2) : nullptr;
-  launch_encode(coder, true, d_units, d_offsets, n, S.keysA(), st, S.sms, s, packed_payload);
-  launch_hist_scan(n, st, s);
-
-  // ---- A2 key sort: (code, index) -> sorted codes, perm.  The pass plan (which
-  // digits are not shared by all keys) is made on device, so the host enqueues
-  // all 8 pass slots without waiting; slots beyond the plan exit at once.  Input
-  // violations (bad offsets, ASCII domain) make every later kernel a no-op and
-  // are reported at the single synchronisation below.
   uint64_t *keysA = S.keysA(), *keysB = S.keysB();
   uint32_t *vals_tmp = S.at<uint32_t>(L.vals);
-  launch_radix_plan(st, keysA, keysB, s);
-  for (int slot = 0; slot < 8; ++slot)
-    launch_onesweep_slot(slot, keysA, keysB, packed_payload, d_perm, vals_tmp, n, st, S.lb_radix(),
-                         S.next_counter(), S.next_epoch(), s);
-  launch_radix_finalize(st, packed_payload, d_perm, n, s);
+  const bool use_msd = keysort_msd();
+  if (use_msd) {
+    // ---- A2 key sort, MSD hybrid (msd.cu): codes in keysB -> sorted keys in
+    // keysA (DevState::sorted_keys), payload in d_perm.  One host
+    // synchronisation per partition level after the first.
+    launch_encode(coder, false, d_units, d_offsets, n, keysB, st, S.sms, s, packed_payload);
+    MsdBufs B;
+    B.k[0] = keysB;
+    B.k[1] = S.at<uint64_t>(L.keysC);
+    B.v[0] = vals_tmp;
+    B.v[1] = S.at<uint32_t>(L.vals3);
+    B.kh = keysA;
+    B.vh = d_perm;
+    B.v_init = packed_payload;
+    for (int i = 0; i < 2; ++i) {
+      B.segs[i] = S.at<MsdSeg>(L.segs[i]);
+      B.tile_seg[i] = S.at<uint32_t>(L.tile_seg[i]);
+    }
+    B.hist = S.at<uint32_t>(L.hist);
+    B.seg_or = S.at<unsigned long long>(L.seg_or);
+    B.seg_nand = S.at<unsigned long long>(L.seg_nand);
+    B.cont = S.at<uint32_t>(L.cont);
+    B.win_lo = S.at<uint32_t>(L.win_lo);
+    B.win_hi = S.at<uint32_t>(L.win_hi);
+    B.lb = S.lb_radix();
+    if (husky_status e = msd_key_sort(S, B)) return e;
+  } else {
+    launch_encode(coder, true, d_units, d_offsets, n, S.keysA(), st, S.sms, s, packed_payload);
+    launch_hist_scan(n, st, s);
+
+    // ---- A2 key sort, LSD onesweep: (code, index) -> sorted codes, perm.  The
+    // pass plan (which digits are not shared by all keys) is made on device, so
+    // the host enqueues all 8 pass slots without waiting; slots beyond the plan
+    // exit at once.  Input violations (bad offsets, ASCII domain) make every
+    // later kernel a no-op and are reported at the single synchronisation below.
+    launch_radix_plan(st, keysA, keysB, s);
+    for (int slot = 0; slot < 8; ++slot)
+      launch_onesweep_slot(slot, keysA, keysB, packed_payload, d_perm, vals_tmp, n, st, S.lb_radix(),
+                           S.next_counter(), S.next_epoch(), s);
+    launch_radix_finalize(st, packed_payload, d_perm, n, s);
+  }
   if (packed && !d_sorted_units) launch_unpack_perm(d_perm, n, s);  // the gather unpacks otherwise
 
   // ---- A4 gather in (code, index) order.  Done BEFORE the fix-up: the order
@@ -216,7 +269,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   if (hs.violations & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing");
   if (coder == HUSKY_CODER_ASCII && (hs.violations & kDomainBad))
     return fail(HUSKY_ERR_DOMAIN, "ASCII coder: a unit > 0x7F inside a code prefix (Alg. 4 mask is not monotone there)");
-  S.radix_passes = hs.np;
+  if (!use_msd) S.radix_passes = hs.np;
   debug_check_perm(d_perm, n, "fix-up", s);
 
   // ---- A6 giant-run refinement (rare: runs > 4096 strings with an inversion)
@@ -233,6 +286,8 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
     h_out->n_runs = hs.runs_total;
     h_out->refine_rounds = S.refine_rounds;
     h_out->radix_passes = S.radix_passes;
+    h_out->keys_partitioned = use_msd ? hs.msd_keys_part : (uint64_t)hs.np * n;
+    h_out->keys_local = hs.msd_keys_local;
   }
   return HUSKY_OK;
 }
@@ -355,7 +410,8 @@ __device__ DevState g_encode_state;
 extern "C" {
 
 static const char *kStageNames[ST_COUNT] = {"encode", "hist_scan", "radix_pass", "runs_scan", "runs_classify",
-                                            "fix_small", "fix_medium", "refine", "gather", "multi"};
+                                            "fix_small", "fix_medium", "refine", "gather", "multi",
+                                            "msd_hist", "local_sort"};
 
 void husky_profile_enable(int on) {
   Profiler &P = profiler();

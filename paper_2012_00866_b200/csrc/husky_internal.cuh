@@ -57,6 +57,13 @@ struct DevState {
   uint32_t np;
   uint32_t pass_digit[8];
   unsigned long long sorted_keys;  // uint64_t* of the sorted keys
+  // MSD key sort (msd.cu): OR and NOT-AND of all codes (fused into A1; zero-
+  // initialised), segment-list fill counts and tile counts of the two level
+  // lists, keys moved by partition passes / sorted by the local sort
+  unsigned long long key_or, key_nand;
+  uint32_t msd_count[2], msd_tiles[2];
+  uint32_t msd_all_equal, msd_pad;
+  unsigned long long msd_keys_part, msd_keys_local;
   uint32_t pad[16];
 };
 

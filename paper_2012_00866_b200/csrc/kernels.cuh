@@ -50,6 +50,41 @@ void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint
 void launch_radix_finalize(const DevState *st, const uint32_t *vals_init, uint32_t *vals_final, uint64_t n,
                            cudaStream_t s);
 
+// A2 key sort, MSD variant (msd.cu; the default).  Levels of segmented
+// partition passes on the top varying byte of each segment (onesweep tiles with
+// per-segment look-back), until every bucket has <= kMsdSmall keys; buckets are
+// then sorted in shared memory, several per CTA, by windows of kMsdWin positions.
+constexpr uint32_t kMsdSmall = 2048, kMsdWin = 2048, kMsdLocalCap = kMsdSmall + kMsdWin;
+constexpr uint32_t kSegPart = 1u;  // MsdSeg::flags: partitioned at this level
+struct MsdSeg {
+  uint32_t start, len;  // positions [start, start + len)
+  uint32_t digit;       // byte the segment is partitioned on (its top varying byte)
+  uint32_t tile0;       // first tile of the segment in the level's launch
+  uint32_t buf;         // scratch buffer (0/1) holding the segment's keys and payload
+  uint32_t flags;
+};
+inline uint64_t msd_max_segs(uint64_t n) { return n / (kMsdSmall + 1) + 2; }
+inline uint64_t msd_max_tiles(uint64_t n) { return radix_tiles(n) + msd_max_segs(n) + 1; }
+inline uint64_t msd_windows(uint64_t n) { return (n + kMsdWin - 1) / kMsdWin; }
+struct MsdBufs {
+  uint64_t *k[2];            // scratch keys (k[0] holds the codes written by A1)
+  uint32_t *v[2];            // scratch payload
+  uint64_t *kh;              // home: final sorted keys
+  uint32_t *vh;              // home: final payload (the caller's perm)
+  const uint32_t *v_init;    // level-0 payload (NULL: the index)
+  MsdSeg *segs[2];           // segment lists of alternate levels
+  uint32_t *tile_seg[2];     // tile -> segment of each list
+  uint32_t *hist;            // [max_segs][256]: counts, then absolute bucket starts
+  unsigned long long *seg_or, *seg_nand;  // [max_segs]
+  uint32_t *cont;            // [max_segs][8]: bucket continues to the next level
+  uint32_t *win_lo, *win_hi; // [windows]: span of the local-sort buckets starting in a window
+  unsigned long long *lb;    // look-back words [msd_max_tiles][256]
+};
+struct Sorter;
+// Runs the whole MSD key sort: codes in B.k[0] -> sorted keys (DevState::sorted_keys)
+// + payload in B.vh.  One host synchronisation per level after the first.
+husky_status msd_key_sort(Sorter &S, const MsdBufs &B);
+
 // A3 run detection (single-pass scan with decoupled look-back)
 constexpr int kScanThreads = 512, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
 // padded smem staging sizes of k_runs_scan (one pad u64 every 8, one pad u32 every 32)

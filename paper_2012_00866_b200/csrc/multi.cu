@@ -177,7 +177,8 @@ static MultiLayout make_multi_layout(int coder, uint64_t n, uint64_t units, int 
   L.keysA = take(n * 8 + 8);
   L.keysB = take(n * 8 + 8);
   L.vals = take(n * 4 + 4);
-  L.lb_radix = take(radix_lb_words(n) * 8);
+  L.lb_radix_words = radix_lb_words(n);
+  L.lb_radix = take(L.lb_radix_words * 8);
   L.lb_scan = take(L.tiles_s * 8 + 8);
   M.send_perm = take(n * 4 + 4);
   M.samples = take((size_t)world * kSampleStride * 8);
@@ -696,6 +697,7 @@ husky_status husky_sort_multi_loopback(int coder, int world, const void *d_units
     agg.max_run = std::max(agg.max_run, o.max_run);
     for (int c = 0; c < 4; ++c) agg.runs_by_class[c] += o.runs_by_class[c];
     agg.refine_rounds += o.refine_rounds; agg.radix_passes += o.radix_passes;
+    agg.keys_partitioned += o.keys_partitioned; agg.keys_local += o.keys_local;
     out_n += dst.n_out; out_u += dst.units_out;
   }
   if (n == 0 && d_sorted_offsets) HCHECK(cudaMemsetAsync(d_sorted_offsets, 0, 8, s));

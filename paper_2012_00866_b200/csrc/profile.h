@@ -18,7 +18,7 @@ namespace husky {
 
 enum Stage : int {
   ST_ENCODE = 0, ST_HIST_SCAN, ST_RADIX, ST_RUNS_SCAN, ST_CLASSIFY, ST_FIX_SMALL, ST_FIX_MEDIUM,
-  ST_REFINE, ST_GATHER, ST_MULTI, ST_COUNT
+  ST_REFINE, ST_GATHER, ST_MULTI, ST_MSD_HIST, ST_LOCAL_SORT, ST_COUNT
 };
 
 struct Profiler {
