@@ -9,9 +9,8 @@ namespace husky {
 int device_sm_count();  // husky.cu
 
 // A1 encode
-// tile of 1024 strings per CTA iteration; its unit span (<= 16 KB) is staged in smem
-constexpr int kEncThreads = 256, kEncItems = 4, kEncTile = kEncThreads * kEncItems, kEncBlocksPerSM = 4;
-constexpr int kEncStageWords = 2048;
+// 256 threads x 4 strings in flight per CTA iteration, persistent grid
+constexpr int kEncThreads = 256, kEncBlocksPerSM = 8;
 // packed (nullable, n <= 2^28): also writes the initial radix payload
 // index | min(len, 15) << 28, so the gather knows short strings' lengths
 // without a random offsets read.
@@ -50,7 +49,7 @@ void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint
 void launch_radix_finalize(const DevState *st, const uint32_t *vals_init, uint32_t *vals_final, uint64_t n,
                            cudaStream_t s);
 
-// A2 key sort, MSD variant (msd.cu; the default).  Levels of segmented
+// A2 key sort, MSD variant (msd.cu; opt-in, HUSKY_KEYSORT=msd).  Levels of segmented
 // partition passes on the top varying byte of each segment (onesweep tiles with
 // per-segment look-back), until every bucket has <= kMsdSmall keys; buckets are
 // then sorted in shared memory, several per CTA, by windows of kMsdWin positions.
