@@ -95,8 +95,11 @@ _sig("husky_profile_stage_name", ctypes.c_char_p, _I)
 _sig("husky_launch_count", _U64)
 
 
-def husky_profile_enable(on: bool = True):
-    _lib.husky_profile_enable(1 if on else 0)
+def husky_profile_enable(on=True):
+    """on: False/0 off; True/1 an event pair per kernel launch; 2 event pairs only
+    around launch groups (the radix passes, the encoder) -- cheap enough for a
+    timed region."""
+    _lib.husky_profile_enable(int(on))
 
 
 def husky_profile_reset():

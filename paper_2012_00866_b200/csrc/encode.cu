@@ -192,11 +192,14 @@ void launch_encode(int coder, bool hist, const void *units, const int64_t *offse
     else
       k_encode<HUSKY_CODER_UNICODE><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, st, packed);
   }
-  if (hist) {
-    Scope sc_(ST_HIST_SCAN, s, n);
-    const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * 2);
-    k_hist8<<<(unsigned)blocks, 512, 0, s>>>(codes, n, st);
-  }
+  if (hist) launch_hist8(codes, n, st, num_sms, s);
+}
+
+void launch_hist8(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s) {
+  if (n == 0) return;
+  Scope sc_(ST_HIST_SCAN, s, n);
+  const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * 2);
+  k_hist8<<<(unsigned)blocks, 512, 0, s>>>(keys, n, st);
 }
 
 }  // namespace husky

@@ -219,7 +219,11 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
     B.lb = S.lb_radix();
     if (husky_status e = msd_key_sort(S, B)) return e;
   } else {
-    launch_encode(coder, true, d_units, d_offsets, n, S.keysA(), st, S.sms, s, packed_payload);
+    {
+      GroupScope grp(ST_ENCODE, s);
+      launch_encode(coder, false, d_units, d_offsets, n, S.keysA(), st, S.sms, s, packed_payload);
+    }
+    launch_hist8(S.keysA(), n, st, S.sms, s);
     launch_hist_scan(n, st, s);
 
     // ---- A2 key sort, LSD onesweep: (code, index) -> sorted codes, perm.  The
@@ -228,9 +232,12 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
     // exit at once.  Input violations (bad offsets, ASCII domain) make every
     // later kernel a no-op and are reported at the single synchronisation below.
     launch_radix_plan(st, keysA, keysB, s);
-    for (int slot = 0; slot < 8; ++slot)
-      launch_onesweep_slot(slot, keysA, keysB, packed_payload, d_perm, vals_tmp, n, st, S.lb_radix(),
-                           S.next_counter(), S.next_epoch(), s);
+    {
+      GroupScope grp(ST_RADIX, s);  // profiler mode 2: the 8 pass slots as one timed group
+      for (int slot = 0; slot < 8; ++slot)
+        launch_onesweep_slot(slot, keysA, keysB, packed_payload, d_perm, vals_tmp, n, st, S.lb_radix(),
+                             S.next_counter(), S.next_epoch(), s);
+    }
     launch_radix_finalize(st, packed_payload, d_perm, n, s);
   }
   if (packed && !d_sorted_units) launch_unpack_perm(d_perm, n, s);  // the gather unpacks otherwise
@@ -417,7 +424,7 @@ void husky_profile_enable(int on) {
   Profiler &P = profiler();
   P.flush();
   std::lock_guard<std::mutex> g(P.mu);
-  P.on = on != 0;
+  P.on = on == 2 ? 2 : (on != 0 ? 1 : 0);
 }
 
 void husky_profile_reset(void) {

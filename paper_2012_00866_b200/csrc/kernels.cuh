@@ -17,6 +17,8 @@ constexpr int kEncThreads = 256, kEncBlocksPerSM = 8;
 constexpr uint64_t kPackMaxN = 1ull << 28;
 void launch_encode(int coder, bool hist, const void *units, const int64_t *offsets, uint64_t n,
                    uint64_t *codes, DevState *st, int num_sms, cudaStream_t s, uint32_t *packed = nullptr);
+// 8 x 256 digit histograms of n keys into DevState::hist (accumulates)
+void launch_hist8(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s);
 
 // A2 onesweep radix
 // 512 threads x 8 keys = 4096-key tiles, 64 KB smem, <= 64 registers -> 2 CTAs

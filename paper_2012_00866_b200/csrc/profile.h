@@ -23,7 +23,7 @@ enum Stage : int {
 
 struct Profiler {
   std::mutex mu;
-  bool on = false;
+  int on = 0;  // 0 off, 1 an event pair per launch, 2 event pairs per GroupScope only
   struct Pending { int stage; cudaEvent_t a, b; uint64_t elems; };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> pool;
@@ -74,7 +74,7 @@ struct Scope {
     P.total_launches++;
     P.launches[stage]++;
     P.elems[stage] += m;
-    if (P.on) {
+    if (P.on == 1) {
       a = P.get();
       cudaEventRecord(a, s);
     }
@@ -93,6 +93,31 @@ struct Scope {
     cudaEvent_t b = P.get();
     cudaEventRecord(b, s);
     P.pending.push_back({stage, a, b, elems});
+  }
+};
+
+// Profiler mode 2: one event pair around a group of launches of one stage (e.g.
+// all radix passes of a sort), so the timed region carries two event records
+// per group instead of two per launch.  Adds the group's time to the stage.
+struct GroupScope {
+  int stage;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  GroupScope(int st, cudaStream_t str) : stage(st), s(str) {
+    Profiler &P = profiler();
+    std::lock_guard<std::mutex> g(P.mu);
+    if (P.on == 2) {
+      a = P.get();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~GroupScope() {
+    if (!a) return;
+    Profiler &P = profiler();
+    std::lock_guard<std::mutex> g(P.mu);
+    cudaEvent_t b = P.get();
+    cudaEventRecord(b, s);
+    P.pending.push_back({stage, a, b, 0});
   }
 };
 
