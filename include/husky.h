@@ -14,9 +14,9 @@
  *     (NULL = legacy default stream).  No torch types cross this boundary.
  *   - Strings are given as a unit buffer plus int64 offsets[n+1] (non-decreasing);
  *     string i is units[offsets[i] .. offsets[i+1]).  offsets[0] need not be 0.
- *     Units are uint8 for HUSKY_CODER_ASCII and native little-endian uint16
- *     (UTF-16 code units, Java String semantics, reading R8) for
- *     HUSKY_CODER_UNICODE.
+ *     Units are uint8 for HUSKY_CODER_ASCII / ENGLISH5 / ENGLISH6 and native
+ *     little-endian uint16 (UTF-16 code units, Java String semantics, DESIGN.md
+ *     reading R8) for HUSKY_CODER_UNICODE.
  *   - The caller owns every buffer.  Inputs are never written.  The library
  *     never allocates or frees caller memory; scratch memory comes only from
  *     the caller's workspace (size from the *_workspace query).  Plans and
@@ -44,9 +44,10 @@ typedef enum {
   HUSKY_OK = 0,
   HUSKY_ERR_INVALID_ARG = 1, /* null required pointer, unknown coder, n >= 2^32,
                                 non-monotone offsets, workspace misaligned      */
-  HUSKY_ERR_DOMAIN = 2,      /* husky_sort with ASCII coder saw a unit > 0x7F in a
-                                code prefix: Alg. 4's mask breaks
-                                monotonicity there (reading R5)       */
+  HUSKY_ERR_DOMAIN = 2,      /* husky_sort saw a unit outside the coder's domain in
+                                a code prefix (ASCII: > 0x7F; ENGLISH5/6: see the
+                                coder): Alg. 4's mask breaks
+                                monotonicity there (readings R5, R15) */
   HUSKY_ERR_CUDA = 3,        /* a CUDA runtime call failed                       */
   HUSKY_ERR_NCCL = 4,        /* an NCCL call failed (multi-GPU only)             */
   HUSKY_ERR_WORKSPACE = 5,   /* workspace smaller than the query returned        */
@@ -54,37 +55,49 @@ typedef enum {
 } husky_status;
 
 typedef enum {
-  HUSKY_CODER_ASCII = 0,  /* asciiToLong: stringToLong(s, 9, 7, 0x7F) */
-  HUSKY_CODER_UNICODE = 1 /* unicodeToLong: stringToLong(s, 4, 16, 0xFFFF)>>>1 PAPER.md:463-465, 487-490 */
+  HUSKY_CODER_ASCII = 0,   /* asciiToLong: stringToLong(s, 9, 7, 0x7F) */
+  HUSKY_CODER_UNICODE = 1, /* unicodeToLong: stringToLong(s, 4, 16, 0xFFFF)>>>1 PAPER.md:463-465, 487-490 */
+  HUSKY_CODER_ENGLISH5 = 2,/* "5-bit ASCII ... 12 (or fewer) characters":
+                              stringToLong(s, 12, 5, 0x1F), uint8 units (reading R15).
+                              husky_sort domain: every unit inside the 12-unit code
+                              window is a lowercase letter, or every one is an
+                              uppercase letter (case folding is monotone only then) */
+  HUSKY_CODER_ENGLISH6 = 3 /* "case-dependent strings (6-bit ASCII) ... 10 characters"
+                              (PAPER.md:219): stringToLong(s, 10, 6, 0x3F), uint8 units.
+                              husky_sort domain: units inside the 10-unit window are
+                              letters A-Z / a-z (reading R15)                        */
 } husky_coder;
 
 /* Mirrors SortOutcome (a reading of Alg. 1's `coding.perfect`, plus
  * run statistics of the step-3 fix-up). */
 typedef struct {
   int32_t perfect;          /* Alg. 3 AND_i perfectForLength(len_i);
-                               ASCII len<=9, UNICODE len<=3 (reading R4).  Reported only:
+                               ASCII len<=9, UNICODE len<=3 (reading R4), ENGLISH5 12,
+                               ENGLISH6 10 (R15).  Reported only:
                                the fix-up never relies on it.                           */
-  int32_t domain_ok;        /* all code-prefix units <= mask (always 1 for UNICODE)      */
+  int32_t domain_ok;        /* all code-window units in the coder's domain (UNICODE: 1)  */
   uint64_t n_runs;          /* runs of >= 2 equal codes after the key sort               */
   uint64_t n_in_runs;       /* strings inside those runs                                 */
   uint64_t max_run;         /* longest run                                               */
   uint64_t runs_by_class[4];/* [0] already ordered (check only)  [1] warp-sorted (<=32)
                                [2] CTA-sorted (<=4096)           [3] giant (refined)     */
   uint32_t refine_rounds;   /* giant-run refinement rounds (re-key + segment radix)      */
-  uint32_t radix_passes;    /* key-sort partition passes: MSD levels (default key sort) or
-                               non-trivial 8-bit LSD passes (HUSKY_KEYSORT=lsd), 0..8    */
-  uint64_t keys_partitioned;/* keys moved by those passes, summed over passes            */
+  uint32_t radix_passes;    /* key-sort partition passes: non-trivial 8-bit LSD passes
+                               (default), or MSD levels (HUSKY_KEYSORT=msd); refinement
+                               (A6) passes are added                                     */
+  uint64_t keys_partitioned;/* keys moved by the main key sort's passes, summed          */
   uint64_t keys_local;      /* keys sorted in shared memory by the MSD local sort        */
 } husky_outcome;
 
-/* 1 for ASCII, 2 for UNICODE, 0 for an unknown coder. */
+/* 1 for ASCII / ENGLISH5 / ENGLISH6 (uint8 units), 2 for UNICODE, 0 for an unknown coder. */
 size_t husky_unit_bytes(int coder);
 
 /* A1 -- Alg. 2/3/4 over an array.
  * d_codes[i] = stringToLong(string i) exactly as Alg. 4 computes it, including
- * the per-unit mask (off-domain ASCII units are masked, never rejected:
- * SPEC.md:198, reading R5).  If h_perfect is non-NULL the call synchronizes
- * `stream` and stores Alg. 3's perfect flag there.
+ * the per-unit mask (off-domain units are masked, never rejected: SPEC.md:198,
+ * reading R5).  If h_perfect is non-NULL the call synchronizes `stream` and
+ * stores Alg. 3's perfect flag there: every length <= 9 (ASCII), 3 (UNICODE),
+ * 12 (ENGLISH5), 10 (ENGLISH6) (readings R4, R15).
  * Errors: INVALID_ARG (null pointer with n > 0, unknown coder, offsets not
  * non-decreasing -- detected on device, reported only when h_perfect != NULL),
  * CUDA.  n == 0 is a no-op. */
@@ -108,11 +121,32 @@ husky_status husky_sort_workspace(int coder, uint64_t n, uint64_t total_units, s
  *   h_out              (nullable) outcome statistics
  * Synchronizes `stream` before returning.  n in {0, 1} returns HUSKY_OK at once
  * (d_perm = {0} for n = 1; sorted outputs copied).
- * Errors: INVALID_ARG, DOMAIN (ASCII unit > 0x7F inside the first 9 units of a
- * string; outputs are then unspecified), WORKSPACE, CUDA. */
+ * Errors: INVALID_ARG, DOMAIN (a unit outside the coder's domain inside the
+ * code window of a string -- ASCII: > 0x7F in the first 9 units; ENGLISH5/6:
+ * see husky_coder; outputs are then unspecified), WORKSPACE, CUDA. */
 husky_status husky_sort(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
                         uint32_t *d_perm, void *d_sorted_units, int64_t *d_sorted_offsets,
                         void *d_ws, size_t ws_bytes, husky_outcome *h_out, void *stream);
+
+/* ------------------------------------------------------------ numeric keys
+ * The hot path for objects whose husky code is a PERFECT encoding (PAPER.md:
+ * 213-217: "p = 0 ... we can skip step 3"): the code is an order-preserving
+ * bijection of the key (SPEC.md:264-275 identity coder; reading R16), so
+ * Alg. 1 reduces to encode -> sort (code, index) with no cleanup.
+ *   key_type  HUSKY_KEY_U64: uint64 (unsigned order)
+ *             HUSKY_KEY_I64: int64 (Java Long.compare order)
+ *             HUSKY_KEY_F64: IEEE double in Java Double.compare order: -0.0 <
+ *                            +0.0, every NaN equal and above +inf
+ *   d_keys         n keys (8 bytes each, read only)
+ *   d_perm         (required) stable argsort: original index of the r-th key
+ *                  (equal keys by original index)
+ *   d_sorted_keys  (nullable) d_keys[d_perm[r]], bit-exact
+ * Synchronizes `stream`.  Errors: INVALID_ARG (unknown key_type, null pointer,
+ * n >= 2^32 - 1), WORKSPACE, CUDA. */
+typedef enum { HUSKY_KEY_U64 = 0, HUSKY_KEY_I64 = 1, HUSKY_KEY_F64 = 2 } husky_key_type;
+husky_status husky_sort_keys_workspace(int key_type, uint64_t n, size_t *bytes);
+husky_status husky_sort_keys(int key_type, const void *d_keys, uint64_t n, uint32_t *d_perm,
+                             void *d_sorted_keys, void *d_ws, size_t ws_bytes, void *stream);
 
 /* husky_sort on HOST buffers: copies units/offsets host->device, sorts, and
  * copies perm (and, if h_sorted_units != NULL, the sorted units and offsets)

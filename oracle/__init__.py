@@ -17,6 +17,9 @@ import numpy as np
 
 ASCII = 0
 UNICODE = 1
+ENGLISH5 = 2
+ENGLISH6 = 3
+KEY_U64, KEY_I64, KEY_F64 = 0, 1, 2
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "husky_oracle.c")
@@ -49,12 +52,14 @@ def _load():
         lib.oracle_verify.restype = ctypes.c_int64
         lib.oracle_huskysort_alg1.argtypes = [ctypes.c_int, P, P, U64, P, P, P]
         lib.oracle_huskysort_alg1.restype = ctypes.c_int
+        lib.oracle_sort_keys.argtypes = [ctypes.c_int, P, U64, P]
+        lib.oracle_sort_keys.restype = ctypes.c_int
         _lib = lib
     return _lib
 
 
 def _prep(coder, units, offsets):
-    dt = np.uint8 if coder == ASCII else np.uint16
+    dt = np.uint16 if coder == UNICODE else np.uint8
     units = np.ascontiguousarray(units, dtype=dt)
     if units.size == 0:
         units = np.zeros(1, dtype=dt)  # valid pointer for empty inputs
@@ -122,3 +127,15 @@ def huskysort_alg1(coder, units, offsets):
     if rc:
         raise ValueError(f"oracle_huskysort_alg1 rc={rc}")
     return perm[:n], bool(perfect.value), int(resid.value)
+
+
+def sort_keys(key_type, keys):
+    """-> perm uint32[n]: stable merge sort of 8-byte keys (u64 / i64 / f64 in
+    Java compareTo order), equal keys by index."""
+    k = np.ascontiguousarray(keys).view(np.uint64)
+    n = k.size
+    perm = np.zeros(max(n, 1), dtype=np.uint32)
+    rc = _load().oracle_sort_keys(key_type, _p(k if n else np.zeros(1, np.uint64)), n, _p(perm))
+    if rc:
+        raise ValueError(f"oracle_sort_keys rc={rc}")
+    return perm[:n]

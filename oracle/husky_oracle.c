@@ -40,6 +40,8 @@
 
 #define ORACLE_CODER_ASCII 0
 #define ORACLE_CODER_UNICODE 1
+#define ORACLE_CODER_ENGLISH5 2
+#define ORACLE_CODER_ENGLISH6 3
 
 /* PAPER.md:486-494 (section 4.3, "Constants") */
 #define BITS_LONG 64
@@ -50,11 +52,25 @@
 #define BIT_WIDTH_ASCII 7
 #define MAX_LENGTH_ASCII (BITS_LONG / BIT_WIDTH_ASCII) /* 9 */
 #define MASK_ASCII 0x7F
+/* PAPER.md:218-219 (section 3.2): "5-bit ASCII, words of 12 (or fewer)
+ * characters" and "case-dependent strings (6-bit ASCII) ... 10 characters or
+ * less".  The paper prints only these capacities; width/length/mask follow the
+ * section-4.3 pattern (MAX_LENGTH = 64 / BIT_WIDTH, mask = 2^BIT_WIDTH - 1),
+ * as SPEC.md:224-240 concretises them (reading R15). */
+#define BIT_WIDTH_ENGLISH5 5
+#define MAX_LENGTH_ENGLISH5 (BITS_LONG / BIT_WIDTH_ENGLISH5) /* 12 */
+#define MASK_ENGLISH5 0x1F
+#define BIT_WIDTH_ENGLISH6 6
+#define MAX_LENGTH_ENGLISH6 (BITS_LONG / BIT_WIDTH_ENGLISH6) /* 10 */
+#define MASK_ENGLISH6 0x3F
 
-/* unit i of string s for either coder: u8 for ASCII, u16 for UNICODE
- * (reading R8: Java Strings are UTF-16 code units). */
+static int byte_coder(int coder) { return coder != ORACLE_CODER_UNICODE; }
+static int known_coder(int coder) { return coder >= ORACLE_CODER_ASCII && coder <= ORACLE_CODER_ENGLISH6; }
+
+/* unit i of string s: u8 for the byte coders (ASCII, ENGLISH5/6), u16 for
+ * UNICODE (reading R8: Java Strings are UTF-16 code units). */
 static uint32_t unit_at(int coder, const void *units, int64_t pos) {
-  if (coder == ORACLE_CODER_ASCII) return ((const uint8_t *)units)[pos];
+  if (byte_coder(coder)) return ((const uint8_t *)units)[pos];
   return ((const uint16_t *)units)[pos];
 }
 
@@ -90,11 +106,25 @@ static uint64_t unicode_to_long(const void *units, int64_t start, int64_t len) {
                         BIT_WIDTH_UNICODE, MASK_UNICODE) >> 1;
 }
 
+/* englishToLong: 5-bit letters, case folded by the mask */
+static uint64_t english5_to_long(const void *units, int64_t start, int64_t len) {
+  return string_to_long(ORACLE_CODER_ENGLISH5, units, start, len, MAX_LENGTH_ENGLISH5,
+                        BIT_WIDTH_ENGLISH5, MASK_ENGLISH5);
+}
+
+/* case-dependent 6-bit letters */
+static uint64_t english6_to_long(const void *units, int64_t start, int64_t len) {
+  return string_to_long(ORACLE_CODER_ENGLISH6, units, start, len, MAX_LENGTH_ENGLISH6,
+                        BIT_WIDTH_ENGLISH6, MASK_ENGLISH6);
+}
+
 /* perfectForLength: ASCII is exact up to MAX_LENGTH_ASCII = 9 chars;
  * UNICODE keeps only "the first 3 15/16ths characters" => 3
- * (reading R4). */
+ * (reading R4); ENGLISH5 12 and ENGLISH6 10 characters. */
 static int perfect_for_length(int coder, int64_t len) {
   if (coder == ORACLE_CODER_ASCII) return len <= MAX_LENGTH_ASCII;
+  if (coder == ORACLE_CODER_ENGLISH5) return len <= MAX_LENGTH_ENGLISH5;
+  if (coder == ORACLE_CODER_ENGLISH6) return len <= MAX_LENGTH_ENGLISH6;
   return len <= MAX_LENGTH_UNICODE - 1;
 }
 
@@ -102,14 +132,18 @@ static int perfect_for_length(int coder, int64_t len) {
  * Returns 0 on success, 1 on a bad argument. */
 int oracle_encode(int coder, const void *units, const int64_t *offsets, uint64_t n,
                   uint64_t *codes, int32_t *perfect) {
-  if (coder != ORACLE_CODER_ASCII && coder != ORACLE_CODER_UNICODE) return 1;
+  if (!known_coder(coder)) return 1;
   int isPerfect = 1; /* isPerfect = true */
   for (uint64_t i = 0; i < n; i++) {
     int64_t start = offsets[i], len = offsets[i + 1] - offsets[i];
     if (len < 0) return 1;
     if (isPerfect) isPerfect = perfect_for_length(coder, len);
-    codes[i] = coder == ORACLE_CODER_ASCII ? ascii_to_long(units, start, len)
-                                           : unicode_to_long(units, start, len);
+    switch (coder) {
+      case ORACLE_CODER_ASCII: codes[i] = ascii_to_long(units, start, len); break;
+      case ORACLE_CODER_UNICODE: codes[i] = unicode_to_long(units, start, len); break;
+      case ORACLE_CODER_ENGLISH5: codes[i] = english5_to_long(units, start, len); break;
+      default: codes[i] = english6_to_long(units, start, len); break;
+    }
   }
   if (perfect) *perfect = isPerfect;
   return 0;
@@ -156,7 +190,7 @@ static void merge_sort(const ctx_t *c, uint32_t *a, uint32_t *tmp, uint64_t lo, 
 
 /* perm[r] = original index of the r-th string in sorted order.  0 ok, 1 bad arg, 2 OOM. */
 int oracle_sort(int coder, const void *units, const int64_t *offsets, uint64_t n, uint32_t *perm) {
-  if (coder != ORACLE_CODER_ASCII && coder != ORACLE_CODER_UNICODE) return 1;
+  if (!known_coder(coder)) return 1;
   if (n > 0xFFFFFFFFull) return 1;
   ctx_t c = {coder, units, offsets};
   for (uint64_t i = 0; i < n; i++) perm[i] = (uint32_t)i;
@@ -171,7 +205,7 @@ int oracle_sort(int coder, const void *units, const int64_t *offsets, uint64_t n
 /* sorted_units = concatenation of strings in perm order; sorted_offsets[0] = 0. */
 int oracle_gather(int coder, const void *units, const int64_t *offsets, uint64_t n,
                   const uint32_t *perm, void *sorted_units, int64_t *sorted_offsets) {
-  size_t w = coder == ORACLE_CODER_ASCII ? 1 : 2;
+  size_t w = byte_coder(coder) ? 1 : 2;
   int64_t pos = 0;
   sorted_offsets[0] = 0;
   for (uint64_t r = 0; r < n; r++) {
@@ -280,5 +314,69 @@ int oracle_huskysort_alg1(int coder, const void *units, const int64_t *offsets, 
   free(codes);
   if (perfect) *perfect = isPerfect;
   if (residual) *residual = moves;
+  return 0;
+}
+
+/* ------------------------------------------------- numeric keys (perfect coding)
+ * for a perfect encoding (p = 0) step 3 is skipped, so
+ * Huskysort's result is the plain sort of the keys.  The plain definition is a
+ * stable sort of indices under the key type's natural order (Java compareTo;
+ * SPEC.md:264-275, reading R16), equal keys by original index:
+ *   0 uint64 (unsigned), 1 int64 (Long.compare), 2 double (Double.compare:
+ *   numeric order; -0.0 < +0.0; every NaN equal to every NaN and above +inf). */
+typedef struct {
+  int type;
+  const uint64_t *keys;
+} kctx_t;
+
+static int cmp_double_java(uint64_t a, uint64_t b) {
+  double x, y;
+  memcpy(&x, &a, 8);
+  memcpy(&y, &b, 8);
+  if (x < y) return -1;
+  if (x > y) return 1;
+  /* equal or unordered: Double.compare falls back to doubleToLongBits, which
+   * maps every NaN to one canonical NaN */
+  int xn = x != x, yn = y != y;
+  if (xn || yn) return xn == yn ? 0 : (xn ? 1 : -1);
+  int64_t sa = (int64_t)a, sb = (int64_t)b; /* +-0.0: signed bit patterns */
+  return sa < sb ? -1 : (sa > sb ? 1 : 0);
+}
+
+static int cmp_key(const kctx_t *c, uint32_t i, uint32_t j) {
+  uint64_t a = c->keys[i], b = c->keys[j];
+  int r;
+  if (c->type == 0) r = a < b ? -1 : (a > b ? 1 : 0);
+  else if (c->type == 1) r = (int64_t)a < (int64_t)b ? -1 : ((int64_t)a > (int64_t)b ? 1 : 0);
+  else r = cmp_double_java(a, b);
+  if (r) return r;
+  return i < j ? -1 : (i > j ? 1 : 0);
+}
+
+static void merge_sort_keys(const kctx_t *c, uint32_t *a, uint32_t *tmp, uint64_t lo, uint64_t hi) {
+  if (hi - lo < 2) return;
+  uint64_t mid = lo + (hi - lo) / 2;
+  merge_sort_keys(c, a, tmp, lo, mid);
+  merge_sort_keys(c, a, tmp, mid, hi);
+  uint64_t i = lo, j = mid, k = lo;
+  while (i < mid && j < hi) {
+    if (cmp_key(c, a[j], a[i]) < 0) tmp[k++] = a[j++];
+    else tmp[k++] = a[i++];
+  }
+  while (i < mid) tmp[k++] = a[i++];
+  while (j < hi) tmp[k++] = a[j++];
+  memcpy(a + lo, tmp + lo, (hi - lo) * sizeof(uint32_t));
+}
+
+/* perm[r] = original index of the r-th key.  0 ok, 1 bad arg, 2 OOM. */
+int oracle_sort_keys(int type, const uint64_t *keys, uint64_t n, uint32_t *perm) {
+  if (type < 0 || type > 2 || n > 0xFFFFFFFFull) return 1;
+  kctx_t c = {type, keys};
+  for (uint64_t i = 0; i < n; i++) perm[i] = (uint32_t)i;
+  if (n < 2) return 0;
+  uint32_t *tmp = (uint32_t *)malloc(n * sizeof(uint32_t));
+  if (!tmp) return 2;
+  merge_sort_keys(&c, perm, tmp, 0, n);
+  free(tmp);
   return 0;
 }

@@ -41,12 +41,12 @@ def test_worked_values_golden(oracle_mod):
         if not line.strip() or line.startswith("#"):
             continue
         coder_s, units_s, expect_s, cite = [x.strip() for x in line.split("|")]
-        coder = ASCII if coder_s == "ascii" else UNICODE
+        coder = {"ascii": ASCII, "unicode": UNICODE, "english5": 2, "english6": 3}[coder_s]
         units = [int(x, 16) for x in units_s.split(",")] if units_s else []
         codes, _ = _codes(oracle_mod, [units], coder)
         assert codes[0] == int(expect_s), cite
         n += 1
-    assert n == 4
+    assert n == 8
 
 
 def closed_form_ascii(s):

@@ -21,6 +21,8 @@ import numpy as np
 MASTER_SEED = 20120866
 ASCII = 0
 UNICODE = 1
+ENGLISH5 = 2
+ENGLISH6 = 3
 
 ALNUM = np.frombuffer(b"0123456789ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz", dtype=np.uint8)
 LOWER = np.frombuffer(b"abcdefghijklmnopqrstuvwxyz", dtype=np.uint8)
@@ -62,11 +64,11 @@ def _offsets(lens: np.ndarray) -> np.ndarray:
 
 def from_strings(strings, coder: int = ASCII, name: str = "custom") -> Workload:
     """Build a workload from a list of bytes / str / sequences of ints."""
-    dt = np.uint8 if coder == ASCII else np.uint16
+    dt = np.uint16 if coder == UNICODE else np.uint8  # byte coders: ASCII, ENGLISH5, ENGLISH6
     parts = []
     for s in strings:
         if isinstance(s, str):
-            s = list(s.encode("latin-1")) if coder == ASCII else list(s.encode("utf-16-le"))
+            s = list(s.encode("latin-1")) if coder != UNICODE else list(s.encode("utf-16-le"))
             if coder == UNICODE:
                 s = [s[2 * k] | (s[2 * k + 1] << 8) for k in range(len(s) // 2)]
         parts.append(np.asarray(list(s), dtype=dt))
