@@ -8,6 +8,7 @@ a GPU fail with HUSKY_ERR_CUDA.
 
 The public functions carry the C names:
   husky_unit_bytes, husky_encode, husky_sort_workspace, husky_sort,
+  husky_sort_keys_workspace, husky_sort_keys,
   husky_sort_host_workspace, husky_sort_host, husky_select_splitters,
   husky_comm_unique_id, husky_comm_create, husky_comm_destroy,
   husky_sort_multi_workspace, husky_sort_multi_plan, husky_sort_multi_recv_workspace,
@@ -23,6 +24,9 @@ import numpy as np
 
 ASCII = 0
 UNICODE = 1
+ENGLISH5 = 2
+ENGLISH6 = 3
+KEY_U64, KEY_I64, KEY_F64 = 0, 1, 2
 HUSKY_OK = 0
 STATUS = {0: "HUSKY_OK", 1: "HUSKY_ERR_INVALID_ARG", 2: "HUSKY_ERR_DOMAIN", 3: "HUSKY_ERR_CUDA",
           4: "HUSKY_ERR_NCCL", 5: "HUSKY_ERR_WORKSPACE", 6: "HUSKY_ERR_CAPACITY"}
@@ -78,6 +82,8 @@ _sig("husky_sort", _ST, _I, _P, _P, _U64, _P, _P, _P, _P, _SZ, ctypes.POINTER(hu
 _sig("husky_sort_host_workspace", _ST, _I, _U64, _U64, ctypes.POINTER(_SZ))
 _sig("husky_sort_host", _ST, _I, _P, _P, _U64, _P, _P, _P, _P, _SZ, ctypes.POINTER(husky_outcome), _P)
 _sig("husky_last_error", ctypes.c_char_p)
+_sig("husky_sort_keys_workspace", _ST, _I, _U64, ctypes.POINTER(_SZ))
+_sig("husky_sort_keys", _ST, _I, _P, _U64, _P, _P, _P, _SZ, _P)
 
 EXPORTED = ["husky_unit_bytes", "husky_encode", "husky_sort_workspace", "husky_sort",
             "husky_sort_host_workspace", "husky_sort_host", "husky_comm_unique_id",
@@ -86,7 +92,8 @@ EXPORTED = ["husky_unit_bytes", "husky_encode", "husky_sort_workspace", "husky_s
             "husky_plan_destroy", "husky_sort_multi", "husky_sort_multi_loopback_workspace",
             "husky_sort_multi_loopback", "husky_select_splitters", "husky_last_error",
             "husky_profile_enable", "husky_profile_reset", "husky_profile_read",
-            "husky_profile_stage_name", "husky_launch_count"]
+            "husky_profile_stage_name", "husky_launch_count", "husky_sort_keys_workspace",
+            "husky_sort_keys"]
 
 _sig("husky_profile_enable", None, _I)
 _sig("husky_profile_reset", None)
@@ -217,6 +224,24 @@ def husky_sort_host(coder, h_units, h_offsets, h_perm, h_sorted_units, h_sorted_
                                 ws.numel() * ws.element_size(), ctypes.byref(out), _stream(stream)),
            "husky_sort_host")
     return out.as_dict()
+
+
+def husky_sort_keys_workspace(key_type, n) -> int:
+    b = _SZ(0)
+    _check(_lib.husky_sort_keys_workspace(key_type, n, ctypes.byref(b)), "husky_sort_keys_workspace")
+    return int(b.value)
+
+
+def husky_sort_keys(key_type, keys, perm, sorted_keys=None, ws=None, stream=None):
+    """Numeric keys (perfect coding): keys = CUDA tensor of 8-byte elements
+    (uint64 bits / int64 / float64).  perm: int32 CUDA tensor [n].  Returns perm."""
+    import torch
+    n = keys.numel()
+    if ws is None:
+        ws = torch.empty(husky_sort_keys_workspace(key_type, n), dtype=torch.uint8, device=keys.device)
+    _check(_lib.husky_sort_keys(key_type, _ptr(keys), n, _ptr(perm), _ptr(sorted_keys), _ptr(ws),
+                                ws.numel() * ws.element_size(), _stream(stream)), "husky_sort_keys")
+    return perm
 
 
 from .multi import (husky_comm_create, husky_comm_destroy, husky_comm_unique_id,  # noqa: E402

@@ -31,17 +31,40 @@ __device__ __forceinline__ uint64_t pack_ascii(uint64_t lo, uint64_t b8) {
   return (x << 7) | (b8 & 0x7F);
 }
 
-// Code of one string from the two aligned words covering its window: w0 holds
-// the byte at address `a` (sh = a & 7), w1 the next word (only read when the
-// window crosses into it).
+// Code of one string from the aligned words covering its window: w0 holds
+// the byte at address `a` (sh = a & 7), w1 / w2 the next words (w2 is used only
+// by the 10- and 12-unit English windows).
 template <int CODER>
-__device__ __forceinline__ uint64_t encode_words(uint64_t w0, uint64_t w1, int sh, int64_t len,
+__device__ __forceinline__ uint64_t encode_words(uint64_t w0, uint64_t w1, uint64_t w2, int sh, int64_t len,
                                                  uint32_t &viol) {
   using T = CoderTraits<CODER>;
   if (len < 0) { viol |= kOffsetsBad; len = 0; }
   if (len > T::kPL) viol |= kNotPerfect;
   uint64_t lo = sh ? ((w0 >> (8 * sh)) | (w1 << (64 - 8 * sh))) : w0;
-  if (CODER == HUSKY_CODER_ASCII) {
+  if constexpr (CODER == HUSKY_CODER_ENGLISH5 || CODER == HUSKY_CODER_ENGLISH6) {
+    // Alg. 4 with (K, bits, 2^bits - 1): fold the first m = min(len, K) bytes,
+    // then shift by bits * (K - m) -- the same arithmetic as the closed form
+    // sum_{i<m} (u_i & mask) << bits * (K - 1 - i)
+    constexpr int K = T::kK, B = T::kBits;
+    constexpr uint32_t mask = (1u << B) - 1;
+    const uint64_t hi = sh ? ((w1 >> (8 * sh)) | (w2 << (64 - 8 * sh))) : w1;  // bytes 8..15
+    const int m = len < K ? (int)len : K;
+    uint64_t r = 0;
+    uint32_t bad_lo = 0, bad_up = 0, bad_letter = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const uint32_t u = (uint32_t)(((i < 8) ? (lo >> (8 * i)) : (hi >> (8 * (i - 8)))) & 0xFF);
+      const bool in = i < m;
+      const bool lower = u >= 0x61 && u <= 0x7A, upper = u >= 0x41 && u <= 0x5A;
+      bad_lo |= in && !lower;
+      bad_up |= in && !upper;
+      bad_letter |= in && !(lower || upper);
+      r = (r << B) | (in ? (u & mask) : 0u);
+    }
+    if (CODER == HUSKY_CODER_ENGLISH5) viol |= (bad_lo ? kNotLower : 0u) | (bad_up ? kNotUpper : 0u);
+    else if (bad_letter) viol |= kDomainBad;
+    return r;
+  } else if constexpr (CODER == HUSKY_CODER_ASCII) {
     int m = len < 9 ? (int)len : 9;
     uint64_t b8 = (m == 9) ? ((w1 >> (8 * sh)) & 0xFF) : 0ull;
     if (m < 8) lo &= (1ull << (8 * m)) - 1;  // m == 0 -> 0
@@ -95,18 +118,24 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
         o1[k] = ofirst;
       }
     }
-    uint64_t w0[kEncIT], w1[kEncIT];
+    constexpr bool kThird = CODER == HUSKY_CODER_ENGLISH5 || CODER == HUSKY_CODER_ENGLISH6;
+    uint64_t w0[kEncIT], w1[kEncIT], w2[kEncIT];
     int sh[kEncIT];
 #pragma unroll
     for (int k = 0; k < kEncIT; ++k) {
       const uintptr_t a = ub + (uintptr_t)(o0[k] * W);
       sh[k] = (int)(a & 7);
+      w2[k] = 0;
       if (any_units) {
         uintptr_t aw = a & ~(uintptr_t)7;
         aw = aw < lo_word ? lo_word : (aw > hi_word ? hi_word : aw);
         const uintptr_t aw1 = aw + 8 > hi_word ? hi_word : aw + 8;
         w0[k] = __ldg((const uint64_t *)aw);
         w1[k] = __ldg((const uint64_t *)aw1);
+        if (kThird) {
+          const uintptr_t aw2 = aw1 + 8 > hi_word ? hi_word : aw1 + 8;
+          w2[k] = __ldg((const uint64_t *)aw2);
+        }
       } else {
         w0[k] = 0;
         w1[k] = 0;
@@ -115,7 +144,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
 #pragma unroll
     for (int k = 0; k < kEncIT; ++k) {
       const uint64_t i = base + threadIdx.x + (uint64_t)k * blockDim.x;
-      const uint64_t c = encode_words<CODER>(w0[k], w1[k], sh[k], o1[k] - o0[k], viol);
+      const uint64_t c = encode_words<CODER>(w0[k], w1[k], w2[k], sh[k], o1[k] - o0[k], viol);
       if (i < n) {
         codes[i] = c;
         kor |= c;
@@ -187,10 +216,20 @@ void launch_encode(int coder, bool hist, const void *units, const int64_t *offse
     uint64_t blocks = (n + kEncThreads * kEncIT - 1) / (kEncThreads * kEncIT);
     const uint64_t cap = (uint64_t)num_sms * kEncBlocksPerSM;
     if (blocks > cap) blocks = cap;
-    if (coder == HUSKY_CODER_ASCII)
-      k_encode<HUSKY_CODER_ASCII><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, st, packed);
-    else
-      k_encode<HUSKY_CODER_UNICODE><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, st, packed);
+    switch (coder) {
+      case HUSKY_CODER_ASCII:
+        k_encode<HUSKY_CODER_ASCII><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, st, packed);
+        break;
+      case HUSKY_CODER_UNICODE:
+        k_encode<HUSKY_CODER_UNICODE><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, st, packed);
+        break;
+      case HUSKY_CODER_ENGLISH5:
+        k_encode<HUSKY_CODER_ENGLISH5><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, st, packed);
+        break;
+      default:
+        k_encode<HUSKY_CODER_ENGLISH6><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, st, packed);
+        break;
+    }
   }
   if (hist) launch_hist8(codes, n, st, num_sms, s);
 }

@@ -26,6 +26,19 @@ struct Layout {
 Layout make_layout(uint64_t n);
 
 husky_status fail(husky_status st, const char *fmt, ...);
+
+inline bool valid_coder(int c) { return c >= HUSKY_CODER_ASCII && c <= HUSKY_CODER_ENGLISH6; }
+inline size_t coder_unit_bytes(int c) { return c == HUSKY_CODER_UNICODE ? 2 : (valid_coder(c) ? 1 : 0); }
+// Kernels other than the encoder are instantiated for the unit type only: the
+// byte coders (ASCII, ENGLISH5/6) share the ASCII instantiation.
+inline int kernel_coder(int c) { return c == HUSKY_CODER_UNICODE ? HUSKY_CODER_UNICODE : HUSKY_CODER_ASCII; }
+// Input outside the coder's domain inside a code window (readings R5, R15):
+// the equal-run fix-up is exact only on the domain.
+inline bool domain_violation(int c, uint32_t viol) {
+  if (c == HUSKY_CODER_ASCII || c == HUSKY_CODER_ENGLISH6) return (viol & kDomainBad) != 0;
+  if (c == HUSKY_CODER_ENGLISH5) return (viol & kNotLower) && (viol & kNotUpper);
+  return false;
+}
 int device_sm_count();
 
 // The single-GPU path (husky_sort) -- also the local phase of the sample sort.

@@ -151,8 +151,9 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
                        uint32_t *d_perm, void *d_sorted_units, int64_t *d_sorted_offsets, void *d_ws,
                        size_t ws_bytes, husky_outcome *h_out, cudaStream_t s) {
   if (h_out) memset(h_out, 0, sizeof *h_out);
-  if (coder != HUSKY_CODER_ASCII && coder != HUSKY_CODER_UNICODE)
-    return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  // byte coders share the ASCII instantiation of every kernel but the encoder
+  const int kc = kernel_coder(coder);
   if (n >= 0xFFFFFFFFull) return fail(HUSKY_ERR_INVALID_ARG, "n = %llu >= 2^32 - 1", (unsigned long long)n);
   if ((d_sorted_units == nullptr) != (d_sorted_offsets == nullptr))
     return fail(HUSKY_ERR_INVALID_ARG, "d_sorted_units and d_sorted_offsets must both be set or both NULL");
@@ -170,7 +171,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
     return fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, L.total);
 
   Sorter S;
-  S.coder = coder;
+  S.coder = kc;
   S.units = d_units;
   S.offsets = d_offsets;
   S.n = n;
@@ -188,7 +189,8 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // ---- A1 encode (+ digit histograms, flags) and the histogram scan
   // n <= 2^28: the payload carries min(len, 15) in its top 4 bits, so the
   // gather rebuilds strings of length <= PL from their code (no random reads)
-  const bool packed = n <= kPackMaxN;
+  // the gather rebuilds short strings from ASCII / UNICODE codes only
+  const bool packed = n <= kPackMaxN && (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE);
   uint32_t *packed_payload = packed ? S.at<uint32_t>(L.vals2) : nullptr;
   uint64_t *keysA = S.keysA(), *keysB = S.keysB();
   uint32_t *vals_tmp = S.at<uint32_t>(L.vals);
@@ -247,7 +249,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // a second random perm -> offsets -> units walk; only spans the fix-up
   // reorders are gathered again (rare outside all-colliding inputs).
   if (d_sorted_units)
-    launch_gather(coder, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),
+    launch_gather(kc, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),
                   S.next_counter(), S.next_epoch(), s, nullptr, packed, nullptr, st);
   debug_check_perm(d_perm, n, "key sort", s);
 
@@ -256,7 +258,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   uint8_t *dirty = S.at<uint8_t>(L.dirty);
   uint2 *list_sm = S.at<uint2>(L.list_sm), *list_g = S.at<uint2>(L.list_g);
   HCHECK(cudaMemsetAsync(dirty, 0, L.cap_sm, s));
-  launch_runs_scan(coder, 0, nullptr, n, d_perm, d_units, d_offsets, 0, run_start, run_end, dirty, st,
+  launch_runs_scan(kc, 0, nullptr, n, d_perm, d_units, d_offsets, 0, run_start, run_end, dirty, st,
                    S.lb_scan(), S.next_counter(), S.next_epoch(), s, d_sorted_units, d_sorted_offsets);
   launch_runs_classify(run_start, run_end, dirty, st, list_sm, L.cap_sm, list_g, true, S.sms, s);
 
@@ -264,18 +266,19 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // A4 again for the spans it reordered.  Enqueued optimistically before the
   // host knows whether there are giant runs: giant runs are disjoint from the
   // small/medium ones, so their refinement below only appends list entries.
-  launch_fix_small(coder, list_sm, st, d_perm, d_units, d_offsets, S.sms, s);
-  launch_fix_medium(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s);
+  launch_fix_small(kc, list_sm, st, d_perm, d_units, d_offsets, S.sms, s);
+  launch_fix_medium(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s);
   if (d_sorted_units)
-    launch_regather_runs(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, d_sorted_units,
+    launch_regather_runs(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, d_sorted_units,
                          d_sorted_offsets, S.sms, s);
   DevState hs;
   HCHECK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, s));
   HCHECK(cudaStreamSynchronize(s));
   if (husky_status e = cuda_check("sort")) return e;
   if (hs.violations & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing");
-  if (coder == HUSKY_CODER_ASCII && (hs.violations & kDomainBad))
-    return fail(HUSKY_ERR_DOMAIN, "ASCII coder: a unit > 0x7F inside a code prefix (Alg. 4 mask is not monotone there)");
+  if (domain_violation(coder, hs.violations))
+    return fail(HUSKY_ERR_DOMAIN, "coder %d: a unit outside the coder's domain inside a code window (Alg. 4's mask "
+                "is not monotone there; readings R5, R15)", coder);
   if (!use_msd) S.radix_passes = hs.np;
   debug_check_perm(d_perm, n, "fix-up", s);
 
@@ -286,7 +289,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   }
   if (h_out) {
     h_out->perfect = !(hs.violations & kNotPerfect);
-    h_out->domain_ok = !(hs.violations & kDomainBad) || coder != HUSKY_CODER_ASCII;
+    h_out->domain_ok = !domain_violation(coder, hs.violations);
     h_out->n_in_runs = hs.n_in_runs;
     h_out->max_run = hs.max_run;
     for (int c = 0; c < 4; ++c) h_out->runs_by_class[c] = hs.runs_by_class[c];
@@ -458,15 +461,14 @@ uint64_t husky_launch_count(void) {
 }
 
 size_t husky_unit_bytes(int coder) {
-  return coder == HUSKY_CODER_ASCII ? 1 : coder == HUSKY_CODER_UNICODE ? 2 : 0;
+  return coder_unit_bytes(coder);
 }
 
 const char *husky_last_error(void) { return g_last_error.c_str(); }
 
 husky_status husky_encode(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
                           uint64_t *d_codes, int32_t *h_perfect, void *stream) {
-  if (coder != HUSKY_CODER_ASCII && coder != HUSKY_CODER_UNICODE)
-    return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
   cudaStream_t s = (cudaStream_t)stream;
   if (n == 0) {
     if (h_perfect) *h_perfect = 1;
@@ -493,8 +495,7 @@ husky_status husky_encode(int coder, const void *d_units, const int64_t *d_offse
 
 husky_status husky_sort_workspace(int coder, uint64_t n, uint64_t total_units, size_t *bytes) {
   (void)total_units;
-  if (coder != HUSKY_CODER_ASCII && coder != HUSKY_CODER_UNICODE)
-    return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
   if (!bytes) return fail(HUSKY_ERR_INVALID_ARG, "bytes is NULL");
   *bytes = make_layout(n).total;
   return HUSKY_OK;
@@ -522,8 +523,7 @@ static size_t host_layout(int coder, uint64_t n, uint64_t total_units, size_t *o
 }
 
 husky_status husky_sort_host_workspace(int coder, uint64_t n, uint64_t total_units, size_t *bytes) {
-  if (coder != HUSKY_CODER_ASCII && coder != HUSKY_CODER_UNICODE)
-    return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
   if (!bytes) return fail(HUSKY_ERR_INVALID_ARG, "bytes is NULL");
   size_t a, b, c, d, e, f;
   *bytes = host_layout(coder, n, total_units, &a, &b, &c, &d, &e, &f);
@@ -533,8 +533,7 @@ husky_status husky_sort_host_workspace(int coder, uint64_t n, uint64_t total_uni
 husky_status husky_sort_host(int coder, const void *h_units, const int64_t *h_offsets, uint64_t n,
                              uint32_t *h_perm, void *h_sorted_units, int64_t *h_sorted_offsets,
                              void *d_ws, size_t ws_bytes, husky_outcome *h_out, void *stream) {
-  if (coder != HUSKY_CODER_ASCII && coder != HUSKY_CODER_UNICODE)
-    return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
   if (!h_offsets || (n && (!h_perm || !h_units)) || !d_ws)
     return fail(HUSKY_ERR_INVALID_ARG, "null required pointer");
   cudaStream_t s = (cudaStream_t)stream;

@@ -31,11 +31,29 @@ template <> struct CoderTraits<HUSKY_CODER_UNICODE> {
   static constexpr int kTagCap = 4;
 };
 
+// ENGLISH5 / ENGLISH6 (reading R15): byte units; only the
+// encoder is specific to them -- every other kernel runs its ASCII (byte)
+// instantiation, whose S = 9 / PL = 9 are conservative for these coders (equal
+// 5/6-bit codes on the coder's domain imply equal first 12 / 10 units).
+template <> struct CoderTraits<HUSKY_CODER_ENGLISH5> {
+  using unit_t = uint8_t;
+  static constexpr int kUnitBytes = 1, kS = 12, kPL = 12, kK = 12, kBits = 5;
+  static constexpr int kWin = 7, kTagCap = 8;
+};
+template <> struct CoderTraits<HUSKY_CODER_ENGLISH6> {
+  using unit_t = uint8_t;
+  static constexpr int kUnitBytes = 1, kS = 10, kPL = 10, kK = 10, kBits = 6;
+  static constexpr int kWin = 7, kTagCap = 8;
+};
+
 constexpr int kSmallMax = 32;    // dirty runs up to this many strings: one warp
 constexpr int kMediumMax = 4096; // ... up to this many: one CTA (bitonic in smem)
 
 // violation bits (OR-reduced; zero-initialised state)
 constexpr uint32_t kNotPerfect = 1u, kDomainBad = 2u, kOffsetsBad = 4u;
+// ENGLISH5 domain (reading R15): a window unit that is not a lowercase / not an
+// uppercase letter; the domain holds unless both bits are set
+constexpr uint32_t kNotLower = 8u, kNotUpper = 16u;
 
 // ------------------------------------------------------ device-resident state
 // Lives at the start of the caller's workspace; zeroed once per husky_sort.

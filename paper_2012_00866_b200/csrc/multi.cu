@@ -168,7 +168,7 @@ static MultiLayout make_multi_layout(int coder, uint64_t n, uint64_t units, int 
   MultiLayout M;
   size_t off = 0;
   auto take = [&](size_t b) { size_t o = off; off = align_up(off + b, 256); return o; };
-  size_t w = coder == HUSKY_CODER_ASCII ? 1 : 2;
+  size_t w = coder_unit_bytes(coder);
   Layout &L = M.L;
   L.n = n;
   L.tiles_r = radix_tiles(n);
@@ -201,7 +201,7 @@ static RecvLayout make_recv_layout(int coder, uint64_t n_out, uint64_t units_out
   RecvLayout R;
   size_t off = 0;
   auto take = [&](size_t b) { size_t o = off; off = align_up(off + b, 256); return o; };
-  size_t w = coder == HUSKY_CODER_ASCII ? 1 : 2;
+  size_t w = coder_unit_bytes(coder);
   R.units = take(units_out * w + 16);
   R.offsets = take((n_out + 1) * 8);
   R.lens = take(n_out * 4 + 4);
@@ -229,7 +229,7 @@ struct Plan {
 
   template <typename T> T *at(size_t o) const { return reinterpret_cast<T *>(ws + o); }
   DevState *st() const { return at<DevState>(M.L.state); }
-  size_t w() const { return coder == HUSKY_CODER_ASCII ? 1 : 2; }
+  size_t w() const { return coder_unit_bytes(coder); }
 
   void init_sorter() {
     S.coder = coder;
@@ -273,8 +273,9 @@ struct Plan {
       }
     }
     if (viol & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing (some rank)");
-    if (coder == HUSKY_CODER_ASCII && (viol & kDomainBad))
-      return fail(HUSKY_ERR_DOMAIN, "ASCII coder: a unit > 0x7F inside a code prefix (some rank)");
+    if (domain_violation(coder, viol))
+      return fail(HUSKY_ERR_DOMAIN, "coder %d: a unit outside the coder's domain inside a code window (some rank)",
+                  coder);
     splitters.assign(world > 1 ? world - 1 : 0, 0);
     if (world > 1) husky_select_splitters(smp.data(), smp.size(), world, splitters.data());
     if (world > 1)
@@ -324,7 +325,7 @@ struct Plan {
     HUSKY_SCOPE(ST_MULTI, s, 0);
     k_send_meta<<<grid_for(n), 256, 0, s>>>(at<uint32_t>(M.send_perm), n, offsets, (uint32_t)gbase,
                                             at<uint32_t>(M.send_gidx), at<uint32_t>(M.send_lens));
-    launch_gather(coder, at<uint32_t>(M.send_perm), n, units, offsets, at<void>(M.send_units),
+    launch_gather(kernel_coder(coder), at<uint32_t>(M.send_perm), n, units, offsets, at<void>(M.send_units),
                   at<int64_t>(M.send_offsets), S.lb_scan(), S.next_counter(), S.next_epoch(), s);
     HCHECK(cudaGetLastError());
     return HUSKY_OK;
@@ -406,7 +407,6 @@ static husky_status nccl_exchange(Plan &P, uint8_t *rws, const RecvLayout &R) {
   return HUSKY_OK;
 }
 
-static bool valid_coder(int c) { return c == HUSKY_CODER_ASCII || c == HUSKY_CODER_UNICODE; }
 
 }  // namespace husky
 
@@ -657,7 +657,7 @@ husky_status husky_sort_multi_loopback(int coder, int world, const void *d_units
   for (auto &p : P) if (husky_status e = p.read_counts()) return e;
   for (auto &p : P) if (husky_status e = p.phase3()) return e;
   // data exchange + local sorts, one destination rank at a time (shared recv ws)
-  const size_t w = coder == HUSKY_CODER_ASCII ? 1 : 2;
+  const size_t w = coder_unit_bytes(coder);
   uint64_t out_n = 0, out_u = 0;
   husky_outcome agg;
   memset(&agg, 0, sizeof agg);

@@ -42,6 +42,10 @@ def test_library_is_sm100a_only():
 def test_unit_bytes_and_workspace_queries():
     import paper_2012_00866_b200 as h
     assert h.husky_unit_bytes(0) == 1 and h.husky_unit_bytes(1) == 2 and h.husky_unit_bytes(7) == 0
+    assert h.husky_unit_bytes(2) == 1 and h.husky_unit_bytes(3) == 1
+    assert h.husky_sort_keys_workspace(2, 1000) > 1000 * 20
+    with pytest.raises(h.HuskyError):
+        h.husky_sort_keys_workspace(3, 10)
     w1 = h.husky_sort_workspace(0, 10_000_000)
     w2 = h.husky_sort_workspace(0, 20_000_000)
     assert 10_000_000 * 20 < w1 < w2
