@@ -161,9 +161,10 @@ husky_status husky_sort_host(int coder, const void *h_units, const int64_t *h_of
 /* ------------------------------------------------------------------ multi-GPU
  * Sample sort over P ranks (one process per GPU).  Input is block-distributed
  * by global index: rank r holds strings [global_base_r, global_base_r + n_local)
- * (reading R12).  Splitters are husky codes, so no run of equal codes straddles
- * ranks; after one all-to-all each rank sorts its bucket with the single-GPU
- * path.  Rank r's output is its shard of the global order; the global result is
+ * (reading R12).  Splitters are sampled string prefixes compared in the sort
+ * order (code first, units on a code tie), so equal strings never straddle
+ * ranks and all-colliding codes still spread; after one all-to-all each rank
+ * sorts its bucket with the single-GPU path.  Rank r's output is its shard of the global order; the global result is
  * the concatenation of the shards in rank order.  perm entries are GLOBAL indices.
  */
 
@@ -219,12 +220,16 @@ husky_status husky_sort_multi_loopback(int coder, int world, const void *d_units
                                        int64_t *d_sorted_offsets, void *d_ws, size_t ws_bytes,
                                        uint64_t *h_shard_n, husky_outcome *h_out, void *stream);
 
-/* Host-side splitter selection used by the sample sort, exposed for testing
- * (no GPU needed): given the P*s gathered sample codes (any order), writes the
- * P-1 splitters: the sorted samples at positions floor(k*P*s/P), k = 1..P-1.
- * Bucket of a code = number of splitters <= code. */
-husky_status husky_select_splitters(const uint64_t *h_samples, uint64_t n_samples, int world,
-                                    uint64_t *h_splitters);
+/* The sample sort's splitter rule, on the host, exposed for testing (no GPU
+ * needed; multi-GPU ranks apply the same rule on the GPU).  Input: the m
+ * gathered sample strings (each rank's prefixes of at most 32 units, rank-major)
+ * as units + offsets[m+1].  Output: h_idx[k-1] (k = 1..P-1) = index of the
+ * sample at position floor(k*m/P) of the samples sorted in the sort order
+ * (ties by index).  Splitter k is that sample's string; bucket(x) = number of
+ * splitters <= x in the sort order (composite splitters, SURVEY.md 8(f)
+ * NEXT-1): equal-code runs may straddle ranks, equal strings never do. */
+husky_status husky_select_splitters(int coder, const void *h_units, const int64_t *h_offsets, uint64_t m,
+                                    int world, uint64_t *h_idx);
 
 /* --------------------------------------------------------------- profiling
  * Per-stage accounting (the T1/T2/T3 split of PAPER.md:238-245, per kernel

@@ -3,15 +3,21 @@
 // that runs P virtual ranks through the very same phases with device-to-device
 // copies as the transport (used to test the sharded path on one GPU).
 //
-// Not in the paper (single-threaded Java); the design follows
-// from the husky-code contract: buckets are ranges of CODES,
-// so a run of equal codes never straddles two GPUs and every rank can resolve
-// its runs locally.  Phases:
-//   1. encode the local strings (A1) and take s regular samples of the codes;
+// Not in the paper (single-threaded Java).  Splitters are
+// STRINGS (composite splitters): a splitter is
+// the prefix (<= kPrefixUnits units) of a sampled string, and bucket(x) =
+// #splitters <= x in the sort order itself (code first -- the code is a
+// function of the prefix, PAPER.md:195-211 -- then the units).  Equal-code runs
+// may therefore straddle ranks (an all-colliding input like C4 spreads over all
+// GPUs), while equal STRINGS never do, and the concatenation of the locally
+// sorted buckets is the global order.  Phases:
+//   1. encode the local strings (A1); take s regular samples: code + prefix;
 //      all-gather the P*s samples (+ each rank's input-violation word);
-//   2. every rank picks the same P-1 splitters (husky_select_splitters);
-//      bucket(code) = #splitters <= code; per-destination string/unit counts;
-//      all-to-all of the counts (grouped send/recv);
+//   2. every rank sorts the gathered sample prefixes on the GPU (husky_sort of
+//      the samples) and picks the same P-1 splitters (the rule of
+//      husky_select_splitters); bucket(x) = #splitters <= x (binary search,
+//      strings compared only on code ties); per-destination string/unit
+//      counts; all-to-all of the counts (grouped send/recv);
 //   3. stable partition by bucket = one onesweep pass on the bucket digit, then
 //      the A4 gather builds the send buffers (units, lengths, global indices);
 //      grouped ncclSend/ncclRecv of the three arrays;
@@ -31,6 +37,17 @@ namespace husky {
 constexpr int kSamplesPerRank = 4096;
 constexpr int kMaxWorld = 256;  // bucket ids must fit one radix digit
 constexpr int kSampleStride = kSamplesPerRank + 1;  // + the rank's violation word
+// A sample / splitter string: its code, its length capped at kPrefixUnits and
+// the first kPrefixUnits units (zero-filled).  Equal prefixes cannot be split,
+// so only strings sharing a 32-unit prefix are kept on one rank.
+constexpr int kPrefixUnits = 32;
+struct SampleRec {
+  uint64_t code;
+  uint32_t len;  // min(length, kPrefixUnits); 0xFFFFFFFF: no sample (empty rank)
+  uint32_t pad;
+  uint8_t u[kPrefixUnits * 2];
+};
+static_assert(sizeof(SampleRec) == 80, "SampleRec layout");
 
 #define HCHECK(expr)                                                                               \
   do {                                                                                             \
@@ -51,29 +68,97 @@ __global__ void k_sample(const uint64_t *__restrict__ codes, uint64_t n, uint64_
   if (threadIdx.x == 0) out[kSamplesPerRank] = st->violations;
 }
 
+// the sample records of one rank: s regular samples (positions i*n/s)
+template <int W>
+__global__ void k_sample_str(const uint64_t *__restrict__ codes, uint64_t n, const void *__restrict__ units,
+                             const int64_t *__restrict__ offsets, SampleRec *__restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kSamplesPerRank; i += gridDim.x * blockDim.x) {
+    SampleRec r;
+    memset(&r, 0, sizeof r);
+    if (n == 0) {
+      r.len = 0xFFFFFFFFu;
+    } else {
+      const uint64_t p = (uint64_t)i * n / kSamplesPerRank;
+      const int64_t o = offsets[p], L = offsets[p + 1] - o;
+      const uint32_t m = (uint32_t)(L < kPrefixUnits ? L : kPrefixUnits);
+      r.code = codes[p];
+      r.len = m;
+      const uint8_t *src = (const uint8_t *)units + o * W;
+      for (uint32_t b = 0; b < m * W; ++b) r.u[b] = src[b];
+    }
+    out[i] = r;
+  }
+}
+
+// gathered records of the non-empty ranks -> a string array (units + offsets)
+// for the GPU sort of the samples: lengths first (scanned by k_lens_to_offsets),
+// then the units at their offsets
+__device__ __forceinline__ const SampleRec &sample_rec(const SampleRec *recs, const int *ranks, uint64_t i) {
+  return recs[(uint64_t)ranks[i / kSamplesPerRank] * kSamplesPerRank + i % kSamplesPerRank];
+}
+__global__ void k_sample_lens(const SampleRec *__restrict__ recs, const int *__restrict__ ranks, uint64_t m,
+                              uint32_t *__restrict__ lens) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+    lens[i] = sample_rec(recs, ranks, i).len;
+}
+template <int W>
+__global__ void k_sample_units(const SampleRec *__restrict__ recs, const int *__restrict__ ranks, uint64_t m,
+                               const int64_t *__restrict__ so, uint8_t *__restrict__ su) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const SampleRec &r = sample_rec(recs, ranks, i);
+    for (uint32_t b = 0; b < r.len * W; ++b) su[so[i] * W + b] = r.u[b];
+  }
+}
+
+// splitter k (1..P-1) = the sample at sorted position floor(k*m/P)
+__global__ void k_pick_splitters(const SampleRec *__restrict__ recs, const int *__restrict__ ranks, uint64_t m,
+                                 const uint32_t *__restrict__ sorted, int world, SampleRec *__restrict__ split) {
+  for (int k = 1 + threadIdx.x; k < world; k += blockDim.x) {
+    split[k - 1] = sample_rec(recs, ranks, sorted[(uint64_t)((unsigned __int128)k * m / world)]);
+  }
+}
+
+// x (code c, units xs[0..xl)) >= splitter?  Code first; on a code tie the units
+// (unsigned, position by position), then the shorter string first.
+template <int W>
+__device__ __forceinline__ bool ge_splitter(uint64_t c, const uint8_t *xs, int64_t xl, const SampleRec &sp) {
+  if (c != sp.code) return c > sp.code;
+  const int64_t m = xl < (int64_t)sp.len ? xl : (int64_t)sp.len;
+  for (int64_t k = 0; k < m; ++k) {
+    uint32_t a, b;
+    if (W == 1) { a = xs[k]; b = sp.u[k]; }
+    else { a = ((const uint16_t *)xs)[k]; b = ((const uint16_t *)sp.u)[k]; }
+    if (a != b) return a > b;
+  }
+  return xl >= (int64_t)sp.len;
+}
+
+template <int W>
 __global__ void __launch_bounds__(256)
-    k_bucket(const uint64_t *__restrict__ codes, uint64_t n, const uint64_t *__restrict__ splitters,
-             int nsplit, int world, const int64_t *__restrict__ offsets, uint64_t *__restrict__ keys,
-             DevState *st, unsigned long long *counts) {
-  __shared__ uint64_t s_split[kMaxWorld];
+    k_bucket(const uint64_t *__restrict__ codes, uint64_t n, const SampleRec *__restrict__ splitters,
+             int nsplit, int world, const void *__restrict__ units, const int64_t *__restrict__ offsets,
+             uint64_t *__restrict__ keys, DevState *st, unsigned long long *counts) {
+  __shared__ SampleRec s_split[kMaxWorld - 1];
   __shared__ unsigned long long s_cnt[kMaxWorld], s_units[kMaxWorld];
+  for (int i = threadIdx.x; i < nsplit; i += blockDim.x) s_split[i] = splitters[i];
   for (int i = threadIdx.x; i < kMaxWorld; i += blockDim.x) {
-    s_split[i] = i < nsplit ? splitters[i] : ~0ull;
     s_cnt[i] = 0;
     s_units[i] = 0;
   }
   __syncthreads();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t c = codes[i];
-    int lo = 0, hi = nsplit;  // number of splitters <= c
+    const uint64_t c = codes[i];
+    const int64_t o = offsets[i], L = offsets[i + 1] - o;
+    const uint8_t *xs = (const uint8_t *)units + o * W;
+    int lo = 0, hi = nsplit;  // number of splitters <= x
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
-      if (s_split[mid] <= c) lo = mid + 1;
+      if (ge_splitter<W>(c, xs, L, s_split[mid])) lo = mid + 1;
       else hi = mid;
     }
     keys[i] = (uint64_t)lo;
     atomicAdd(&s_cnt[lo], 1ull);
-    atomicAdd(&s_units[lo], (unsigned long long)(offsets[i + 1] - offsets[i]));
+    atomicAdd(&s_units[lo], (unsigned long long)L);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < world; b += blockDim.x) {
@@ -162,6 +247,9 @@ struct MultiLayout {
   Layout L;  // state, keysA (= codes), keysB, vals, lb_radix, lb_scan used by the Sorter
   size_t send_perm = 0, samples = 0, splitters = 0, counts = 0, rcounts = 0, send_units = 0,
          send_offsets = 0, send_gidx = 0, send_lens = 0, total = 0;
+  // composite splitters: gathered sample records, their packed strings, the
+  // GPU sort of the samples (perm + workspace), the non-empty rank list
+  size_t recs = 0, smp_units = 0, smp_offsets = 0, smp_lens = 0, smp_lb = 0, smp_perm = 0, smp_ws = 0, ranks = 0;
 };
 
 static MultiLayout make_multi_layout(int coder, uint64_t n, uint64_t units, int world) {
@@ -182,7 +270,16 @@ static MultiLayout make_multi_layout(int coder, uint64_t n, uint64_t units, int 
   L.lb_scan = take(L.tiles_s * 8 + 8);
   M.send_perm = take(n * 4 + 4);
   M.samples = take((size_t)world * kSampleStride * 8);
-  M.splitters = take((size_t)world * 8);
+  M.splitters = take((size_t)world * sizeof(SampleRec));
+  const uint64_t ms = (uint64_t)world * kSamplesPerRank;
+  M.recs = take(ms * sizeof(SampleRec));
+  M.smp_units = take(ms * kPrefixUnits * w + 16);
+  M.smp_offsets = take((ms + 1) * 8);
+  M.smp_lens = take(ms * 4);
+  M.smp_lb = take(scan_tiles(ms) * 8 + 8);
+  M.smp_perm = take(ms * 4 + 4);
+  M.smp_ws = take(make_layout(ms).total);
+  M.ranks = take((size_t)world * 4);
   M.counts = take((size_t)world * 16);
   M.rcounts = take((size_t)world * 16);
   M.send_units = take(units * w + 16);
@@ -225,7 +322,6 @@ struct Plan {
   Sorter S;
   std::vector<uint64_t> send_cnt, send_u, recv_cnt, recv_u;  // per peer
   uint64_t n_out = 0, units_out = 0;
-  std::vector<uint64_t> splitters;
 
   template <typename T> T *at(size_t o) const { return reinterpret_cast<T *>(ws + o); }
   DevState *st() const { return at<DevState>(M.L.state); }
@@ -253,6 +349,9 @@ struct Plan {
     HUSKY_SCOPE(ST_MULTI, s, 0);
     k_sample<<<1, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, at<uint64_t>(M.samples) + (size_t)rank * kSampleStride,
                                st());
+    SampleRec *mine = at<SampleRec>(M.recs) + (size_t)rank * kSamplesPerRank;
+    if (w() == 1) k_sample_str<1><<<16, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, units, offsets, mine);
+    else k_sample_str<2><<<16, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, units, offsets, mine);
     HCHECK(cudaGetLastError());
     return HUSKY_OK;
   }
@@ -263,24 +362,50 @@ struct Plan {
     HCHECK(cudaMemcpyAsync(all.data(), at<uint64_t>(M.samples), all.size() * 8, cudaMemcpyDeviceToHost, s));
     HCHECK(cudaStreamSynchronize(s));
     uint32_t viol = 0;
-    std::vector<uint64_t> smp;
-    smp.reserve((size_t)world * kSamplesPerRank);
+    std::vector<int> ranks;  // ranks with strings (a rank's samples are all valid or all absent)
     for (int r = 0; r < world; ++r) {
       viol |= (uint32_t)all[(size_t)r * kSampleStride + kSamplesPerRank];
-      for (int i = 0; i < kSamplesPerRank; ++i) {
-        uint64_t v = all[(size_t)r * kSampleStride + i];
-        if (v != ~0ull) smp.push_back(v);
-      }
+      if (all[(size_t)r * kSampleStride] != ~0ull) ranks.push_back(r);
     }
     if (viol & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing (some rank)");
     if (domain_violation(coder, viol))
       return fail(HUSKY_ERR_DOMAIN, "coder %d: a unit outside the coder's domain inside a code window (some rank)",
                   coder);
-    splitters.assign(world > 1 ? world - 1 : 0, 0);
-    if (world > 1) husky_select_splitters(smp.data(), smp.size(), world, splitters.data());
-    if (world > 1)
-      HCHECK(cudaMemcpyAsync(at<uint64_t>(M.splitters), splitters.data(), splitters.size() * 8,
-                             cudaMemcpyHostToDevice, s));
+    if (world == 1) return HUSKY_OK;
+    SampleRec *split = at<SampleRec>(M.splitters);
+    const uint64_t m = (uint64_t)ranks.size() * kSamplesPerRank;
+    if (m == 0) {  // no strings anywhere: any splitters
+      HCHECK(cudaMemsetAsync(split, 0, (size_t)(world - 1) * sizeof(SampleRec), s));
+      return HUSKY_OK;
+    }
+    // the same rule as husky_select_splitters, on the GPU: sort the gathered
+    // sample prefixes (index order = rank-major, the host rule's input order)
+    // and take positions floor(k*m/P)
+    HCHECK(cudaMemcpyAsync(at<int>(M.ranks), ranks.data(), ranks.size() * 4, cudaMemcpyHostToDevice, s));
+    const SampleRec *recs = at<SampleRec>(M.recs);
+    const int *rk = at<int>(M.ranks);
+    const unsigned g = grid_for(m);
+    {
+      HUSKY_SCOPE(ST_MULTI, s, 0);
+      k_sample_lens<<<g, 256, 0, s>>>(recs, rk, m, at<uint32_t>(M.smp_lens));
+      HCHECK(cudaMemsetAsync(at<uint8_t>(M.smp_lb), 0, scan_tiles(m) * 8 + 8, s));
+      HCHECK(cudaMemsetAsync(&st()->tile_counter[61], 0, 4, s));
+      k_lens_to_offsets<<<(unsigned)scan_tiles(m), kScanThreads, 0, s>>>(
+          at<uint32_t>(M.smp_lens), m, at<int64_t>(M.smp_offsets), at<unsigned long long>(M.smp_lb),
+          &st()->tile_counter[61], 1, 0);
+      if (w() == 1)
+        k_sample_units<1><<<g, 256, 0, s>>>(recs, rk, m, at<int64_t>(M.smp_offsets), at<uint8_t>(M.smp_units));
+      else
+        k_sample_units<2><<<g, 256, 0, s>>>(recs, rk, m, at<int64_t>(M.smp_offsets), at<uint8_t>(M.smp_units));
+      HCHECK(cudaGetLastError());
+    }
+    if (husky_status e = sort_impl(coder, at<void>(M.smp_units), at<int64_t>(M.smp_offsets), m,
+                                   at<uint32_t>(M.smp_perm), nullptr, nullptr, at<void>(M.smp_ws),
+                                   make_layout(m).total, nullptr, s))
+      return e;
+    HUSKY_SCOPE(ST_MULTI, s, 0);
+    k_pick_splitters<<<1, 256, 0, s>>>(recs, rk, m, at<uint32_t>(M.smp_perm), world, split);
+    HCHECK(cudaGetLastError());
     return HUSKY_OK;
   }
 
@@ -290,8 +415,14 @@ struct Plan {
     if (n) {
       unsigned blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)S.sms * 4);
       HUSKY_SCOPE(ST_MULTI, s, 0);
-      k_bucket<<<blocks, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, at<uint64_t>(M.splitters), world - 1, world,
-                                      offsets, at<uint64_t>(M.L.keysB), st(), at<unsigned long long>(M.counts));
+      if (w() == 1)
+        k_bucket<1><<<blocks, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, at<SampleRec>(M.splitters), world - 1, world,
+                                           units, offsets, at<uint64_t>(M.L.keysB), st(),
+                                           at<unsigned long long>(M.counts));
+      else
+        k_bucket<2><<<blocks, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, at<SampleRec>(M.splitters), world - 1, world,
+                                           units, offsets, at<uint64_t>(M.L.keysB), st(),
+                                           at<unsigned long long>(M.counts));
       launch_hist_scan(n, st(), s);
       HCHECK(cudaGetLastError());
     }
@@ -371,7 +502,12 @@ struct Plan {
 // exchange over NCCL: counts (phase 2) and data (phase 3)
 static husky_status nccl_allgather_samples(Plan &P) {
   uint64_t *buf = P.at<uint64_t>(P.M.samples);
+  SampleRec *recs = P.at<SampleRec>(P.M.recs);
+  NCHECK(ncclGroupStart());
   NCHECK(ncclAllGather(buf + (size_t)P.rank * kSampleStride, buf, kSampleStride, ncclUint64, P.comm->nccl, P.s));
+  NCHECK(ncclAllGather(recs + (size_t)P.rank * kSamplesPerRank, recs, kSamplesPerRank * sizeof(SampleRec), ncclUint8,
+                       P.comm->nccl, P.s));
+  NCHECK(ncclGroupEnd());
   return HUSKY_OK;
 }
 
@@ -414,15 +550,29 @@ using namespace husky;
 
 extern "C" {
 
-husky_status husky_select_splitters(const uint64_t *h_samples, uint64_t n_samples, int world,
-                                    uint64_t *h_splitters) {
+husky_status husky_select_splitters(int coder, const void *h_units, const int64_t *h_offsets, uint64_t m,
+                                    int world, uint64_t *h_idx) {
+  if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
   if (world < 1 || world > kMaxWorld) return fail(HUSKY_ERR_INVALID_ARG, "world %d out of range", world);
-  if (world == 1) return HUSKY_OK;
-  if (!h_splitters || (n_samples && !h_samples)) return fail(HUSKY_ERR_INVALID_ARG, "null pointer");
-  std::vector<uint64_t> v(h_samples, h_samples + n_samples);
-  std::sort(v.begin(), v.end());
-  for (int k = 1; k < world; ++k)
-    h_splitters[k - 1] = n_samples ? v[(size_t)((unsigned __int128)k * n_samples / world)] : ~0ull;
+  if (world == 1 || m == 0) return HUSKY_OK;
+  if (!h_idx || !h_offsets || !h_units) return fail(HUSKY_ERR_INVALID_ARG, "null pointer");
+  const size_t w = coder_unit_bytes(coder);
+  auto unit = [&](int64_t p) -> uint32_t {
+    return w == 1 ? ((const uint8_t *)h_units)[p] : ((const uint16_t *)h_units)[p];
+  };
+  std::vector<uint64_t> idx(m);
+  for (uint64_t i = 0; i < m; ++i) idx[i] = i;
+  // the sort order (units unsigned, shorter first), ties by index
+  std::stable_sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t b) {
+    const int64_t oa = h_offsets[a], la = h_offsets[a + 1] - oa, ob = h_offsets[b], lb = h_offsets[b + 1] - ob;
+    const int64_t k = la < lb ? la : lb;
+    for (int64_t t = 0; t < k; ++t) {
+      const uint32_t x = unit(oa + t), y = unit(ob + t);
+      if (x != y) return x < y;
+    }
+    return la < lb;
+  });
+  for (int k = 1; k < world; ++k) h_idx[k - 1] = idx[(size_t)((unsigned __int128)k * m / world)];
   return HUSKY_OK;
 }
 
@@ -644,9 +794,14 @@ husky_status husky_sort_multi_loopback(int coder, int world, const void *d_units
   for (int r = 0; r < world; ++r)
     for (int q = 0; q < world; ++q)
       if (q != r)
+      {
         HCHECK(cudaMemcpyAsync(P[r].at<uint64_t>(P[r].M.samples) + (size_t)q * kSampleStride,
                                P[q].at<uint64_t>(P[q].M.samples) + (size_t)q * kSampleStride, kSampleStride * 8,
                                cudaMemcpyDeviceToDevice, s));
+        HCHECK(cudaMemcpyAsync(P[r].at<SampleRec>(P[r].M.recs) + (size_t)q * kSamplesPerRank,
+                               P[q].at<SampleRec>(P[q].M.recs) + (size_t)q * kSamplesPerRank,
+                               kSamplesPerRank * sizeof(SampleRec), cudaMemcpyDeviceToDevice, s));
+      }
   for (auto &p : P) if (husky_status e = p.choose_splitters()) return e;
   for (auto &p : P) if (husky_status e = p.phase2()) return e;
   // "all-to-all" of the counts: rcounts[r][q] = counts[q][r]

@@ -26,7 +26,7 @@ def _sig(name, res, *args):
     return f
 
 
-_sig("husky_select_splitters", _ST, _P, _U64, ctypes.c_int, _P)
+_sig("husky_select_splitters", _ST, ctypes.c_int, _P, _P, _U64, ctypes.c_int, _P)
 _sig("husky_comm_unique_id", _ST, _P)
 _sig("husky_comm_create", _ST, ctypes.c_int, ctypes.c_int, _P, ctypes.POINTER(_P))
 _sig("husky_comm_destroy", _ST, _P)
@@ -43,12 +43,15 @@ _sig("husky_sort_multi_loopback", _ST, ctypes.c_int, ctypes.c_int, _P, _P, _U64,
      ctypes.POINTER(husky_outcome), _P)
 
 
-def husky_select_splitters(samples: np.ndarray, world: int) -> np.ndarray:
-    """Host-only (no GPU): P-1 splitters from the gathered samples."""
-    s = np.ascontiguousarray(samples, dtype=np.uint64)
+def husky_select_splitters(coder: int, units: np.ndarray, offsets: np.ndarray, world: int) -> np.ndarray:
+    """Host-only (no GPU): indices of the P-1 splitter samples among the m sample
+    strings (units + offsets), by the sample sort's rule."""
+    u = np.ascontiguousarray(units)
+    o = np.ascontiguousarray(offsets, dtype=np.int64)
+    m = o.size - 1
     out = np.zeros(max(world - 1, 1), dtype=np.uint64)
-    _check(_lib.husky_select_splitters(s.ctypes.data if s.size else None, s.size, world, out.ctypes.data),
-           "husky_select_splitters")
+    _check(_lib.husky_select_splitters(coder, u.ctypes.data if u.size else None, o.ctypes.data, m, world,
+                                       out.ctypes.data), "husky_select_splitters")
     return out[:world - 1]
 
 

@@ -55,10 +55,17 @@ def test_unit_bytes_and_workspace_queries():
 
 
 def test_select_splitters_host():
+    """The sample sort's splitter rule (host copy, no GPU): sample strings sorted
+    in the sort order (ties by index), positions floor(k*m/P)."""
     import paper_2012_00866_b200 as h
+    import workloads as W
     rng = np.random.default_rng(0)
-    s = rng.integers(0, 2**63, size=4 * 4096, dtype=np.uint64)
-    sp = h.husky_select_splitters(s, 4)
-    ss = np.sort(s)
-    assert sp.tolist() == [ss[k * s.size // 4] for k in (1, 2, 3)]
-    assert h.husky_select_splitters(s, 1).size == 0
+    strings = [rng.integers(0x61, 0x64, size=int(rng.integers(0, 6))).tolist() for _ in range(4 * 4096)]
+    w = W.from_strings(strings, 0)
+    idx = h.husky_select_splitters(0, w.units, w.offsets, 4)
+    order = sorted(range(len(strings)), key=lambda i: (strings[i], i))
+    m = len(strings)
+    assert idx.tolist() == [order[k * m // 4] for k in (1, 2, 3)]
+    assert h.husky_select_splitters(0, w.units, w.offsets, 1).size == 0
+    u = W.from_strings([[0x4E00, 5], [0x4E00], [3]], 1)
+    assert h.husky_select_splitters(1, u.units, u.offsets, 3).tolist() == [1, 0]

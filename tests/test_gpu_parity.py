@@ -289,10 +289,11 @@ def test_sort_repeatable_and_workspace_reuse(torch, h):
 
 # ------------------------------------------------------- sharded (loopback)
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
-@pytest.mark.parametrize("name,n", [("C1", 60_000), ("C3", 100_000), ("C4", 50_000)])
+@pytest.mark.parametrize("name,n", [("C1", 60_000), ("C3", 100_000), ("C4", 50_000), ("C2", 80_000)])
 def test_multi_loopback_vs_oracle(torch, h, oracle_mod, world, name, n):
     """Sample sort over `world` virtual ranks on one GPU: concatenation of the
-    shards == oracle; no equal-code run straddles shards."""
+    shards == oracle; equal strings never straddle shards; shard sizes follow
+    the splitter rule; C4 (all codes equal) spreads evenly."""
     w = W.make(name, n)
     u, o = to_dev(torch, w)
     tot = w.units.size
@@ -311,12 +312,42 @@ def test_multi_loopback_vs_oracle(torch, h, oracle_mod, world, name, n):
     if w.coder == UNICODE:
         s_u = s_u.view(np.uint16)
     assert np.array_equal(so.cpu().numpy(), rso) and np.array_equal(s_u, rsu)
-    # shard boundaries never split an equal-code run
-    codes, _ = oracle_mod.encode(w.coder, w.units, w.offsets)
-    sc = codes[ref]
+    # shard boundaries never split equal strings (composite splitters may split
+    # equal-code runs), and the shard sizes are those of the splitter rule
+    # (husky_select_splitters, host copy) applied to the same samples
+    strs = w.strings()
     b = np.cumsum(shards)[:-1]
     b = b[(b > 0) & (b < w.n)]
-    assert not np.any(sc[b] == sc[b - 1])
+    assert not any(strs[ref[i]] == strs[ref[i - 1]] for i in b)
+    assert list(shards) == expected_shards(h, w, world)
+    if name == "C4" and world > 1:  # all codes collide: still balanced (NEXT-1)
+        assert max(shards) <= 2 * w.n / world
+
+
+def expected_shards(h, w, world, s=4096, cap=32):
+    """Shard sizes of the sample sort by its documented rule: rank r holds
+    block [n*r/P, n*(r+1)/P); samples at local positions i*n_r/s, each the
+    string's first <= 32 units; splitters by husky_select_splitters; bucket(x) =
+    number of splitter strings <= x in the sort order."""
+    import bisect
+    n = w.n
+    strs = w.strings()
+    samples = []
+    for r in range(world):
+        lo, hi = n * r // world, n * (r + 1) // world
+        nl = hi - lo
+        if nl == 0:
+            continue
+        samples += [list(strs[lo + i * nl // s][:cap]) for i in range(s)]
+    if world == 1:
+        return [n]
+    sw = W.from_strings(samples, w.coder)
+    idx = h.husky_select_splitters(w.coder, sw.units, sw.offsets, world)
+    spl = [tuple(samples[int(i)]) for i in idx]
+    counts = [0] * world
+    for x in strs:
+        counts[bisect.bisect_right(spl, x)] += 1
+    return counts
 
 
 def test_multi_nccl_single_rank(torch, h, oracle_mod):
