@@ -30,23 +30,41 @@ __device__ __forceinline__ uint8_t decode_byte(uint64_t code, int b) {
 // through the radix as the payload).  Strings whose length is <= PL are then
 // rebuilt from their sorted code (sequential reads only); perm is unpacked in
 // place.  Only longer strings read offsets / units at random.
-template <int CODER, bool PACKED>
-__global__ void __launch_bounds__(kGatherThreads)
+// CHECK (the main gather after the key sort) also does A3 in the same pass:
+// run detection (equal adjacent codes; the k-th run start / end of the array
+// belong to run k, ids from a second single-pass scan whose look-back runs in
+// warp 1 next to the length scan's in warp 0) and the order check of every
+// adjacent equal-code pair on the strings this tile just staged (pairs whose
+// strings are not both in the stage compare the source strings).  A run with an
+// out-of-order pair is marked dirty for the fix-up (A5).
+struct GatherRuns {
+  uint32_t *run_start, *run_end;
+  uint8_t *dirty;
+  unsigned long long *lb;  // look-back words of the run-count scan (one per tile)
+  DevState *st;            // n_runs
+};
+
+template <int CODER, bool PACKED, bool CHECK>
+__global__ void __launch_bounds__(kGatherThreads, 4)
     k_gather(uint32_t *__restrict__ perm, uint64_t n, const void *__restrict__ units,
              const int64_t *__restrict__ offsets, void *__restrict__ sorted_units,
              int64_t *__restrict__ sorted_offsets, unsigned long long *lb, uint32_t *tile_counter,
              uint32_t epoch, const int64_t *base_ptr, int dbg, const uint64_t *__restrict__ codes,
-             const DevState *st) {
-  constexpr int W = CoderTraits<CODER>::kUnitBytes;
-  constexpr uint32_t PL = CoderTraits<CODER>::kPL;
+             const DevState *st, GatherRuns runs) {
+  using T = CoderTraits<CODER>;
+  constexpr int W = T::kUnitBytes;
+  constexpr uint32_t PL = T::kPL;
   extern __shared__ __align__(16) uint8_t stage[];  // kGatherStage + 32 bytes
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_wt[kGatherThreads / 32 + 1];
-  __shared__ unsigned long long s_base;
+  __shared__ unsigned long long s_base, s_rbase;
+  // CHECK: each thread's last item (code, length, index, tile-local unit offset)
+  __shared__ unsigned long long s_lcode[CHECK ? kGatherThreads : 1], s_loff[CHECK ? kGatherThreads : 1];
+  __shared__ uint32_t s_llen[CHECK ? kGatherThreads : 1], s_lidx[CHECK ? kGatherThreads : 1];
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   if (st) {
     if (st->violations & kOffsetsBad) return;  // invalid input: reported by the caller
-    if (PACKED && codes == nullptr) codes = reinterpret_cast<const uint64_t *>(st->sorted_keys);
+    if ((PACKED || CHECK) && codes == nullptr) codes = reinterpret_cast<const uint64_t *>(st->sorted_keys);
   }
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   // re-gather of a span: output positions start at *base_ptr (unchanged by us)
@@ -59,14 +77,16 @@ __global__ void __launch_bounds__(kGatherThreads)
   // from their code, the code itself (bit j of `dec`)
   uint32_t raw[kGatherItems];
 #pragma unroll
-  for (int j = 0; j < kGatherItems; ++j) raw[j] = p0 + j < n ? perm[p0 + j] : 0xFFFFFFFFu;
-  uint64_t sv[kGatherItems];
-  uint32_t len[kGatherItems];
+  for (int j = 0; j < kGatherItems; ++j) raw[j] = p0 + j < n ? perm[p0 + j] : 0u;
+  uint64_t sv[kGatherItems], cc[kGatherItems];
+  uint32_t len[kGatherItems], ix[kGatherItems];
   uint32_t dec = 0;
   unsigned long long mine = 0;
 #pragma unroll
   for (int j = 0; j < kGatherItems; ++j) {
-    if (raw[j] == 0xFFFFFFFFu) {
+    cc[j] = 0;
+    ix[j] = 0;
+    if (p0 + j >= n) {
       sv[j] = 0;
       len[j] = 0;
     } else {
@@ -76,10 +96,12 @@ __global__ void __launch_bounds__(kGatherThreads)
         idx &= 0x0FFFFFFFu;
         perm[p0 + j] = idx;
       }
+      ix[j] = idx;
+      if (CHECK) cc[j] = __ldg(codes + p0 + j);
       if (PACKED && lc <= PL) {
         dec |= 1u << j;
         len[j] = lc;
-        sv[j] = __ldg(codes + p0 + j);
+        sv[j] = CHECK ? cc[j] : __ldg(codes + p0 + j);
       } else {
         int64_t a = __ldg(offsets + idx), b = __ldg(offsets + idx + 1);
         sv[j] = (uint64_t)a;
@@ -88,9 +110,38 @@ __global__ void __launch_bounds__(kGatherThreads)
     }
     mine += len[j];
   }
+  // CHECK: run flags.  eqp bit j: position p0+j equals its predecessor; eqn:
+  // equals its successor (neighbours across lanes by shuffles, across warps and
+  // tiles from global memory)
+  uint32_t eqp = 0, eqn = 0, nstart = 0;
+  if (CHECK) {
+    unsigned long long prevc = __shfl_up_sync(0xFFFFFFFFu, cc[kGatherItems - 1], 1);
+    unsigned long long nextc = __shfl_down_sync(0xFFFFFFFFu, cc[0], 1);
+    if (lane == 0) prevc = p0 > 0 && p0 - 1 < n ? __ldg(codes + p0 - 1) : 0ull;
+    if (lane == 31) nextc = p0 + kGatherItems < n ? __ldg(codes + p0 + kGatherItems) : 0ull;
+#pragma unroll
+    for (int j = 0; j < kGatherItems; ++j) {
+      const uint64_t p = p0 + j;
+      const unsigned long long pc = j == 0 ? prevc : cc[j - 1];
+      const unsigned long long nc = j == kGatherItems - 1 ? nextc : cc[j + 1];
+      const bool ep = p < n && p > 0 && cc[j] == pc;
+      const bool en = p + 1 < n && cc[j] == nc;
+      eqp |= (uint32_t)ep << j;
+      eqn |= (uint32_t)en << j;
+      nstart += (!ep && en);
+    }
+  }
+  // one scan for both: units in the low 48 bits, run starts above
   unsigned long long tile_total;
-  unsigned long long excl_t = block_exclusive_scan<unsigned long long, kGatherThreads>(mine, &tile_total, s_wt);
-  if (tid == 0) st_relaxed_u64(lb + tile, make_flag(tile == 0 ? kFlagInc : kFlagAgg, epoch, tile_total));
+  unsigned long long excl_t = block_exclusive_scan<unsigned long long, kGatherThreads>(
+      mine | ((unsigned long long)nstart << 48), &tile_total, s_wt);
+  const uint32_t excl_r = (uint32_t)(excl_t >> 48), tile_runs = (uint32_t)(tile_total >> 48);
+  excl_t &= (1ull << 48) - 1;
+  tile_total &= (1ull << 48) - 1;
+  if (tid == 0) {
+    st_relaxed_u64(lb + tile, make_flag(tile == 0 ? kFlagInc : kFlagAgg, epoch, tile_total));
+    if (CHECK) st_relaxed_u64(runs.lb + tile, make_flag(tile == 0 ? kFlagInc : kFlagAgg, epoch, tile_runs));
+  }
 
   const uint8_t *ub = (const uint8_t *)units;
   uint8_t *ob = (uint8_t *)sorted_units;
@@ -147,6 +198,12 @@ __global__ void __launch_bounds__(kGatherThreads)
   const uint64_t first_w1 = tile_bytes < (uint64_t)kGatherStage ? tile_bytes : (uint64_t)kGatherStage;
   if (sorted_units && !direct) stage_window(0, first_w1);  // overlaps the look-back
 
+  if (CHECK) {
+    s_lcode[tid] = cc[kGatherItems - 1];
+    s_llen[tid] = len[kGatherItems - 1];
+    s_lidx[tid] = ix[kGatherItems - 1];
+    s_loff[tid] = excl_t + mine - len[kGatherItems - 1];
+  }
   if (warp == 0) {
     unsigned long long ex =
         tile == 0 ? 0ull : ((dbg & 2) ? lookback(lb, tile, 1, epoch) : warp_lookback(lb, tile, epoch));
@@ -154,6 +211,13 @@ __global__ void __launch_bounds__(kGatherThreads)
       if (tile != 0) st_relaxed_u64(lb + tile, make_flag(kFlagInc, epoch, ex + tile_total));
       s_base = ex;
       if ((uint64_t)(tile + 1) * kGatherTile >= n) sorted_offsets[n] = (int64_t)(gbase + ex + tile_total);
+    }
+  } else if (CHECK && warp == 1) {  // the run-count scan's look-back, next to warp 0's
+    unsigned long long ex = tile == 0 ? 0ull : warp_lookback(runs.lb, tile, epoch);
+    if (lane == 0) {
+      if (tile != 0) st_relaxed_u64(runs.lb + tile, make_flag(kFlagInc, epoch, ex + tile_runs));
+      s_rbase = ex;
+      if ((uint64_t)(tile + 1) * kGatherTile >= n) runs.st->n_runs = (uint32_t)(ex + tile_runs);
     }
   }
   __syncthreads();
@@ -164,6 +228,63 @@ __global__ void __launch_bounds__(kGatherThreads)
     for (int j = 0; j < kGatherItems; ++j) {
       if (p0 + j < n) sorted_offsets[p0 + j] = (int64_t)d;
       d += len[j];
+    }
+  }
+  if (CHECK) {
+    // adjacent pairs (p-1, p) with equal codes, p = my items
+    const uint64_t win_units = first_w1 / W;  // units [0, win_units) of the tile are staged
+    unsigned long long pc, po;
+    uint32_t pl, pi;
+    if (tid > 0) {
+      pc = s_lcode[tid - 1]; pl = s_llen[tid - 1]; pi = s_lidx[tid - 1]; po = s_loff[tid - 1];
+    } else if (p0 > 0) {  // the previous tile's last string: from the source
+      pc = __ldg(codes + p0 - 1);
+      pi = perm[p0 - 1] & (PACKED ? 0x0FFFFFFFu : 0xFFFFFFFFu);  // unpacked or not yet
+      pl = (uint32_t)(__ldg(offsets + pi + 1) - __ldg(offsets + pi));
+      po = ~0ull;  // not staged
+    } else {
+      pc = ~cc[0]; pl = 0; pi = 0; po = ~0ull;  // position 0: no pair
+    }
+    unsigned long long d = excl_t;
+    uint32_t bad = 0;
+#pragma unroll
+    for (int j = 0; j < kGatherItems; ++j) {
+      if ((eqp >> j) & 1) {
+        int c;
+        if (pl <= PL || len[j] <= PL) {
+          c = pl < len[j] ? -1 : (pl > len[j] ? 1 : 0);  // short rule (R6)
+        } else if (sorted_units && !direct && po != ~0ull && po + pl <= win_units && d + len[j] <= win_units) {
+          c = 0;  // both staged: compare units [S, min) in shared memory
+          const uint32_t m = pl < len[j] ? pl : len[j];
+          for (uint32_t k = T::kS; k < m && c == 0; ++k) {
+            uint32_t a, b;
+            if (W == 1) { a = stage[po + k]; b = stage[d + k]; }
+            else {
+              a = stage[2 * (po + k)] | (uint32_t)stage[2 * (po + k) + 1] << 8;
+              b = stage[2 * (d + k)] | (uint32_t)stage[2 * (d + k) + 1] << 8;
+            }
+            if (a != b) c = a < b ? -1 : 1;
+          }
+          if (c == 0) c = pl < len[j] ? -1 : (pl > len[j] ? 1 : 0);
+        } else {
+          c = cmp_units_from<CODER>(units, __ldg(offsets + pi), pl, __ldg(offsets + ix[j]), len[j], T::kS);
+        }
+        if (c > 0 || (c == 0 && pi > ix[j])) bad |= 1u << j;
+      }
+      pc = cc[j]; pl = len[j]; pi = ix[j]; po = d;
+      d += len[j];
+    }
+    // runs: the k-th start and the k-th end of the array belong to run k
+    if (eqp | eqn) {
+      uint32_t rid = (uint32_t)s_rbase + excl_r - 1;
+#pragma unroll
+      for (int j = 0; j < kGatherItems; ++j) {
+        const bool ep = (eqp >> j) & 1, en = (eqn >> j) & 1;
+        const uint32_t p = (uint32_t)(p0 + j);
+        if (!ep && en) runs.run_start[++rid] = p;
+        if (ep && !en) runs.run_end[rid] = p;
+        if ((bad >> j) & 1) runs.dirty[rid] = 1;
+      }
     }
   }
   if (sorted_units == nullptr) return;
@@ -202,15 +323,17 @@ __global__ void __launch_bounds__(kGatherThreads)
 void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, const int64_t *offsets,
                    void *sorted_units, int64_t *sorted_offsets, unsigned long long *lb,
                    uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, const int64_t *base_ptr,
-                   bool packed, const uint64_t *packed_codes, const DevState *st) {
+                   bool packed, const uint64_t *packed_codes, const DevState *st, const GatherRunsOut *runs_out) {
   if (n == 0) return;
   constexpr int kSmem = kGatherStage + 32;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_gather<HUSKY_CODER_ASCII, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    cudaFuncSetAttribute(k_gather<HUSKY_CODER_ASCII, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    cudaFuncSetAttribute(k_gather<HUSKY_CODER_UNICODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    cudaFuncSetAttribute(k_gather<HUSKY_CODER_UNICODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+#define G_ATTR(C, P, K) cudaFuncSetAttribute(k_gather<C, P, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem)
+    G_ATTR(HUSKY_CODER_ASCII, true, false); G_ATTR(HUSKY_CODER_ASCII, false, false);
+    G_ATTR(HUSKY_CODER_UNICODE, true, false); G_ATTR(HUSKY_CODER_UNICODE, false, false);
+    G_ATTR(HUSKY_CODER_ASCII, true, true); G_ATTR(HUSKY_CODER_ASCII, false, true);
+    G_ATTR(HUSKY_CODER_UNICODE, true, true); G_ATTR(HUSKY_CODER_UNICODE, false, true);
+#undef G_ATTR
     configured = true;
   }
   Scope sc_(ST_GATHER, s, n);
@@ -220,14 +343,27 @@ void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, con
     const char *v = getenv("HUSKY_DEBUG_GATHER");
     return v ? atoi(v) : 0;
   }();
+  GatherRuns runs{};
+  if (runs_out) runs = GatherRuns{runs_out->run_start, runs_out->run_end, runs_out->dirty, runs_out->lb, runs_out->st};
 #define G_ARGS \
-  perm, n, units, offsets, sorted_units, sorted_offsets, lb, tile_counter, epoch, base_ptr, dbg, packed_codes, st
+  perm, n, units, offsets, sorted_units, sorted_offsets, lb, tile_counter, epoch, base_ptr, dbg, packed_codes, st, runs
+  const bool chk = runs_out != nullptr;
   if (coder == HUSKY_CODER_ASCII) {
-    if (packed) k_gather<HUSKY_CODER_ASCII, true><<<g, b, kSmem, s>>>(G_ARGS);
-    else k_gather<HUSKY_CODER_ASCII, false><<<g, b, kSmem, s>>>(G_ARGS);
+    if (packed) {
+      if (chk) k_gather<HUSKY_CODER_ASCII, true, true><<<g, b, kSmem, s>>>(G_ARGS);
+      else k_gather<HUSKY_CODER_ASCII, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+    } else {
+      if (chk) k_gather<HUSKY_CODER_ASCII, false, true><<<g, b, kSmem, s>>>(G_ARGS);
+      else k_gather<HUSKY_CODER_ASCII, false, false><<<g, b, kSmem, s>>>(G_ARGS);
+    }
   } else {
-    if (packed) k_gather<HUSKY_CODER_UNICODE, true><<<g, b, kSmem, s>>>(G_ARGS);
-    else k_gather<HUSKY_CODER_UNICODE, false><<<g, b, kSmem, s>>>(G_ARGS);
+    if (packed) {
+      if (chk) k_gather<HUSKY_CODER_UNICODE, true, true><<<g, b, kSmem, s>>>(G_ARGS);
+      else k_gather<HUSKY_CODER_UNICODE, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+    } else {
+      if (chk) k_gather<HUSKY_CODER_UNICODE, false, true><<<g, b, kSmem, s>>>(G_ARGS);
+      else k_gather<HUSKY_CODER_UNICODE, false, false><<<g, b, kSmem, s>>>(G_ARGS);
+    }
   }
 #undef G_ARGS
 }

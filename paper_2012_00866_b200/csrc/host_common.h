@@ -68,10 +68,12 @@ struct Sorter {
   uint64_t *keysB() const { return at<uint64_t>(L.keysB); }
   unsigned long long *lb_radix() const { return at<unsigned long long>(L.lb_radix); }
   unsigned long long *lb_scan() const { return at<unsigned long long>(L.lb_scan); }
+  // second scan-look-back array (the run-count scan fused into the gather)
+  unsigned long long *lb_scan2() const { return at<unsigned long long>(L.lb_scan) + L.tiles_s; }
 
   cudaError_t reset_lookback() {
     cudaError_t e = cudaMemsetAsync(ws + L.lb_radix, 0, L.lb_radix_words * 8, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ws + L.lb_scan, 0, L.tiles_s * 8, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ws + L.lb_scan, 0, L.tiles_s * 16, s);
     return e;
   }
   // next look-back epoch (1..255); wraps by clearing the flag arrays

@@ -79,7 +79,7 @@ Layout make_layout(uint64_t n) {
     L.lb_radix_words = w > wm ? w : wm;
   }
   L.lb_radix = take(L.lb_radix_words * 8);
-  L.lb_scan = take(L.tiles_s * 8);
+  L.lb_scan = take(L.tiles_s * 16);  // two look-back arrays (lengths, run counts)
   L.run_start = take(L.cap_sm * 4);
   L.run_end = take(L.cap_sm * 4);
   L.dirty = take(L.cap_sm);
@@ -248,18 +248,24 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // check below then reads every run's strings contiguously instead of through
   // a second random perm -> offsets -> units walk; only spans the fix-up
   // reorders are gathered again (rare outside all-colliding inputs).
-  if (d_sorted_units)
+  // A3 is fused into this gather: run detection and the order check of every
+  // adjacent equal-code pair on the strings it stages (perm-only mode runs the
+  // separate run scan below instead).
+  uint32_t *run_start = S.at<uint32_t>(L.run_start), *run_end = S.at<uint32_t>(L.run_end);
+  uint8_t *dirty = S.at<uint8_t>(L.dirty);
+  HCHECK(cudaMemsetAsync(dirty, 0, L.cap_sm, s));
+  if (d_sorted_units) {
+    GatherRunsOut ro{run_start, run_end, dirty, S.lb_scan2(), st};
     launch_gather(kc, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),
-                  S.next_counter(), S.next_epoch(), s, nullptr, packed, nullptr, st);
+                  S.next_counter(), S.next_epoch(), s, nullptr, packed, nullptr, st, &ro);
+  }
   debug_check_perm(d_perm, n, "key sort", s);
 
   // ---- A3 run detection + order check (keys: DevState::sorted_keys), classification
-  uint32_t *run_start = S.at<uint32_t>(L.run_start), *run_end = S.at<uint32_t>(L.run_end);
-  uint8_t *dirty = S.at<uint8_t>(L.dirty);
   uint2 *list_sm = S.at<uint2>(L.list_sm), *list_g = S.at<uint2>(L.list_g);
-  HCHECK(cudaMemsetAsync(dirty, 0, L.cap_sm, s));
-  launch_runs_scan(kc, 0, nullptr, n, d_perm, d_units, d_offsets, 0, run_start, run_end, dirty, st,
-                   S.lb_scan(), S.next_counter(), S.next_epoch(), s, d_sorted_units, d_sorted_offsets);
+  if (!d_sorted_units)
+    launch_runs_scan(kc, 0, nullptr, n, d_perm, d_units, d_offsets, 0, run_start, run_end, dirty, st,
+                     S.lb_scan(), S.next_counter(), S.next_epoch(), s);
   launch_runs_classify(run_start, run_end, dirty, st, list_sm, L.cap_sm, list_g, true, S.sms, s);
 
   // ---- A5 fix-up of small / medium dirty runs (counts read on device), then

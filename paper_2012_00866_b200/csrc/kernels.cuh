@@ -132,7 +132,16 @@ inline uint64_t gather_tiles(uint64_t n) { return (n + kGatherTile - 1) / kGathe
 void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, const int64_t *offsets,
                    void *sorted_units, int64_t *sorted_offsets, unsigned long long *lb,
                    uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, const int64_t *base_ptr = nullptr,
-                   bool packed = false, const uint64_t *packed_codes = nullptr, const DevState *st = nullptr);
+                   bool packed = false, const uint64_t *packed_codes = nullptr, const DevState *st = nullptr,
+                   const struct GatherRunsOut *runs_out = nullptr);
+// A3 fused into the main gather (runs_out != NULL): run starts / ends / dirty
+// flags as k_runs_scan writes them, DevState::n_runs; lb: gather_tiles(n) words
+struct GatherRunsOut {
+  uint32_t *run_start, *run_end;
+  uint8_t *dirty;
+  unsigned long long *lb;
+  DevState *st;
+};
 void launch_unpack_perm(uint32_t *perm, uint64_t n, cudaStream_t s);
 void launch_regather_runs(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                           const uint32_t *perm, const void *units, const int64_t *offsets,

@@ -267,7 +267,7 @@ static MultiLayout make_multi_layout(int coder, uint64_t n, uint64_t units, int 
   L.vals = take(n * 4 + 4);
   L.lb_radix_words = radix_lb_words(n);
   L.lb_radix = take(L.lb_radix_words * 8);
-  L.lb_scan = take(L.tiles_s * 8 + 8);
+  L.lb_scan = take(L.tiles_s * 16 + 8);  // Sorter::reset_lookback clears two arrays
   M.send_perm = take(n * 4 + 4);
   M.samples = take((size_t)world * kSampleStride * 8);
   M.splitters = take((size_t)world * sizeof(SampleRec));
