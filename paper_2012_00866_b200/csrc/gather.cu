@@ -45,7 +45,7 @@ struct GatherRuns {
 };
 
 template <int CODER, bool PACKED, bool CHECK>
-__global__ void __launch_bounds__(kGatherThreads, 4)
+__global__ void __launch_bounds__(kGatherThreads, 1024 / kGatherThreads)
     k_gather(uint32_t *__restrict__ perm, uint64_t n, const void *__restrict__ units,
              const int64_t *__restrict__ offsets, void *__restrict__ sorted_units,
              int64_t *__restrict__ sorted_offsets, unsigned long long *lb, uint32_t *tile_counter,
