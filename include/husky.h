@@ -158,6 +158,24 @@ husky_status husky_sort_host(int coder, const void *h_units, const int64_t *h_of
                              uint32_t *h_perm, void *h_sorted_units, int64_t *h_sorted_offsets,
                              void *d_ws, size_t ws_bytes, husky_outcome *h_out, void *stream);
 
+/* Many independent sorts on HOST buffers, pipelined: `depth` worker threads,
+ * each with its own stream and workspace slice, run batches b = w, w + depth,
+ * ... exactly as husky_sort_host does, so one batch's host->device copy, another's
+ * kernels and a third's device->host copy overlap (PCIe is full duplex; the
+ * copy engines are independent of the SMs).  Batch b: h_units[b],
+ * h_offsets[b] (n[b] + 1 entries), outputs h_perm[b] and, if non-NULL,
+ * h_sorted_units[b] / h_sorted_offsets[b] (pass NULL arrays for perm-only).
+ * Distinct batches must not share output buffers.  d_ws must hold
+ * husky_sort_host_many_workspace(coder, n_max, units_max, depth) bytes, where
+ * n_max / units_max bound every batch.  h_out (nullable) receives k outcomes.
+ * Returns after every batch has finished; the first failing batch's status. */
+husky_status husky_sort_host_many_workspace(int coder, uint64_t n_max, uint64_t units_max, int depth,
+                                            size_t *bytes);
+husky_status husky_sort_host_many(int coder, int k, const void *const *h_units, const int64_t *const *h_offsets,
+                                  const uint64_t *n, uint32_t *const *h_perm, void *const *h_sorted_units,
+                                  int64_t *const *h_sorted_offsets, int depth, void *d_ws, size_t ws_bytes,
+                                  husky_outcome *h_out);
+
 /* ------------------------------------------------------------------ multi-GPU
  * Sample sort over P ranks (one process per GPU).  Input is block-distributed
  * by global index: rank r holds strings [global_base_r, global_base_r + n_local)

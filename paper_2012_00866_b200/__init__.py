@@ -84,6 +84,8 @@ _sig("husky_sort_host", _ST, _I, _P, _P, _U64, _P, _P, _P, _P, _SZ, ctypes.POINT
 _sig("husky_last_error", ctypes.c_char_p)
 _sig("husky_sort_keys_workspace", _ST, _I, _U64, ctypes.POINTER(_SZ))
 _sig("husky_sort_keys", _ST, _I, _P, _U64, _P, _P, _P, _SZ, _P)
+_sig("husky_sort_host_many_workspace", _ST, _I, _U64, _U64, _I, ctypes.POINTER(_SZ))
+_sig("husky_sort_host_many", _ST, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _SZ, ctypes.POINTER(husky_outcome))
 
 EXPORTED = ["husky_unit_bytes", "husky_encode", "husky_sort_workspace", "husky_sort",
             "husky_sort_host_workspace", "husky_sort_host", "husky_comm_unique_id",
@@ -93,7 +95,7 @@ EXPORTED = ["husky_unit_bytes", "husky_encode", "husky_sort_workspace", "husky_s
             "husky_sort_multi_loopback", "husky_select_splitters", "husky_last_error",
             "husky_profile_enable", "husky_profile_reset", "husky_profile_read",
             "husky_profile_stage_name", "husky_launch_count", "husky_sort_keys_workspace",
-            "husky_sort_keys"]
+            "husky_sort_keys", "husky_sort_host_many_workspace", "husky_sort_host_many"]
 
 _sig("husky_profile_enable", None, _I)
 _sig("husky_profile_reset", None)
@@ -242,6 +244,34 @@ def husky_sort_keys(key_type, keys, perm, sorted_keys=None, ws=None, stream=None
     _check(_lib.husky_sort_keys(key_type, _ptr(keys), n, _ptr(perm), _ptr(sorted_keys), _ptr(ws),
                                 ws.numel() * ws.element_size(), _stream(stream)), "husky_sort_keys")
     return perm
+
+
+def husky_sort_host_many_workspace(coder, n_max, units_max, depth=2) -> int:
+    b = _SZ(0)
+    _check(_lib.husky_sort_host_many_workspace(coder, n_max, units_max, depth, ctypes.byref(b)),
+           "husky_sort_host_many_workspace")
+    return int(b.value)
+
+
+def husky_sort_host_many(coder, batches, ws, depth=2):
+    """Pipelined husky_sort_host over many batches.  batches: list of
+    (h_units, h_offsets, h_perm, h_sorted_units | None, h_sorted_offsets | None)
+    host arrays (numpy or pinned CPU tensors).  -> list of outcome dicts."""
+    k = len(batches)
+    arr = lambda vals: (ctypes.c_void_p * max(k, 1))(*vals)
+    def n_of(o):
+        return (o.size if isinstance(o, np.ndarray) else o.numel()) - 1
+    units = arr([_ptr(b[0]) for b in batches])
+    offs = arr([_ptr(b[1]) for b in batches])
+    ns = (ctypes.c_uint64 * max(k, 1))(*[n_of(b[1]) for b in batches])
+    perms = arr([_ptr(b[2]) for b in batches])
+    with_units = k > 0 and batches[0][3] is not None
+    su = arr([_ptr(b[3]) for b in batches]) if with_units else None
+    so = arr([_ptr(b[4]) for b in batches]) if with_units else None
+    outs = (husky_outcome * max(k, 1))()
+    _check(_lib.husky_sort_host_many(coder, k, units, offs, ns, perms, su, so, depth, _ptr(ws),
+                                     ws.numel() * ws.element_size(), outs), "husky_sort_host_many")
+    return [outs[i].as_dict() for i in range(k)]
 
 
 from .multi import (husky_comm_create, husky_comm_destroy, husky_comm_unique_id,  # noqa: E402

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -568,6 +569,65 @@ husky_status husky_sort_host(int coder, const void *h_units, const int64_t *h_of
     HCHECK(cudaMemcpyAsync(h_sorted_offsets, ws + o_so, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
   }
   HCHECK(cudaStreamSynchronize(s));
+  return HUSKY_OK;
+}
+
+husky_status husky_sort_host_many_workspace(int coder, uint64_t n_max, uint64_t units_max, int depth,
+                                            size_t *bytes) {
+  if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  if (!bytes || depth < 1 || depth > 16) return fail(HUSKY_ERR_INVALID_ARG, "bad arguments");
+  size_t a, b, c, d, e, f;
+  *bytes = (size_t)depth * align_up(host_layout(coder, n_max, units_max, &a, &b, &c, &d, &e, &f), 256);
+  return HUSKY_OK;
+}
+
+husky_status husky_sort_host_many(int coder, int k, const void *const *h_units, const int64_t *const *h_offsets,
+                                  const uint64_t *n, uint32_t *const *h_perm, void *const *h_sorted_units,
+                                  int64_t *const *h_sorted_offsets, int depth, void *d_ws, size_t ws_bytes,
+                                  husky_outcome *h_out) {
+  if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
+  if (k < 0 || depth < 1 || depth > 16 || (k && (!h_units || !h_offsets || !n || !h_perm)) || !d_ws)
+    return fail(HUSKY_ERR_INVALID_ARG, "bad arguments");
+  if ((uintptr_t)d_ws % 256) return fail(HUSKY_ERR_INVALID_ARG, "workspace not 256-byte aligned");
+  uint64_t n_max = 0, u_max = 0;
+  for (int b = 0; b < k; ++b) {
+    if (!h_offsets[b]) return fail(HUSKY_ERR_INVALID_ARG, "batch %d: null offsets", b);
+    n_max = std::max<uint64_t>(n_max, n[b]);
+    if (n[b]) u_max = std::max<uint64_t>(u_max, (uint64_t)(h_offsets[b][n[b]] - h_offsets[b][0]));
+  }
+  size_t a, bb, c, d, e, f;
+  const size_t slice = align_up(host_layout(coder, n_max, u_max, &a, &bb, &c, &d, &e, &f), 256);
+  if (ws_bytes < slice * depth) return fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, slice * depth);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<husky_status> st(depth, HUSKY_OK);
+  std::vector<std::string> err(depth);
+  std::vector<std::thread> workers;
+  for (int w = 0; w < depth && w < k; ++w) {
+    workers.emplace_back([&, w]() {
+      cudaSetDevice(dev);
+      cudaStream_t s;
+      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+        st[w] = fail(HUSKY_ERR_CUDA, "stream creation failed");
+        err[w] = g_last_error;
+        return;
+      }
+      for (int b = w; b < k && st[w] == HUSKY_OK; b += depth) {
+        st[w] = husky_sort_host(coder, h_units[b], h_offsets[b], n[b], h_perm[b],
+                                h_sorted_units ? h_sorted_units[b] : nullptr,
+                                h_sorted_offsets ? h_sorted_offsets[b] : nullptr, (uint8_t *)d_ws + slice * w, slice,
+                                h_out ? h_out + b : nullptr, s);
+        if (st[w] != HUSKY_OK) err[w] = g_last_error;
+      }
+      cudaStreamDestroy(s);
+    });
+  }
+  for (auto &t : workers) t.join();
+  for (int w = 0; w < depth; ++w)
+    if (st[w] != HUSKY_OK) {
+      g_last_error = err[w];
+      return st[w];
+    }
   return HUSKY_OK;
 }
 

@@ -363,3 +363,30 @@ def test_multi_nccl_single_rank(torch, h, oracle_mod):
         assert np.array_equal(perm.cpu().numpy().view(np.uint32), ref)
     finally:
         h.husky_comm_destroy(comm)
+
+
+def test_sort_host_many_pipelined(torch, h, oracle_mod):
+    """The pipelined host API: several batches (different configs and sizes,
+    one empty) on 2 and 3 workers, each bit-exact against the oracle."""
+    wls = [W.make("C1", 50_000), W.make("C3", 70_000), W.make("C2", 120_000),
+           W.from_strings([], ASCII), W.make("C1", 3)]
+    for depth in (2, 3):
+        for coder in (ASCII, UNICODE):
+            sel = [w for w in wls if w.coder == coder]
+            batches = []
+            for w in sel:
+                tot = int(w.offsets[-1] - w.offsets[0]) if w.n else 0
+                batches.append((w.units if w.units.size else np.zeros(1, w.units.dtype), w.offsets,
+                                np.zeros(max(w.n, 1), np.uint32), np.zeros(tot + 8, w.units.dtype),
+                                np.zeros(w.n + 1, np.int64)))
+            n_max = max(w.n for w in sel)
+            u_max = max(int(w.offsets[-1] - w.offsets[0]) if w.n else 0 for w in sel)
+            ws = torch.empty(h.husky_sort_host_many_workspace(coder, n_max, u_max, depth), dtype=torch.uint8,
+                             device="cuda")
+            h.husky_sort_host_many(coder, batches, ws, depth)
+            for w, b in zip(sel, batches):
+                ref = oracle_mod.sort(w.coder, w.units, w.offsets)
+                assert np.array_equal(b[2][:w.n], ref)
+                rsu, rso = oracle_mod.gather(w.coder, w.units, w.offsets, ref)
+                assert np.array_equal(b[4], rso)
+                assert np.array_equal(b[3][:rsu.size], rsu)
