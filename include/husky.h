@@ -44,10 +44,9 @@ typedef enum {
   HUSKY_OK = 0,
   HUSKY_ERR_INVALID_ARG = 1, /* null required pointer, unknown coder, n >= 2^32,
                                 non-monotone offsets, workspace misaligned      */
-  HUSKY_ERR_DOMAIN = 2,      /* husky_sort saw a unit outside the coder's domain in
-                                a code prefix (ASCII: > 0x7F; ENGLISH5/6: see the
-                                coder): Alg. 4's mask breaks
-                                monotonicity there (readings R5, R15) */
+  HUSKY_ERR_DOMAIN = 2,      /* reserved (no call returns it any more: input outside
+                                a coder's domain is sorted by the general cleanup,
+                                see husky_sort)                                 */
   HUSKY_ERR_CUDA = 3,        /* a CUDA runtime call failed                       */
   HUSKY_ERR_NCCL = 4,        /* an NCCL call failed (multi-GPU only)             */
   HUSKY_ERR_WORKSPACE = 5,   /* workspace smaller than the query returned        */
@@ -59,13 +58,14 @@ typedef enum {
   HUSKY_CODER_UNICODE = 1, /* unicodeToLong: stringToLong(s, 4, 16, 0xFFFF)>>>1 PAPER.md:463-465, 487-490 */
   HUSKY_CODER_ENGLISH5 = 2,/* "5-bit ASCII ... 12 (or fewer) characters":
                               stringToLong(s, 12, 5, 0x1F), uint8 units (reading R15).
-                              husky_sort domain: every unit inside the 12-unit code
-                              window is a lowercase letter, or every one is an
-                              uppercase letter (case folding is monotone only then) */
+                              Domain: every unit inside the 12-unit code window is a
+                              lowercase letter, or every one is uppercase (case
+                              folding is monotone only then); off-domain input is
+                              sorted by the general cleanup                        */
   HUSKY_CODER_ENGLISH6 = 3 /* "case-dependent strings (6-bit ASCII) ... 10 characters"
                               (PAPER.md:219): stringToLong(s, 10, 6, 0x3F), uint8 units.
-                              husky_sort domain: units inside the 10-unit window are
-                              letters A-Z / a-z (reading R15)                        */
+                              Domain: units inside the 10-unit window are letters A-Z /
+                              a-z (reading R15); else the general cleanup          */
 } husky_coder;
 
 /* Mirrors SortOutcome (a reading of Alg. 1's `coding.perfect`, plus
@@ -121,9 +121,12 @@ husky_status husky_sort_workspace(int coder, uint64_t n, uint64_t total_units, s
  *   h_out              (nullable) outcome statistics
  * Synchronizes `stream` before returning.  n in {0, 1} returns HUSKY_OK at once
  * (d_perm = {0} for n = 1; sorted outputs copied).
- * Errors: INVALID_ARG, DOMAIN (a unit outside the coder's domain inside the
- * code window of a string -- ASCII: > 0x7F in the first 9 units; ENGLISH5/6:
- * see husky_coder; outputs are then unspecified), WORKSPACE, CUDA. */
+ * Input outside the coder's domain (a unit inside a code window that Alg. 4's
+ * mask makes non-monotone -- ASCII: > 0x7F; ENGLISH5/6: see husky_coder) is
+ * sorted exactly by the general cleanup (NEXT-4: the whole array refined as
+ * one segment from unit 0, an MSD string radix over 7-unit windows;
+ * h_out->domain_ok = 0 and refine_rounds > 0 report it).
+ * Errors: INVALID_ARG, WORKSPACE, CUDA. */
 husky_status husky_sort(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
                         uint32_t *d_perm, void *d_sorted_units, int64_t *d_sorted_offsets,
                         void *d_ws, size_t ws_bytes, husky_outcome *h_out, void *stream);

@@ -32,9 +32,13 @@ __global__ void __launch_bounds__(256)
     const uint32_t start = ent.x, len = ent.y;
     uint32_t my = lane < len ? perm[start + lane] : 0xFFFFFFFFu;
     uint32_t rank = 0;
+    const bool general = st->general != 0;
     for (uint32_t j = 0; j < len; ++j) {
       uint32_t other = __shfl_sync(0xFFFFFFFFu, my, j);
-      if (lane < len && j != lane && cmp_equal_code<CODER>(units, offsets, other, my, T::kS) < 0) ++rank;
+      if (lane < len && j != lane &&
+          (general ? cmp_general<CODER>(units, offsets, other, my)
+                   : cmp_equal_code<CODER>(units, offsets, other, my, T::kS)) < 0)
+        ++rank;
     }
     __syncwarp();
     if (lane < len) perm[start + rank] = my;
@@ -50,6 +54,7 @@ __global__ void __launch_bounds__(1024)
   __shared__ uint32_t s[kMediumMax];
   if (st->violations & kOffsetsBad) return;
   const uint32_t nmed = st->n_medium;
+  const bool general = st->general != 0;
   for (uint32_t e = first + blockIdx.x; e < nmed; e += gridDim.x) {
     uint2 ent = list[cap - 1 - e];
     const uint32_t start = ent.x, len = ent.y;
@@ -70,7 +75,8 @@ __global__ void __launch_bounds__(1024)
             bool gt;  // a > b ?  (0xFFFFFFFF = +infinity padding)
             if (a == 0xFFFFFFFFu) gt = b != 0xFFFFFFFFu;
             else if (b == 0xFFFFFFFFu) gt = false;
-            else gt = cmp_equal_code<CODER>(units, offsets, a, b, T::kS) > 0;
+            else gt = (general ? cmp_general<CODER>(units, offsets, a, b)
+                               : cmp_equal_code<CODER>(units, offsets, a, b, T::kS)) > 0;
             bool asc = (i & k) == 0;
             if (gt == asc) { s[i] = b; s[ixj] = a; }
           }
@@ -125,7 +131,7 @@ __global__ void __launch_bounds__(256)
        e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t i = perm_seg[e];
     int64_t o = offsets[i], l = offsets[i + 1] - o;
-    if (l <= T::kPL) has_short = 1;
+    if (l <= T::kPL && !st->general) has_short = 1;  // short rule: equal codes only (R6)
     int64_t m = l < l0 ? l : l0;
     int64_t lim = (int64_t)from + kLcpCap;
     if (m > lim) m = lim;

@@ -146,7 +146,7 @@ static husky_status cuda_check(const char *where) {
   } while (0)
 
 static husky_status refine_giants(Sorter &S, const DevState &hs0, void *d_sorted_units, int64_t *d_sorted_offsets,
-                                  DevState *out);
+                                  DevState *out, bool general);
 
 husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
                        uint32_t *d_perm, void *d_sorted_units, int64_t *d_sorted_offsets, void *d_ws,
@@ -283,16 +283,22 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   HCHECK(cudaStreamSynchronize(s));
   if (husky_status e = cuda_check("sort")) return e;
   if (hs.violations & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing");
-  if (domain_violation(coder, hs.violations))
-    return fail(HUSKY_ERR_DOMAIN, "coder %d: a unit outside the coder's domain inside a code window (Alg. 4's mask "
-                "is not monotone there; readings R5, R15)", coder);
   if (!use_msd) S.radix_passes = hs.np;
   debug_check_perm(d_perm, n, "fix-up", s);
 
+  // ---- Off-domain input (a unit the coder masks inside a code window: the
+  // code is not monotone there, readings R5 / R15): the general cleanup
+  // (NEXT-4) -- Alg. 1's "cleanup repairs everything" restored by refining the
+  // WHOLE array as one segment from unit 0 (an exact MSD string radix over
+  // 7-unit windows, A6's machinery with whole-string comparisons).  Equal
+  // strings have equal codes, so the stable code sort left them in index order.
+  const bool general = domain_violation(coder, hs.violations);
+  if (general) HCHECK(cudaMemsetAsync(&st->general, 1, 1, s));
+
   // ---- A6 giant-run refinement (rare: runs > 4096 strings with an inversion)
   const uint32_t n_giant = hs.n_giant;
-  if (n_giant) {
-    if (husky_status e = refine_giants(S, hs, d_sorted_units, d_sorted_offsets, &hs)) return e;
+  if (n_giant || general) {
+    if (husky_status e = refine_giants(S, hs, d_sorted_units, d_sorted_offsets, &hs, general)) return e;
   }
   if (h_out) {
     h_out->perfect = !(hs.violations & kNotPerfect);
@@ -314,7 +320,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
 // lists, and re-gather the affected spans.  hs: DevState after the main pass;
 // *out: DevState at the end.
 static husky_status refine_giants(Sorter &S, const DevState &hs0, void *d_sorted_units, int64_t *d_sorted_offsets,
-                                  DevState *out) {
+                                  DevState *out, bool general) {
   const int coder = S.coder;
   const Layout &L = S.L;
   DevState *st = S.st;
@@ -334,7 +340,10 @@ static husky_status refine_giants(Sorter &S, const DevState &hs0, void *d_sorted
   struct Seg { uint32_t start, len, from; };
   std::vector<Seg> queue;
   std::vector<uint2> giant_spans;  // top-level giant runs: re-gathered at the end
-  {
+  if (general) {  // the whole array, nothing known in common
+    queue.push_back({0u, (uint32_t)n, 0u});
+    giant_spans.push_back(make_uint2(0u, (uint32_t)n));
+  } else {
     std::vector<uint2> g(n_giant);
     HCHECK(cudaMemcpy(g.data(), list_g, n_giant * sizeof(uint2), cudaMemcpyDeviceToHost));
     for (auto &x : g) queue.push_back({x.x, x.y, (uint32_t)(coder == HUSKY_CODER_ASCII ? 9 : 3)});

@@ -82,6 +82,10 @@ struct DevState {
   uint32_t msd_count[2], msd_tiles[2];
   uint32_t msd_all_equal, msd_pad;
   unsigned long long msd_keys_part, msd_keys_local;
+  // general cleanup (NEXT-4): the coder is not monotone on this input, so the
+  // refinement / fix-up kernels compare whole strings from unit 0 instead of
+  // relying on equal codes (no short rule, no known-equal prefix)
+  uint32_t general;
   uint32_t pad[16];
 };
 
@@ -364,6 +368,17 @@ __device__ __forceinline__ int cmp_equal_code_ol(const void *units, int64_t oa, 
   int c;
   if (la <= T::kPL || lb <= T::kPL) c = (la < lb) ? -1 : (la > lb ? 1 : 0);
   else c = cmp_units_from<CODER>(units, oa, la, ob, lb, from);
+  if (c) return c;
+  return ia < ib ? -1 : (ia > ib ? 1 : 0);
+}
+
+// Exact comparator with no assumption on the codes (general cleanup, NEXT-4):
+// units from 0, a proper prefix first, then the index.
+template <int CODER>
+__device__ __forceinline__ int cmp_general(const void *units, const int64_t *offsets, uint32_t ia, uint32_t ib) {
+  int64_t oa = offsets[ia], la = offsets[ia + 1] - oa;
+  int64_t ob = offsets[ib], lb = offsets[ib + 1] - ob;
+  int c = cmp_units_from<CODER>(units, oa, la, ob, lb, 0);
   if (c) return c;
   return ia < ib ? -1 : (ia > ib ? 1 : 0);
 }

@@ -121,8 +121,9 @@ __global__ void k_pick_splitters(const SampleRec *__restrict__ recs, const int *
 // x (code c, units xs[0..xl)) >= splitter?  Code first; on a code tie the units
 // (unsigned, position by position), then the shorter string first.
 template <int W>
-__device__ __forceinline__ bool ge_splitter(uint64_t c, const uint8_t *xs, int64_t xl, const SampleRec &sp) {
-  if (c != sp.code) return c > sp.code;
+__device__ __forceinline__ bool ge_splitter(uint64_t c, const uint8_t *xs, int64_t xl, const SampleRec &sp,
+                                            bool general) {
+  if (!general && c != sp.code) return c > sp.code;
   const int64_t m = xl < (int64_t)sp.len ? xl : (int64_t)sp.len;
   for (int64_t k = 0; k < m; ++k) {
     uint32_t a, b;
@@ -137,7 +138,7 @@ template <int W>
 __global__ void __launch_bounds__(256)
     k_bucket(const uint64_t *__restrict__ codes, uint64_t n, const SampleRec *__restrict__ splitters,
              int nsplit, int world, const void *__restrict__ units, const int64_t *__restrict__ offsets,
-             uint64_t *__restrict__ keys, DevState *st, unsigned long long *counts) {
+             uint64_t *__restrict__ keys, DevState *st, unsigned long long *counts, int general) {
   __shared__ SampleRec s_split[kMaxWorld - 1];
   __shared__ unsigned long long s_cnt[kMaxWorld], s_units[kMaxWorld];
   for (int i = threadIdx.x; i < nsplit; i += blockDim.x) s_split[i] = splitters[i];
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(256)
     int lo = 0, hi = nsplit;  // number of splitters <= x
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
-      if (ge_splitter<W>(c, xs, L, s_split[mid])) lo = mid + 1;
+      if (ge_splitter<W>(c, xs, L, s_split[mid], general != 0)) lo = mid + 1;
       else hi = mid;
     }
     keys[i] = (uint64_t)lo;
@@ -322,6 +323,7 @@ struct Plan {
   Sorter S;
   std::vector<uint64_t> send_cnt, send_u, recv_cnt, recv_u;  // per peer
   uint64_t n_out = 0, units_out = 0;
+  bool general = false;  // some rank saw off-domain units (readings R5, R15)
 
   template <typename T> T *at(size_t o) const { return reinterpret_cast<T *>(ws + o); }
   DevState *st() const { return at<DevState>(M.L.state); }
@@ -368,9 +370,9 @@ struct Plan {
       if (all[(size_t)r * kSampleStride] != ~0ull) ranks.push_back(r);
     }
     if (viol & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing (some rank)");
-    if (domain_violation(coder, viol))
-      return fail(HUSKY_ERR_DOMAIN, "coder %d: a unit outside the coder's domain inside a code window (some rank)",
-                  coder);
+    // off-domain input somewhere: codes are not monotone, so buckets compare the
+    // strings alone (and every rank's local sort runs the general cleanup)
+    general = domain_violation(coder, viol);
     if (world == 1) return HUSKY_OK;
     SampleRec *split = at<SampleRec>(M.splitters);
     const uint64_t m = (uint64_t)ranks.size() * kSamplesPerRank;
@@ -418,11 +420,11 @@ struct Plan {
       if (w() == 1)
         k_bucket<1><<<blocks, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, at<SampleRec>(M.splitters), world - 1, world,
                                            units, offsets, at<uint64_t>(M.L.keysB), st(),
-                                           at<unsigned long long>(M.counts));
+                                           at<unsigned long long>(M.counts), general ? 1 : 0);
       else
         k_bucket<2><<<blocks, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, at<SampleRec>(M.splitters), world - 1, world,
                                            units, offsets, at<uint64_t>(M.L.keysB), st(),
-                                           at<unsigned long long>(M.counts));
+                                           at<unsigned long long>(M.counts), general ? 1 : 0);
       launch_hist_scan(n, st(), s);
       HCHECK(cudaGetLastError());
     }

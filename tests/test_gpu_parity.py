@@ -239,16 +239,28 @@ def test_sort_perm_only_mode(torch, h, oracle_mod):
     assert np.array_equal(perm, oracle_mod.sort(w.coder, w.units, w.offsets))
 
 
-def test_sort_domain_error_and_beyond_window(torch, h, oracle_mod):
-    """Unit > 0x7F inside the ASCII code window -> HUSKY_ERR_DOMAIN (reading R5);
-    beyond the window the exact byte comparator sorts it correctly."""
-    w = W.from_strings([b"abc", b"a\x80c"], ASCII)
-    with pytest.raises(h.HuskyError) as e:
-        run_sort(torch, h, w)
-    assert e.value.status == 2
+def test_sort_off_domain_general_cleanup_and_beyond_window(torch, h, oracle_mod):
+    """A unit > 0x7F inside the ASCII code window makes Alg. 4's masked code
+    non-monotone (reading R5): the general cleanup (NEXT-4, whole-array
+    refinement from unit 0) still yields the exact order; beyond the window the
+    exact byte comparator handles any byte."""
+    outc = check_against_oracle(torch, h, oracle_mod, W.from_strings([b"abc", b"a\x80c", b"a\x00c"] * 7, ASCII))
+    assert not outc["domain_ok"] and outc["refine_rounds"] >= 1
     rng = random.Random(4)
     strings = [b"abcdefghi" + bytes(rng.randint(0, 255) for _ in range(rng.randint(0, 6))) for _ in range(5000)]
-    check_against_oracle(torch, h, oracle_mod, W.from_strings(strings, ASCII))
+    outc = check_against_oracle(torch, h, oracle_mod, W.from_strings(strings, ASCII))
+    assert outc["domain_ok"]
+
+
+@pytest.mark.parametrize("n", [3000, 70_001])
+def test_sort_arbitrary_bytes_ascii_coder(torch, h, oracle_mod, n):
+    """UTF-8-like arbitrary bytes with the ASCII coder: off-domain everywhere, so
+    the general cleanup sorts the whole array (several refinement rounds)."""
+    rng = np.random.default_rng(n)
+    strings = [rng.integers(0, 256, size=int(rng.integers(0, 30))).tolist() for _ in range(n)]
+    strings += [strings[i] for i in range(0, n, 7)]  # duplicates
+    outc = check_against_oracle(torch, h, oracle_mod, W.from_strings(strings, ASCII))
+    assert not outc["domain_ok"]
 
 
 def test_sort_offsets_not_starting_at_zero(torch, h, oracle_mod):
@@ -390,3 +402,24 @@ def test_sort_host_many_pipelined(torch, h, oracle_mod):
                 rsu, rso = oracle_mod.gather(w.coder, w.units, w.offsets, ref)
                 assert np.array_equal(b[4], rso)
                 assert np.array_equal(b[3][:rsu.size], rsu)
+
+
+@pytest.mark.parametrize("world", [2, 5])
+def test_multi_loopback_off_domain(torch, h, oracle_mod, world):
+    """Off-domain ASCII bytes through the sample sort: buckets compare strings
+    only (codes are not monotone there) and every shard runs the general
+    cleanup; the concatenation is the oracle's order."""
+    rng = np.random.default_rng(world)
+    strings = [rng.integers(0, 256, size=int(rng.integers(0, 14))).tolist() for _ in range(40_000)]
+    w = W.from_strings(strings, ASCII)
+    u, o = to_dev(torch, w)
+    tot = w.units.size
+    ws = torch.empty(h.husky_sort_multi_loopback_workspace(w.coder, world, w.n, tot), dtype=torch.uint8,
+                     device="cuda")
+    perm = torch.empty(w.n, dtype=torch.int32, device="cuda")
+    su = torch.empty(tot + 8, dtype=u.dtype, device="cuda")
+    so = torch.empty(w.n + 1, dtype=torch.int64, device="cuda")
+    shards, outc = h.husky_sort_multi_loopback(w.coder, world, u, o, perm, su, so, ws)
+    ref = oracle_mod.sort(w.coder, w.units, w.offsets)
+    assert np.array_equal(perm.cpu().numpy().view(np.uint32), ref)
+    assert sum(shards) == w.n and max(shards) < w.n
