@@ -46,6 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", *ARCH, f"-I{inc}",
               "-DNDEBUG", "--expt-relaxed-constexpr"]
+    # instrumented builds (per-tile phase timestamps): HUSKY_NVCC_DEFS="-DHUSKY_TIMING"
+    common += os.environ.get("HUSKY_NVCC_DEFS", "").split()
     objs = []
     procs = []
     for src in sources():

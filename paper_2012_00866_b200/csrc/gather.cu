@@ -17,6 +17,21 @@
 
 namespace husky {
 
+#ifdef HUSKY_TIMING
+// per-tile phase timestamps of the last gather (instrumented builds only)
+constexpr int kGTimingTiles = 16384;
+__device__ unsigned long long g_gather_times[kGTimingTiles][8];
+__device__ __forceinline__ unsigned long long gt_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define GT(tile, i) \
+  do { if (threadIdx.x == 0 && (tile) < kGTimingTiles) g_gather_times[tile][i] = gt_now(); } while (0)
+#else
+#define GT(tile, i) do { } while (0)
+#endif
+
 // Byte b of a string whose units are fully determined by its husky code (ASCII
 // length <= 9, UNICODE length <= 3): the inverse of Alg. 4's packing.
 template <int CODER>
@@ -24,6 +39,15 @@ __device__ __forceinline__ uint8_t decode_byte(uint64_t code, int b) {
   if (CODER == HUSKY_CODER_ASCII) return (uint8_t)((code >> (56 - 7 * b)) & 0x7F);
   uint32_t u = (uint32_t)(((code << 1) >> (48 - 16 * (b >> 1))) & 0xFFFF);
   return (uint8_t)(b & 1 ? u >> 8 : u);
+}
+
+// 8 bytes at an arbitrary byte offset of the stage (little-endian), from three
+// aligned 32-bit words (the stage has 32 bytes of slack past its end)
+__device__ __forceinline__ uint64_t stage_load8(const uint8_t *stage, uint32_t off) {
+  const uint32_t *sw = reinterpret_cast<const uint32_t *>(stage) + (off >> 2);
+  const uint32_t sh = (off & 3) * 8;
+  const uint32_t x0 = sw[0], x1 = sw[1], x2 = sw[2];
+  return (uint64_t)__funnelshift_r(x0, x1, sh) | ((uint64_t)__funnelshift_r(x1, x2, sh) << 32);
 }
 
 // PACKED: perm holds index | min(len,15) << 28 (written by the encoder, carried
@@ -72,6 +96,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1024 / kGatherThreads)
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint64_t p0 = (uint64_t)tile * kGatherTile + (uint64_t)tid * kGatherItems;
+  GT(tile, 0);
 
   // per item: len (units) and either the source offset or, for strings rebuilt
   // from their code, the code itself (bit j of `dec`)
@@ -106,9 +131,24 @@ __global__ void __launch_bounds__(kGatherThreads, 1024 / kGatherThreads)
         int64_t a = __ldg(offsets + idx), b = __ldg(offsets + idx + 1);
         sv[j] = (uint64_t)a;
         len[j] = (uint32_t)(b - a);
+        // the staging reads these units after the block scan: start the fetch now
+        if (sorted_units && len[j]) {
+          const uint8_t *pa = (const uint8_t *)units + (uint64_t)a * W;
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
+          if ((((uintptr_t)pa & 127) + (uint64_t)len[j] * W) > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 127));
+        }
       }
     }
     mine += len[j];
+  }
+  // CHECK, thread 0: the previous tile's last string (the tile-boundary pair),
+  // its dependent loads issued here so they overlap the scan and the staging
+  unsigned long long b_code = 0;
+  uint32_t b_idx = 0, b_len = 0;
+  if (CHECK && tid == 0 && p0 > 0) {
+    b_code = __ldg(codes + p0 - 1);
+    b_idx = perm[p0 - 1] & (PACKED ? 0x0FFFFFFFu : 0xFFFFFFFFu);  // unpacked or not yet
+    b_len = (uint32_t)(__ldg(offsets + b_idx + 1) - __ldg(offsets + b_idx));
   }
   // CHECK: run flags.  eqp bit j: position p0+j equals its predecessor; eqn:
   // equals its successor (neighbours across lanes by shuffles, across warps and
@@ -135,6 +175,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1024 / kGatherThreads)
   unsigned long long tile_total;
   unsigned long long excl_t = block_exclusive_scan<unsigned long long, kGatherThreads>(
       mine | ((unsigned long long)nstart << 48), &tile_total, s_wt);
+  GT(tile, 1);
   const uint32_t excl_r = (uint32_t)(excl_t >> 48), tile_runs = (uint32_t)(tile_total >> 48);
   excl_t &= (1ull << 48) - 1;
   tile_total &= (1ull << 48) - 1;
@@ -197,6 +238,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1024 / kGatherThreads)
 
   const uint64_t first_w1 = tile_bytes < (uint64_t)kGatherStage ? tile_bytes : (uint64_t)kGatherStage;
   if (sorted_units && !direct) stage_window(0, first_w1);  // overlaps the look-back
+  GT(tile, 2);
 
   if (CHECK) {
     s_lcode[tid] = cc[kGatherItems - 1];
@@ -221,6 +263,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1024 / kGatherThreads)
     }
   }
   __syncthreads();
+  GT(tile, 3);
   const unsigned long long tbase = gbase + s_base;  // units before this tile
   {
     unsigned long long d = tbase + excl_t;
@@ -237,10 +280,10 @@ __global__ void __launch_bounds__(kGatherThreads, 1024 / kGatherThreads)
     uint32_t pl, pi;
     if (tid > 0) {
       pc = s_lcode[tid - 1]; pl = s_llen[tid - 1]; pi = s_lidx[tid - 1]; po = s_loff[tid - 1];
-    } else if (p0 > 0) {  // the previous tile's last string: from the source
-      pc = __ldg(codes + p0 - 1);
-      pi = perm[p0 - 1] & (PACKED ? 0x0FFFFFFFu : 0xFFFFFFFFu);  // unpacked or not yet
-      pl = (uint32_t)(__ldg(offsets + pi + 1) - __ldg(offsets + pi));
+    } else if (p0 > 0) {  // the previous tile's last string (loaded above): from the source
+      pc = b_code;
+      pi = b_idx;
+      pl = b_len;
       po = ~0ull;  // not staged
     } else {
       pc = ~cc[0]; pl = 0; pi = 0; po = ~0ull;  // position 0: no pair
@@ -254,16 +297,22 @@ __global__ void __launch_bounds__(kGatherThreads, 1024 / kGatherThreads)
         if (pl <= PL || len[j] <= PL) {
           c = pl < len[j] ? -1 : (pl > len[j] ? 1 : 0);  // short rule (R6)
         } else if (sorted_units && !direct && po != ~0ull && po + pl <= win_units && d + len[j] <= win_units) {
-          c = 0;  // both staged: compare units [S, min) in shared memory
-          const uint32_t m = pl < len[j] ? pl : len[j];
-          for (uint32_t k = T::kS; k < m && c == 0; ++k) {
-            uint32_t a, b;
-            if (W == 1) { a = stage[po + k]; b = stage[d + k]; }
-            else {
-              a = stage[2 * (po + k)] | (uint32_t)stage[2 * (po + k) + 1] << 8;
-              b = stage[2 * (d + k)] | (uint32_t)stage[2 * (d + k) + 1] << 8;
+          c = 0;  // both staged: compare units [S, min) in shared memory, 8 bytes at a time
+          const uint32_t m = (pl < len[j] ? pl : len[j]) * W;  // bytes
+          for (uint32_t k = T::kS * W; k < m && c == 0; k += 8) {
+            uint64_t x = stage_load8(stage, (uint32_t)(po * W) + k), y = stage_load8(stage, (uint32_t)(d * W) + k);
+            const uint32_t take = m - k < 8 ? m - k : 8;
+            if (take < 8) {
+              const uint64_t msk = (1ull << (8 * take)) - 1;
+              x &= msk;
+              y &= msk;
             }
-            if (a != b) c = a < b ? -1 : 1;
+            const uint64_t df = x ^ y;
+            if (df) {
+              const int sh = ((__ffsll((long long)df) - 1) / (8 * W)) * (8 * W);  // first differing unit
+              const uint64_t um = W == 1 ? 0xFFull : 0xFFFFull;
+              c = ((x >> sh) & um) < ((y >> sh) & um) ? -1 : 1;
+            }
           }
           if (c == 0) c = pl < len[j] ? -1 : (pl > len[j] ? 1 : 0);
         } else {
@@ -287,6 +336,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1024 / kGatherThreads)
       }
     }
   }
+  GT(tile, 4);
   if (sorted_units == nullptr) return;
 
   uint8_t *g0 = ob + tbase * W;  // first output byte of the tile
@@ -299,6 +349,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1024 / kGatherThreads)
       __syncthreads();
       write_window(g0, w0, w1);
     }
+    GT(tile, 5);
   } else {
     // debug path: warp-cooperative byte copy, one string at a time per warp
     for (int t = 0; t < 32; ++t) {
@@ -444,3 +495,16 @@ void launch_regather_runs(int coder, const uint2 *list_sm, uint64_t cap_sm, cons
 }
 
 }  // namespace husky
+
+extern "C" int husky_debug_gather_times(unsigned long long *out, int max_tiles) {
+#ifdef HUSKY_TIMING
+  int k = max_tiles < husky::kGTimingTiles ? max_tiles : husky::kGTimingTiles;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, husky::g_gather_times, (size_t)k * 8 * sizeof(unsigned long long));
+  return k;
+#else
+  (void)out;
+  (void)max_tiles;
+  return 0;
+#endif
+}
