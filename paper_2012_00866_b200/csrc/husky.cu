@@ -234,7 +234,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
     // the host enqueues all 8 pass slots without waiting; slots beyond the plan
     // exit at once.  Input violations (bad offsets, ASCII domain) make every
     // later kernel a no-op and are reported at the single synchronisation below.
-    launch_radix_plan(st, keysA, keysB, s);
+    launch_radix_plan(st, keysA, keysB, n, s);
     {
       GroupScope grp(ST_RADIX, s);  // profiler mode 2: the 8 pass slots as one timed group
       for (int slot = 0; slot < 8; ++slot)

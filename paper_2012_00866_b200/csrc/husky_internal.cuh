@@ -74,6 +74,7 @@ struct DevState {
   // and which ping-pong key buffer ends up holding the sorted codes
   uint32_t np;
   uint32_t pass_digit[8];
+  uint32_t pass_ballot[8];  // rank a pass with per-bit ballots instead of __match_any_sync
   unsigned long long sorted_keys;  // uint64_t* of the sorted keys
   // MSD key sort (msd.cu): OR and NOT-AND of all codes (fused into A1; zero-
   // initialised), segment-list fill counts and tile counts of the two level
@@ -96,6 +97,20 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+// Lanes holding the same 8-bit label as this lane (converged warp): one ballot
+// per label bit -- an alternative to __match_any_sync whose cost on sm_100a
+// depends on the label distribution.
+__device__ __forceinline__ uint32_t match_ballot8(uint32_t label) {
+  uint32_t m = 0xFFFFFFFFu;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const bool bit = (label >> b) & 1u;
+    const uint32_t v = __ballot_sync(0xFFFFFFFFu, bit);
+    m &= bit ? v : ~v;
+  }
+  return m;
+}
 
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {

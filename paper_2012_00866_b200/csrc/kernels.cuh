@@ -44,7 +44,7 @@ void launch_iota(uint32_t *perm, uint64_t n, cudaStream_t s);
 // mask into DevState::np / pass_digit / sorted_keys; slots 0..7 are launched
 // unconditionally and resolve their digit and ping-pong buffers on device (the
 // last planned pass writes vals_final); finalize copies the payload when np == 0.
-void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, cudaStream_t s);
+void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint64_t n, cudaStream_t s);
 void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint32_t *vals_init,
                           uint32_t *vals_final, uint32_t *vals_tmp, uint64_t n, DevState *st,
                           unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);

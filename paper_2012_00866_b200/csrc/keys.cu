@@ -86,7 +86,7 @@ husky_status husky_sort_keys(int key_type, const void *d_keys, uint64_t n, uint3
   }
   launch_hist8(keysA, n, st, S.sms, s);
   launch_hist_scan(n, st, s);
-  launch_radix_plan(st, keysA, keysB, s);
+  launch_radix_plan(st, keysA, keysB, n, s);
   for (int slot = 0; slot < 8; ++slot)
     launch_onesweep_slot(slot, keysA, keysB, nullptr, d_perm, S.at<uint32_t>(L.vals), n, st, S.lb_radix(),
                          S.next_counter(), S.next_epoch(), s);

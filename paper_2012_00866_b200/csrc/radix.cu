@@ -66,11 +66,30 @@ __device__ __forceinline__ unsigned long long gtimer() {
 constexpr int kExchangeBytes = kRadixTile * (8 + 4) + kRadixWarps * 256 * 4;
 
 // Device-side pass plan: lets the host launch all 8 pass slots without
-// reading the trivial-digit mask back (no host synchronisation).
-__global__ void k_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB) {
+// reading the trivial-digit mask back (no host synchronisation).  Also picks
+// each pass's ranking primitive: a digit whose largest bin holds < 5% of the
+// keys (many distinct labels per warp) is ranked with per-bit ballots, the rest
+// with __match_any_sync -- measured per digit on C2 / C3.
+__global__ void __launch_bounds__(256) k_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint64_t n,
+                                                    uint32_t force_ballot, uint32_t force_match) {
+  __shared__ uint32_t s_max[8][8];
+  const uint32_t t = threadIdx.x, lane = lane_id(), warp = t >> 5;
+#pragma unroll
+  for (int d = 0; d < 8; ++d) {
+    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, st->hist[d][t]);
+    if (lane == 0) s_max[d][warp] = m;
+  }
+  __syncthreads();
+  if (t != 0) return;
   uint32_t m = st->trivial_mask, np = 0;
   for (int d = 0; d < 8; ++d)
-    if (!((m >> d) & 1)) st->pass_digit[np++] = d;
+    if (!((m >> d) & 1)) {
+      uint32_t mx = 0;
+      for (int w = 0; w < 8; ++w) mx = s_max[d][w] > mx ? s_max[d][w] : mx;
+      const bool spread = (uint64_t)mx * 20 < n;
+      st->pass_ballot[np] = ((force_ballot >> d) & 1) || (spread && !((force_match >> d) & 1));
+      st->pass_digit[np++] = d;
+    }
   st->np = np;
   st->sorted_keys = (unsigned long long)((np & 1) ? keysB : keysA);
 }
@@ -101,10 +120,12 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
                const uint32_t *__restrict__ digit_start, unsigned long long *lb, uint32_t *tile_counter,
                uint32_t epoch, const uint32_t *__restrict__ prefix, uint32_t num_tiles, const DevState *plan,
                int slot, SlotPtrs sp) {
+  bool use_ballot = false;
   if (plan) {
     const uint32_t np = plan->np;
     if ((uint32_t)slot >= np) return;
     const uint32_t digit = plan->pass_digit[slot];
+    use_ballot = plan->pass_ballot[slot] != 0;
     shift = 8 * digit;
     digit_start = plan->digit_start[digit];
     keys_in = (slot & 1) ? sp.kB : sp.kA;
@@ -158,7 +179,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
 #pragma unroll
   for (int r = 0; r < kRadixItems; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & 0xFF;
-    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+    uint32_t peers = use_ballot ? match_ballot8(d) : __match_any_sync(0xFFFFFFFFu, d);
     if (r == 0) HT(tile, 1);
     uint32_t pre = wc[d];
     rank[r] = pre + __popc(peers & lanemask_lt());
@@ -341,9 +362,16 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
                                                           tile_counter, epoch, counts, tiles, nullptr, 0, SlotPtrs{});
 }
 
-void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, cudaStream_t s) {
+void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint64_t n, cudaStream_t s) {
   Scope sc_(ST_HIST_SCAN, s, 0);
-  k_radix_plan<<<1, 1, 0, s>>>(st, keysA, keysB);
+  // experiments: HUSKY_RANK_BALLOT / HUSKY_RANK_MATCH = digit bit masks that
+  // force one primitive (default: the plan's < 5% largest-bin rule)
+  auto env_mask = [](const char *name) {
+    const char *v = getenv(name);
+    return v ? (uint32_t)strtoul(v, nullptr, 0) : 0u;
+  };
+  static const uint32_t force_ballot = env_mask("HUSKY_RANK_BALLOT"), force_match = env_mask("HUSKY_RANK_MATCH");
+  k_radix_plan<<<1, 256, 0, s>>>(st, keysA, keysB, n, force_ballot, force_match);
 }
 
 // Pass slot `slot` (0..7) of the device-side plan, onesweep variant.  Launched
