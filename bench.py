@@ -332,7 +332,7 @@ def run_ours(args):
         # pipelined: the K steps as K batches of husky_sort_host_many (2 workers,
         # each with its own stream), so one step's copies overlap another's
         # kernels and the full-duplex PCIe carries H2D and D2H at once
-        depth = 2
+        depth = int(os.environ.get("HUSKY_E2E_DEPTH", "2"))
         hws = None
         torch.cuda.empty_cache()
         mws = torch.empty(h.husky_sort_host_many_workspace(w.coder, n, total_units, depth), dtype=torch.uint8,
