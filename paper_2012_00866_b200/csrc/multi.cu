@@ -27,6 +27,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -147,19 +149,43 @@ __global__ void __launch_bounds__(256)
     s_units[i] = 0;
   }
   __syncthreads();
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t c = codes[i];
-    const int64_t o = offsets[i], L = offsets[i + 1] - o;
-    const uint8_t *xs = (const uint8_t *)units + o * W;
-    int lo = 0, hi = nsplit;  // number of splitters <= x
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (ge_splitter<W>(c, xs, L, s_split[mid], general != 0)) lo = mid + 1;
-      else hi = mid;
+  // counts are aggregated per warp when the warp's strings share one bucket
+  // (P = 1, sorted or skewed input): per-lane atomics on one shared address
+  // serialise (0.9 ms for 1e7 strings at P = 1)
+  const uint32_t lane = lane_id();
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    uint32_t b = 0xFFFFFFFFu;
+    unsigned long long L = 0;
+    if (valid) {
+      const uint64_t c = codes[i];
+      const int64_t o = offsets[i];
+      L = (unsigned long long)(offsets[i + 1] - o);
+      const uint8_t *xs = (const uint8_t *)units + o * W;
+      int lo = 0, hi = nsplit;  // number of splitters <= x
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (ge_splitter<W>(c, xs, (int64_t)L, s_split[mid], general != 0)) lo = mid + 1;
+        else hi = mid;
+      }
+      b = (uint32_t)lo;
+      keys[i] = (uint64_t)lo;
     }
-    keys[i] = (uint64_t)lo;
-    atomicAdd(&s_cnt[lo], 1ull);
-    atomicAdd(&s_units[lo], (unsigned long long)L);
+    const uint32_t b0 = __shfl_sync(0xFFFFFFFFu, b, 0);
+    if (__all_sync(0xFFFFFFFFu, b == b0 || !valid)) {
+      unsigned long long sum = L;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+      const uint32_t nv = __popc(__ballot_sync(0xFFFFFFFFu, valid));
+      if (lane == 0 && nv) {
+        atomicAdd(&s_cnt[b0], (unsigned long long)nv);
+        atomicAdd(&s_units[b0], sum);
+      }
+    } else if (valid) {  // several buckets: few lanes share an address
+      atomicAdd(&s_cnt[b], 1ull);
+      atomicAdd(&s_units[b], L);
+    }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < world; b += blockDim.x) {
@@ -199,18 +225,14 @@ __global__ void __launch_bounds__(kScanThreads)
   }
   unsigned long long tot;
   unsigned long long ex = block_exclusive_scan<unsigned long long, kScanThreads>(sum, &tot, s_wt);
-  if (threadIdx.x == 0) {
-    unsigned long long *f = lb + tile, b;
-    if (tile == 0) {
-      b = 0;
-      st_relaxed_u64(f, make_flag(kFlagInc, epoch, tot));
-    } else {
-      st_relaxed_u64(f, make_flag(kFlagAgg, epoch, tot));
-      b = lookback(lb, tile, 1, epoch);
-      st_relaxed_u64(f, make_flag(kFlagInc, epoch, b + tot));
+  if (threadIdx.x == 0) st_relaxed_u64(lb + tile, make_flag(tile == 0 ? kFlagInc : kFlagAgg, epoch, tot));
+  if (threadIdx.x < 32) {  // warp-wide look-back: 32 predecessors per round trip
+    const unsigned long long b = tile == 0 ? 0ull : warp_lookback(lb, tile, epoch);
+    if (threadIdx.x == 0) {
+      if (tile != 0) st_relaxed_u64(lb + tile, make_flag(kFlagInc, epoch, b + tot));
+      s_base = b;
+      if ((uint64_t)(tile + 1) * kScanTile >= n) offsets[n] = (int64_t)(b + tot) + add;
     }
-    s_base = b;
-    if ((uint64_t)(tile + 1) * kScanTile >= n) offsets[n] = (int64_t)(b + tot) + add;
   }
   __syncthreads();
   unsigned long long d = s_base + ex;
@@ -237,6 +259,25 @@ static unsigned grid_for(uint64_t n) {
 }
 
 // ------------------------------------------------------------------ host side
+// HUSKY_MULTI_TIMING=1: synchronise after each phase and print its wall time
+// (diagnostics only; changes the overlap it measures)
+struct PhaseClock {
+  cudaStream_t s;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseClock(cudaStream_t st) : s(st) {
+    const char *v = getenv("HUSKY_MULTI_TIMING");
+    on = v && v[0] == '1';
+    if (on) { cudaStreamSynchronize(s); t = std::chrono::steady_clock::now(); }
+  }
+  void mark(const char *name) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[husky multi] %-24s %8.1f us\n", name, std::chrono::duration<double, std::micro>(n - t).count());
+    t = n;
+  }
+};
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Comm {
@@ -650,13 +691,19 @@ husky_status husky_sort_multi_plan(void *comm, int coder, const void *d_units, c
   P->s = s;
   P->M = make_multi_layout(coder, n_local, P->local_units, c->world);
   husky_status e = HUSKY_OK;
+  PhaseClock pc(s);
   if (ws_bytes < P->M.total) e = fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, P->M.total);
   if (!e) e = P->phase1();
+  pc.mark("encode+sample");
   if (!e) e = nccl_allgather_samples(*P);
+  pc.mark("allgather samples");
   if (!e) e = P->choose_splitters();
+  pc.mark("splitters");
   if (!e) e = P->phase2();
+  pc.mark("bucket");
   if (!e) e = nccl_alltoall_counts(*P);
   if (!e) e = P->read_counts();
+  pc.mark("counts");
   if (e) { delete P; return e; }
   if (h_n_out) *h_n_out = P->n_out;
   if (h_units_out) *h_units_out = P->units_out;
@@ -684,10 +731,14 @@ husky_status husky_sort_multi_exec(void *plan, uint32_t *d_perm_out, void *d_sor
   RecvLayout R = make_recv_layout(P->coder, P->n_out, P->units_out);
   if (recv_ws_bytes < R.total) return fail(HUSKY_ERR_WORKSPACE, "recv workspace %zu < %zu", recv_ws_bytes, R.total);
   if ((uintptr_t)d_recv_ws % 256) return fail(HUSKY_ERR_INVALID_ARG, "workspace not 256-byte aligned");
+  PhaseClock pc(P->s);
   if (husky_status e = P->phase3()) return e;
+  pc.mark("partition+send buffers");
   if (husky_status e = nccl_exchange(*P, (uint8_t *)d_recv_ws, R)) return e;
+  pc.mark("exchange");
   if (husky_status e = P->phase4((uint8_t *)d_recv_ws, R, d_perm_out, d_sorted_units_out, d_sorted_offsets_out, h_out))
     return e;
+  pc.mark("local sort");
   HCHECK(cudaStreamSynchronize(P->s));
   return HUSKY_OK;
 }
