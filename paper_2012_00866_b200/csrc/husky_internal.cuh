@@ -193,56 +193,6 @@ __device__ __forceinline__ unsigned long long lookback_window(const unsigned lon
   return excl;
 }
 
-__device__ __forceinline__ void ld_relaxed_v2u64(const unsigned long long *p, unsigned long long &a,
-                                                 unsigned long long &b) {
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
-}
-
-// Look-back over a TRANSPOSED flag row (row[t] = word of tile t for one digit):
-// one round trip reads the 16 nearest predecessors with 8 aligned 16-byte
-// loads, so the inclusive-prefix frontier keeps up with the tile arrival rate
-// (a window of 1-8 tiles per round trip falls behind on a 148-SM part).
-__device__ __forceinline__ unsigned long long lookback_row16(const unsigned long long *row, uint32_t tile,
-                                                             uint32_t epoch) {
-  unsigned long long excl = 0;
-  int64_t j = (int64_t)tile - 1;
-  const unsigned long long inc0 = make_flag(kFlagInc, epoch, 0);
-  while (j >= 0) {
-    const int64_t lo = (j & 1) ? j - 15 : j - 14;  // even: 16-byte aligned pairs; covers lo..j (j <= lo+15)
-    unsigned long long w[16];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      int64_t i = lo + 2 * q;
-      if (i >= 0) ld_relaxed_v2u64(row + i, w[2 * q], w[2 * q + 1]);
-      else { w[2 * q] = inc0; w[2 * q + 1] = inc0; }
-    }
-    int used = 0;
-    bool done = false, blocked = false;
-#pragma unroll
-    for (int q = 15; q >= 0; --q) {
-      if (done || blocked) continue;
-      if (lo + q > j) continue;  // the word past the nearest predecessor
-      unsigned long long x = w[q];
-      bool ok = ((uint32_t)(x >> 54) & 0xFF) == epoch && (x & (3ull << 62)) != 0;
-      if (!ok) { blocked = true; continue; }
-      excl += x & kValMask;
-      ++used;
-      if ((x & (3ull << 62)) == kFlagInc) done = true;
-    }
-    if (done) break;
-    j -= used;
-    if (blocked) {  // poll just the blocking word, backing off
-      unsigned ns = 32;
-      for (;;) {
-        unsigned long long x = ld_relaxed_u64(row + j);
-        if (((uint32_t)(x >> 54) & 0xFF) == epoch && (x & (3ull << 62)) != 0) break;
-        __nanosleep(ns);
-        if (ns < 512) ns <<= 1;
-      }
-    }
-  }
-  return excl;
-}
 
 // Warp-cooperative look-back (all 32 lanes call it): lane l reads the word of
 // tile (base - l); the nearest inclusive word ends the walk.  Returns the
@@ -322,8 +272,6 @@ __device__ __forceinline__ void cp_async4(void *smem_dst, const void *gmem_src) 
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // Unaligned little-endian load of 8 bytes at byte address p, reading only the
 // aligned 8-byte words that contain bytes [p, p + need) (need in 1..8), so it
@@ -372,21 +320,6 @@ __device__ __forceinline__ int cmp_units_from(const void *units, int64_t oa, int
   return 0;
 }
 
-// Exact comparator for two strings whose husky codes are EQUAL (DESIGN.md R6):
-// if either length <= PL the shorter one is a prefix of the longer (order by
-// length, then index); otherwise units [0, S) are equal and the comparison
-// starts at unit `from` (>= S when the caller knows a longer common prefix).
-template <int CODER>
-__device__ __forceinline__ int cmp_equal_code_ol(const void *units, int64_t oa, int64_t la, uint32_t ia,
-                                                 int64_t ob, int64_t lb, uint32_t ib, int64_t from) {
-  using T = CoderTraits<CODER>;
-  int c;
-  if (la <= T::kPL || lb <= T::kPL) c = (la < lb) ? -1 : (la > lb ? 1 : 0);
-  else c = cmp_units_from<CODER>(units, oa, la, ob, lb, from);
-  if (c) return c;
-  return ia < ib ? -1 : (ia > ib ? 1 : 0);
-}
-
 // Exact comparator with no assumption on the codes (general cleanup, NEXT-4):
 // units from 0, a proper prefix first, then the index.
 template <int CODER>
@@ -398,6 +331,10 @@ __device__ __forceinline__ int cmp_general(const void *units, const int64_t *off
   return ia < ib ? -1 : (ia > ib ? 1 : 0);
 }
 
+// Exact comparator for two strings whose husky codes are EQUAL (DESIGN.md R6):
+// if either length <= PL the shorter one is a prefix of the longer (order by
+// length, then index); otherwise units [0, S) are equal and the comparison
+// starts at unit `from` (>= S when the caller knows a longer common prefix).
 template <int CODER>
 __device__ __forceinline__ int cmp_equal_code(const void *units, const int64_t *offsets, uint32_t ia,
                                               uint32_t ib, int64_t from) {

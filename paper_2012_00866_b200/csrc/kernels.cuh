@@ -88,9 +88,8 @@ husky_status msd_key_sort(Sorter &S, const MsdBufs &B);
 
 // A3 run detection (single-pass scan with decoupled look-back)
 constexpr int kScanThreads = 512, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
-// padded smem staging sizes of k_runs_scan (one pad u64 every 8, one pad u32 every 32)
+// padded smem staging size of k_runs_scan (one pad u64 every 8)
 constexpr int kScanKP = kScanTile + 2 + (kScanTile + 2) / 8 + 1;
-constexpr int kScanPP = kScanTile + 2 + (kScanTile + 2) / 32 + 1;
 inline uint64_t scan_tiles(uint64_t n) { return (n + kScanTile - 1) / kScanTile; }
 // mode 0: keys are husky codes; a pair inside a run is checked with the exact
 //         equal-code comparator (strings via perm -> offsets -> units).
@@ -98,8 +97,7 @@ inline uint64_t scan_tiles(uint64_t n) { return (n + kScanTile - 1) / kScanTile;
 void launch_runs_scan(int coder, int mode, const uint64_t *keys, uint64_t n, const uint32_t *perm,
                       const void *units, const int64_t *offsets, uint32_t base, uint32_t *run_start,
                       uint32_t *run_end, uint8_t *dirty, DevState *st, unsigned long long *lb,
-                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s,
-                      const void *sorted_units = nullptr, const int64_t *sorted_offsets = nullptr);
+                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
 void launch_runs_classify(const uint32_t *run_start, const uint32_t *run_end, const uint8_t *dirty,
                           DevState *st, uint2 *list_sm, uint64_t cap_sm, uint2 *list_g,
                           bool count_stats, int num_sms, cudaStream_t s);

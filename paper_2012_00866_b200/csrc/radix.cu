@@ -9,19 +9,21 @@
 //
 // A pass (one 8-bit digit) works on tiles of 4096 keys (512 threads x 8,
 // warp-striped so every load/store instruction is a coalesced 256-B access).
-// Each tile is ranked in shared memory with warp-level match (__match_any_sync)
-// + popc into per-warp digit counters, exchanged through shared memory into
-// digit order, and written out as runs of consecutive addresses.  The tile's
-// global base per digit comes from one of two schemes:
-//   * onesweep (HUSKY_RADIX=onesweep): per-(tile, digit) decoupled look-back
-//     (Adinets & Merrill), global digit starts from the histograms the encoder
-//     fused into A1.  One read of the keys per pass, but the look-back is a chain
-//     of dependent L2 round trips (~1 us each with the memory system saturated;
+// Each tile is ranked in shared memory with warp-level label matching
+// (__match_any_sync, or per-bit ballots when the plan says the digit is spread
+// out) + popc into per-warp digit counters, exchanged through shared memory
+// into digit order, and written out as runs of consecutive addresses.  The
+// tile's global base per digit comes from one of two schemes:
+//   * onesweep (default): per-(tile, digit) decoupled look-back (Adinets &
+//     Merrill), global digit starts from the 8 x 256 histograms of the codes
+//     (k_hist8).  One read of the keys per pass, but the look-back is a chain of
+//     dependent L2 round trips (~1 us each with the memory system saturated;
 //     measured per-tile phases in DESIGN.md).
-//   * reduce-then-scan (default): an upsweep writes each tile's digit counts
-//     (8 B/key read), a digit-parallel scan turns them into per-tile bases, and
-//     the downsweep ranks/exchanges/scatters with no inter-tile dependency.
-// Digits whose histogram puts all keys in one bucket are skipped by the caller.
+//   * reduce-then-scan (HUSKY_RADIX=rts, host-planned passes only): an upsweep
+//     writes each tile's digit counts (8 B/key read), a digit-parallel scan
+//     turns them into per-tile bases, and the downsweep ranks/exchanges/scatters
+//     with no inter-tile dependency (measured slower).
+// Digits whose histogram puts all keys in one bucket are skipped.
 #include "husky_internal.cuh"
 #include "kernels.cuh"
 

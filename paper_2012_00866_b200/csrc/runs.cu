@@ -10,9 +10,11 @@
 // order (Timsort's natural-run idea).  Only dirty runs reach
 // the fix-up (A5) -- the analogue of Alg. 1's cleanup pass.
 //
-// k_runs_scan is a single-pass scan (decoupled look-back over tiles of 2048
+// k_runs_scan is a single-pass scan (decoupled look-back over tiles of 4096
 // positions) of the "nontrivial run starts here" flags; the k-th start and the
-// k-th end belong to run k.
+// k-th end belong to run k.  With sorted outputs the main path does this inside
+// the gather (gather.cu, CHECK); this kernel serves the perm-only mode (MODE 0:
+// strings through perm -> offsets -> units) and the refinement (MODE 1).
 #include "husky_internal.cuh"
 #include "kernels.cuh"
 
@@ -23,17 +25,13 @@ __global__ void __launch_bounds__(kScanThreads)
     k_runs_scan(const uint64_t *__restrict__ keys, uint64_t n, const uint32_t *__restrict__ perm,
                 const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t base,
                 uint32_t *__restrict__ run_start, uint32_t *__restrict__ run_end, uint8_t *__restrict__ dirty,
-                DevState *st, unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch,
-                const void *__restrict__ sunits, const int64_t *__restrict__ soffs) {
+                DevState *st, unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch) {
   using T = CoderTraits<CODER>;
-  // Tile staging in smem (coalesced async copies).  Each thread then works on
-  // kScanItems consecutive positions; the arrays are padded (one pad element
-  // every 8 u64 / 32 u32) so that blocked per-thread reads do not bank-conflict.
-  constexpr bool SO = MODE == 2;
-  extern __shared__ __align__(16) uint8_t dsm[];  // runs_scan_smem(mode) bytes
-  uint64_t *s_keys = reinterpret_cast<uint64_t *>(dsm);                 // keys[tile_base - 1 + i]
-  int64_t *s_soff = reinterpret_cast<int64_t *>(dsm + kScanKP * 8);      // soffs[tile_base + i]
-  uint32_t *s_perm = reinterpret_cast<uint32_t *>(dsm + kScanKP * 16);   // perm[tile_base + i]
+  // Tile staging of the keys in smem (coalesced async copies).  Each thread then
+  // works on kScanItems consecutive positions; the array is padded (one pad
+  // element every 8 u64) so that blocked per-thread reads do not bank-conflict.
+  extern __shared__ __align__(16) uint8_t dsm[];  // kScanKP * 8 bytes
+  uint64_t *s_keys = reinterpret_cast<uint64_t *>(dsm);  // keys[tile_base - 1 + i]
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_wt[kScanThreads / 32 + 1];
   __shared__ unsigned long long s_excl;
@@ -48,11 +46,6 @@ __global__ void __launch_bounds__(kScanThreads)
   for (uint32_t i = tid; i < kScanTile + 2; i += kScanThreads) {
     int64_t p = (int64_t)tb + (int64_t)i - 1;
     if (p >= 0 && (uint64_t)p < n) cp_async8(&s_keys[i + i / 8], keys + p);
-    if (SO) {
-      uint64_t q = tb + i;
-      if (q <= n) cp_async8(&s_soff[i + i / 8], soffs + q);
-      if (q < n) cp_async4(&s_perm[i + i / 32], perm + q);
-    }
   }
   cp_async_commit();
   cp_async_wait_all();
@@ -89,13 +82,6 @@ __global__ void __launch_bounds__(kScanThreads)
       bool bad;
       if (MODE == 0) {
         bad = cmp_equal_code<CODER>(units, offsets, __ldg(perm + p), __ldg(perm + p + 1), T::kS) > 0;
-      } else if (MODE == 2) {
-        // strings already gathered in sorted order: offsets / indices from smem,
-        // units (only for pairs longer than PL) contiguous in sorted_units
-        uint32_t i = tid * kScanItems + j;
-        int64_t oa = s_soff[i + i / 8], ob = s_soff[(i + 1) + (i + 1) / 8], oe = s_soff[(i + 2) + (i + 2) / 8];
-        uint32_t ia = s_perm[i + i / 32], ib = s_perm[(i + 1) + (i + 1) / 32];
-        bad = cmp_equal_code_ol<CODER>(sunits, oa, ob - oa, ia, ob, oe - ob, ib, T::kS) > 0;
       } else {
         constexpr uint64_t tagmask = CODER == HUSKY_CODER_ASCII ? 0xFFull : 0xFFFFull;
         bad = (c[j + 1] & tagmask) == (uint64_t)(16 + T::kTagCap);
@@ -133,33 +119,25 @@ __global__ void __launch_bounds__(kScanThreads)
 void launch_runs_scan(int coder, int mode, const uint64_t *keys, uint64_t n, const uint32_t *perm,
                       const void *units, const int64_t *offsets, uint32_t base, uint32_t *run_start,
                       uint32_t *run_end, uint8_t *dirty, DevState *st, unsigned long long *lb,
-                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, const void *sunits,
-                      const int64_t *soffs) {
+                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s) {
   if (n == 0) return;
-  // staging: keys (all modes) + sorted offsets and perm (mode 2), padded
-  constexpr int kSmem0 = kScanKP * 8, kSmem2 = kScanKP * 16 + kScanPP * 4;
+  constexpr int kSmem0 = kScanKP * 8;  // the padded key staging
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_ASCII, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
     cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_ASCII, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
-    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_ASCII, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
     cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_UNICODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
     cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_UNICODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
-    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_UNICODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
     configured = true;
   }
   Scope sc_(ST_RUNS_SCAN, s, n);
   dim3 g((unsigned)scan_tiles(n)), b(kScanThreads);
-#define RS_ARGS \
-  keys, n, perm, units, offsets, base, run_start, run_end, dirty, st, lb, tile_counter, epoch, sunits, soffs
-  if (mode == 0 && sunits) mode = 2;
+#define RS_ARGS keys, n, perm, units, offsets, base, run_start, run_end, dirty, st, lb, tile_counter, epoch
   if (coder == HUSKY_CODER_ASCII) {
     if (mode == 0) k_runs_scan<HUSKY_CODER_ASCII, 0><<<g, b, kSmem0, s>>>(RS_ARGS);
-    else if (mode == 2) k_runs_scan<HUSKY_CODER_ASCII, 2><<<g, b, kSmem2, s>>>(RS_ARGS);
     else k_runs_scan<HUSKY_CODER_ASCII, 1><<<g, b, kSmem0, s>>>(RS_ARGS);
   } else {
     if (mode == 0) k_runs_scan<HUSKY_CODER_UNICODE, 0><<<g, b, kSmem0, s>>>(RS_ARGS);
-    else if (mode == 2) k_runs_scan<HUSKY_CODER_UNICODE, 2><<<g, b, kSmem2, s>>>(RS_ARGS);
     else k_runs_scan<HUSKY_CODER_UNICODE, 1><<<g, b, kSmem0, s>>>(RS_ARGS);
   }
 #undef RS_ARGS
