@@ -309,6 +309,55 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// Reduce-then-scan for a device-planned pass slot (HUSKY_RADIX=rts): per-tile
+// counts of the slot's digit with plain shared-memory atomics (warp-private
+// copies), then a digit-parallel scan turns them into per-tile bases; the
+// downsweep is k_onesweep<.., false>, which waits on nothing.
+__global__ void __launch_bounds__(256)
+    k_rs_upsweep_slot(const DevState *plan, int slot, const uint64_t *kA, const uint64_t *kB, uint64_t n,
+                      uint32_t *__restrict__ counts, uint32_t num_tiles) {
+  if ((uint32_t)slot >= plan->np) return;
+  __shared__ uint32_t h[8][256];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 8 * 256; i += 256) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const int shift = 8 * (int)plan->pass_digit[slot];
+  const uint64_t *keys = (slot & 1) ? kB : kA;
+  const uint32_t tile = blockIdx.x;
+  const uint64_t tb = (uint64_t)tile * kRadixTile;
+  uint64_t k[kRadixTile / 256];
+#pragma unroll
+  for (int r = 0; r < kRadixTile / 256; ++r) {
+    const uint64_t i = tb + r * 256 + tid;
+    k[r] = i < n ? __ldg(keys + i) : 0;
+  }
+#pragma unroll
+  for (int r = 0; r < kRadixTile / 256; ++r)
+    if (tb + r * 256 + tid < n) atomicAdd(&h[warp][(uint32_t)(k[r] >> shift) & 0xFF], 1u);
+  __syncthreads();
+  uint32_t c = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) c += h[w][tid];
+  counts[(uint64_t)tid * num_tiles + tile] = c;
+}
+
+__global__ void __launch_bounds__(1024)
+    k_rs_scan_slot(const DevState *plan, int slot, uint32_t *__restrict__ counts, uint32_t num_tiles) {
+  if ((uint32_t)slot >= plan->np) return;
+  __shared__ uint32_t wt[33];
+  uint32_t *row = counts + (uint64_t)blockIdx.x * num_tiles;
+  uint32_t running = plan->digit_start[plan->pass_digit[slot]][blockIdx.x];
+  for (uint32_t c = 0; c < num_tiles; c += 1024) {
+    uint32_t i = c + threadIdx.x;
+    uint32_t v = i < num_tiles ? row[i] : 0u;
+    uint32_t total;
+    uint32_t ex = block_exclusive_scan<uint32_t, 1024>(v, &total, wt);
+    if (i < num_tiles) row[i] = running + ex;
+    running += total;
+    __syncthreads();
+  }
+}
+
 // instrumented builds: copy the per-tile phase timestamps of the last pass
 extern "C" int husky_debug_tile_times(unsigned long long *out, int max_tiles) {
 #ifdef HUSKY_TIMING
@@ -391,6 +440,28 @@ void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint
   Scope sc_(ST_RADIX, s, n);
   const uint32_t tiles = (uint32_t)radix_tiles(n);
   SlotPtrs sp{keysA, keysB, vals_init, vals_final, vals_tmp};
+  static const bool rts = [] {
+    const char *v = getenv("HUSKY_RADIX");
+    return v && v[0] == 'r';
+  }();
+  if (rts) {
+    static bool cfg2 = false;
+    if (!cfg2) {
+      cudaFuncSetAttribute(k_onesweep<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
+      cudaFuncSetAttribute(k_onesweep<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
+      cfg2 = true;
+    }
+    uint32_t *counts = reinterpret_cast<uint32_t *>(lb);  // 256 x tiles u32 (the look-back words are unused)
+    k_rs_upsweep_slot<<<tiles, 256, 0, s>>>(st, slot, keysA, keysB, n, counts, tiles);
+    k_rs_scan_slot<<<256, 1024, 0, s>>>(st, slot, counts, tiles);
+    if (slot == 0 && vals_init == nullptr)
+      k_onesweep<true, false><<<tiles, kRadixThreads, kExchangeBytes, s>>>(
+          nullptr, nullptr, nullptr, nullptr, n, 0, nullptr, lb, tile_counter, epoch, counts, tiles, st, slot, sp);
+    else
+      k_onesweep<false, false><<<tiles, kRadixThreads, kExchangeBytes, s>>>(
+          nullptr, nullptr, nullptr, nullptr, n, 0, nullptr, lb, tile_counter, epoch, counts, tiles, st, slot, sp);
+    return;
+  }
   if (slot == 0 && vals_init == nullptr)
     k_onesweep<true, true><<<tiles, kRadixThreads, kExchangeBytes, s>>>(
         nullptr, nullptr, nullptr, nullptr, n, 0, nullptr, lb, tile_counter, epoch, nullptr, tiles, st, slot, sp);
