@@ -121,12 +121,16 @@ def cpu_baseline(name, n_sample):
     import oracle
     oracle.build()
     w = W.make(name, n_sample)
-    t0 = time.perf_counter()
-    oracle.sort(w.coder, w.units, w.offsets)
-    dt = time.perf_counter() - t0
-    return {"value": round(n_sample / dt / 1e6, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{name} generator, n={n_sample} strings, one oracle_sort call (top-down merge sort, "
-                      f"1 thread), {dt:.2f} s wall"}
+    # repeat the sort until about 10 s of CPU work (bounded: at most 8 calls)
+    calls, dt = 0, 0.0
+    while calls < 8 and (calls == 0 or dt < 10.0):
+        t0 = time.perf_counter()
+        oracle.sort(w.coder, w.units, w.offsets)
+        dt += time.perf_counter() - t0
+        calls += 1
+    return {"value": round(n_sample * calls / dt / 1e6, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{name} generator, n={n_sample} strings, {calls} oracle_sort calls (top-down merge sort, "
+                      f"1 thread), {dt:.2f} s wall in total"}
 
 
 def make_config(args, n, coder, world):
