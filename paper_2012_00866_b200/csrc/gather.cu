@@ -101,6 +101,25 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   const uint32_t tile = s_tile;
   const uint64_t p0 = (uint64_t)tile * kGatherTile + (uint64_t)tid * kGatherItems;
   GT(tile, 0);
+  if (CHECK && st && (st->trivial_mask == 0xFFu || st->msd_all_equal) && n > 1) {
+    // every code is equal: the whole array is one run, which the fix-up or the
+    // refinement (A6) reorders and gathers again -- gathering it here in code
+    // order would be thrown away (C4).  Unpack perm, record the run as dirty.
+    if (PACKED)
+      for (int j = 0; j < kGatherItems; ++j)
+        if (p0 + j < n) perm[p0 + j] &= 0x0FFFFFFFu;
+    if (tile == 0 && tid == 0) {
+      runs.run_start[0] = 0;
+      runs.run_end[0] = (uint32_t)(n - 1);
+      runs.dirty[0] = 1;
+      runs.st->n_runs = 1;
+      if (sorted_offsets) {  // the span's ends; the re-gather fills the inside
+        sorted_offsets[0] = (int64_t)gbase;
+        sorted_offsets[n] = (int64_t)gbase + (offsets[n] - offsets[0]);
+      }
+    }
+    return;
+  }
 
   // per item: len (units) and either the source offset or, for strings rebuilt
   // from their code, the code itself (bit j of `dec`)
