@@ -75,6 +75,7 @@ struct DevState {
   uint32_t np;
   uint32_t pass_digit[8];
   uint32_t pass_ballot[8];  // rank a pass with per-bit ballots instead of __match_any_sync
+  uint32_t digit_spread[8]; // k_hist_scan: digit d's largest bin holds < 5% of the keys
   unsigned long long sorted_keys;  // uint64_t* of the sorted keys
   // MSD key sort (msd.cu): OR and NOT-AND of all codes (fused into A1; zero-
   // initialised), segment-list fill counts and tile counts of the two level

@@ -31,14 +31,25 @@ namespace husky {
 
 // Exclusive scan of hist[d][0..255] -> digit_start[d]; trivial_mask bit d when
 // one digit value holds all n keys (that pass is the identity and is skipped).
+// Also digit_spread[d]: the largest bin holds < 5% of the keys (many distinct
+// labels per warp: rank that digit with per-bit ballots).
 __global__ void __launch_bounds__(256) k_hist_scan(uint64_t n, DevState *st) {
   __shared__ uint32_t wt[9];
+  __shared__ uint32_t s_max[8];
   const int d = blockIdx.x;
   uint32_t v = st->hist[d][threadIdx.x];
   uint32_t total;
   uint32_t ex = block_exclusive_scan<uint32_t, 256>(v, &total, wt);
   st->digit_start[d][threadIdx.x] = ex;
   if ((uint64_t)v == n) atomicOr(&st->trivial_mask, 1u << d);
+  const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, v);
+  if (lane_id() == 0) s_max[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t mx = 0;
+    for (int w = 0; w < 8; ++w) mx = s_max[w] > mx ? s_max[w] : mx;
+    st->digit_spread[d] = (uint64_t)mx * 20 < n;
+  }
 }
 
 void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s) {
@@ -69,27 +80,16 @@ constexpr int kExchangeBytes = kRadixTile * (8 + 4) + kRadixWarps * 256 * 4;
 
 // Device-side pass plan: lets the host launch all 8 pass slots without
 // reading the trivial-digit mask back (no host synchronisation).  Also picks
-// each pass's ranking primitive: a digit whose largest bin holds < 5% of the
-// keys (many distinct labels per warp) is ranked with per-bit ballots, the rest
-// with __match_any_sync -- measured per digit on C2 / C3.
-__global__ void __launch_bounds__(256) k_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint64_t n,
-                                                    uint32_t force_ballot, uint32_t force_match) {
-  __shared__ uint32_t s_max[8][8];
-  const uint32_t t = threadIdx.x, lane = lane_id(), warp = t >> 5;
-#pragma unroll
-  for (int d = 0; d < 8; ++d) {
-    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, st->hist[d][t]);
-    if (lane == 0) s_max[d][warp] = m;
-  }
-  __syncthreads();
-  if (t != 0) return;
+// each pass's ranking primitive from k_hist_scan's digit_spread: a digit whose
+// largest bin holds < 5% of the keys (many distinct labels per warp) is ranked
+// with per-bit ballots, the rest with __match_any_sync -- measured per digit on
+// C2 / C3.
+__global__ void k_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint32_t force_ballot,
+                             uint32_t force_match) {
   uint32_t m = st->trivial_mask, np = 0;
   for (int d = 0; d < 8; ++d)
     if (!((m >> d) & 1)) {
-      uint32_t mx = 0;
-      for (int w = 0; w < 8; ++w) mx = s_max[d][w] > mx ? s_max[d][w] : mx;
-      const bool spread = (uint64_t)mx * 20 < n;
-      st->pass_ballot[np] = ((force_ballot >> d) & 1) || (spread && !((force_match >> d) & 1));
+      st->pass_ballot[np] = ((force_ballot >> d) & 1) || (st->digit_spread[d] && !((force_match >> d) & 1));
       st->pass_digit[np++] = d;
     }
   st->np = np;
@@ -108,6 +108,7 @@ struct SlotPtrs {
   uint64_t *kA, *kB;
   const uint32_t *v_init;  // NULL: payload = index (synthesised by slot 0)
   uint32_t *v_final, *v_tmp;
+  const DevState *st;  // host-planned launches: digit_spread of the pass's digit
 };
 
 // One pass over one tile.  LOOKBACK: decoupled look-back on `lb` (onesweep);
@@ -122,7 +123,9 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
                const uint32_t *__restrict__ digit_start, unsigned long long *lb, uint32_t *tile_counter,
                uint32_t epoch, const uint32_t *__restrict__ prefix, uint32_t num_tiles, const DevState *plan,
                int slot, SlotPtrs sp) {
-  bool use_ballot = false;
+  // host-planned passes (refinement, multi-GPU partition): the digit's spread
+  // as measured by k_hist_scan; planned slots: the plan's choice
+  bool use_ballot = !plan && sp.st && sp.st->digit_spread[shift >> 3];
   if (plan) {
     const uint32_t np = plan->np;
     if ((uint32_t)slot >= np) return;
@@ -395,10 +398,10 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
   if (onesweep) {
     if (vals_in == nullptr)
       k_onesweep<true, true><<<g, b, kExchangeBytes, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds,
-                                                          lb, tile_counter, epoch, nullptr, tiles, nullptr, 0, SlotPtrs{});
+                                                          lb, tile_counter, epoch, nullptr, tiles, nullptr, 0, SlotPtrs{nullptr, nullptr, nullptr, nullptr, nullptr, st});
     else
       k_onesweep<false, true><<<g, b, kExchangeBytes, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds,
-                                                           lb, tile_counter, epoch, nullptr, tiles, nullptr, 0, SlotPtrs{});
+                                                           lb, tile_counter, epoch, nullptr, tiles, nullptr, 0, SlotPtrs{nullptr, nullptr, nullptr, nullptr, nullptr, st});
     return;
   }
   // reduce-then-scan: the look-back buffer (tiles*256 u64) holds counts[256][tiles] u32
@@ -407,10 +410,10 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
   k_rs_scan<<<256, 1024, 0, s>>>(counts, tiles, ds);
   if (vals_in == nullptr)
     k_onesweep<true, false><<<g, b, kExchangeBytes, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                         tile_counter, epoch, counts, tiles, nullptr, 0, SlotPtrs{});
+                                                         tile_counter, epoch, counts, tiles, nullptr, 0, SlotPtrs{nullptr, nullptr, nullptr, nullptr, nullptr, st});
   else
     k_onesweep<false, false><<<g, b, kExchangeBytes, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                          tile_counter, epoch, counts, tiles, nullptr, 0, SlotPtrs{});
+                                                          tile_counter, epoch, counts, tiles, nullptr, 0, SlotPtrs{nullptr, nullptr, nullptr, nullptr, nullptr, st});
 }
 
 void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint64_t n, cudaStream_t s) {
@@ -422,7 +425,7 @@ void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint64_t 
     return v ? (uint32_t)strtoul(v, nullptr, 0) : 0u;
   };
   static const uint32_t force_ballot = env_mask("HUSKY_RANK_BALLOT"), force_match = env_mask("HUSKY_RANK_MATCH");
-  k_radix_plan<<<1, 256, 0, s>>>(st, keysA, keysB, n, force_ballot, force_match);
+  k_radix_plan<<<1, 1, 0, s>>>(st, keysA, keysB, force_ballot, force_match);
 }
 
 // Pass slot `slot` (0..7) of the device-side plan, onesweep variant.  Launched
@@ -439,7 +442,7 @@ void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint
   }
   Scope sc_(ST_RADIX, s, n);
   const uint32_t tiles = (uint32_t)radix_tiles(n);
-  SlotPtrs sp{keysA, keysB, vals_init, vals_final, vals_tmp};
+  SlotPtrs sp{keysA, keysB, vals_init, vals_final, vals_tmp, nullptr};
   static const bool rts = [] {
     const char *v = getenv("HUSKY_RADIX");
     return v && v[0] == 'r';
