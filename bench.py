@@ -309,7 +309,7 @@ def run_ours(args):
 
     # ---- end to end through the C ABI with HOST buffers (H2D/D2H inside the timed region)
     e2e = None
-    if world == 1:
+    if world == 1 and not args.force_multi:
         hu = torch.from_numpy(np.ascontiguousarray(units_np)).pin_memory()
         ho = torch.from_numpy(w.offsets).pin_memory()
         hp = torch.empty(n, dtype=torch.int32).pin_memory()
@@ -358,6 +358,50 @@ def run_ours(args):
                "api": f"husky_sort_host_many: {args.steps} steps as {args.steps} pipelined batches on {depth} "
                       "workers (pinned host buffers), host wall clock around the call",
                "single_call": single}
+    elif world > 1 or args.force_multi:
+        # sharded: every step copies the rank's input block from pinned host
+        # memory, runs the sample sort, and reads its output shard back; time =
+        # max over ranks of the CUDA-event time on the current stream
+        hu = torch.from_numpy(np.ascontiguousarray(units_np)).pin_memory()
+        ho = torch.from_numpy(w.offsets).pin_memory()
+        du = torch.empty_like(d_units)
+        do = torch.empty_like(d_off)
+        # shard sizes vary with the splitters: pinned output buffers with slack
+        p0, su0, so0, _ = h.sort_multi(comm, w.coder, d_units, d_off, gbase)
+        cap_n, cap_u = 2 * max(p0.numel(), n) + 1024, 2 * max(su0.numel(), total_units) + 1024
+        hp = torch.empty(cap_n, dtype=torch.int32).pin_memory()
+        hsu = torch.empty(cap_u, dtype=d_units.dtype).pin_memory()
+        hso = torch.empty(cap_n + 1, dtype=torch.int64).pin_memory()
+        e_ms, h2d, d2h = 0.0, 0, 0
+        for i in range(args.steps + max(1, args.warmup)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a.record(stream)
+            du.copy_(hu, non_blocking=True)
+            do.copy_(ho, non_blocking=True)
+            perm_s, su_s, so_s, _ = h.sort_multi(comm, w.coder, du, do, gbase)
+            k, ku = perm_s.numel(), su_s.numel()
+            hp[:k].copy_(perm_s, non_blocking=True)
+            hsu[:ku].copy_(su_s, non_blocking=True)
+            hso[:so_s.numel()].copy_(so_s, non_blocking=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i < max(1, args.warmup):
+                continue  # warm-up (first use of these buffers by the exchange)
+            e_ms += a.elapsed_time(b)
+            h2d = hu.numel() * hu.element_size() + ho.numel() * 8
+            d2h = k * 4 + ku * su_s.element_size() + so_s.numel() * 8
+        e_ms /= args.steps
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": round(world * n / (e_ms * 1e-3) / 1e6, 4), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_ms, 3),
+               "api": "husky_sort_multi per rank: pinned host block -> device, sample sort, shard -> pinned host "
+                      "(bytes of rank 0; time = max over ranks)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
