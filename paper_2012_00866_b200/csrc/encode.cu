@@ -179,13 +179,15 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
   }
 }
 
-// The 8 x 256 digit histograms of the codes for the LSD onesweep (A2): one
-// read of the codes, plain shared-memory atomics.  Measured on C2: 35 us as a
+// The 8 digit histograms (kSlotBits-bit digits) of the codes for the LSD
+// onesweep (A2): one read of the codes, plain shared-memory atomics.  Measured on C2: 35 us as a
 // separate pass vs 51 us when fused into the encoder's loop, and 8x slower with
 // __match_any_sync aggregation.
-__global__ void __launch_bounds__(512) k_hist8(const uint64_t *__restrict__ keys, uint64_t n, DevState *st) {
-  __shared__ uint32_t h[8 * 256];
-  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) h[i] = 0;
+__global__ void __launch_bounds__(512) k_hist_slots(const uint64_t *__restrict__ keys, uint64_t n, DevState *st) {
+  constexpr int R = 1 << kSlotBits;
+  constexpr uint32_t M = R - 1;
+  __shared__ uint32_t h[8 * R];
+  for (int i = threadIdx.x; i < 8 * R; i += blockDim.x) h[i] = 0;
   __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * 4; base < n; base += stride) {
@@ -199,13 +201,12 @@ __global__ void __launch_bounds__(512) k_hist8(const uint64_t *__restrict__ keys
     for (int r = 0; r < 4; ++r) {
       if (base + threadIdx.x + (uint64_t)r * blockDim.x >= n) continue;
 #pragma unroll
-      for (int d = 0; d < 8; ++d) atomicAdd(&h[d * 256 + ((uint32_t)(k[r] >> (8 * d)) & 0xFF)], 1u);
+      for (int d = 0; d < 8; ++d) atomicAdd(&h[d * R + ((uint32_t)(k[r] >> (kSlotBits * d)) & M)], 1u);
     }
   }
   __syncthreads();
-  uint32_t *g = &st->hist[0][0];
-  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
-    if (h[i]) atomicAdd(g + i, h[i]);
+  for (int i = threadIdx.x; i < 8 * R; i += blockDim.x)
+    if (h[i]) atomicAdd(&st->hist[i / R][i % R], h[i]);
 }
 
 void launch_encode(int coder, bool hist, const void *units, const int64_t *offsets, uint64_t n,
@@ -231,14 +232,14 @@ void launch_encode(int coder, bool hist, const void *units, const int64_t *offse
         break;
     }
   }
-  if (hist) launch_hist8(codes, n, st, num_sms, s);
+  if (hist) launch_hist_slots(codes, n, st, num_sms, s);
 }
 
-void launch_hist8(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s) {
+void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s) {
   if (n == 0) return;
   Scope sc_(ST_HIST_SCAN, s, n);
   const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * 2);
-  k_hist8<<<(unsigned)blocks, 512, 0, s>>>(keys, n, st);
+  k_hist_slots<<<(unsigned)blocks, 512, 0, s>>>(keys, n, st);
 }
 
 }  // namespace husky

@@ -236,9 +236,8 @@ __global__ void __launch_bounds__(256)
     }
   }
   __syncthreads();
-  uint32_t *g = &st->hist[0][0];
   for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
-    if (sh_hist[i]) atomicAdd(g + i, sh_hist[i]);
+    if (sh_hist[i]) atomicAdd(&st->hist[i >> 8][i & 255], sh_hist[i]);
 }
 
 void launch_seg_key2(int coder, const uint32_t *perm_seg, uint64_t len, const void *units,

@@ -32,24 +32,6 @@ __device__ __forceinline__ unsigned long long gt_now() {
 #define GT(tile, i) do { } while (0)
 #endif
 
-// Byte b of a string whose units are fully determined by its husky code (ASCII
-// length <= 9, UNICODE length <= 3): the inverse of Alg. 4's packing.
-template <int CODER>
-__device__ __forceinline__ uint8_t decode_byte(uint64_t code, int b) {
-  if (CODER == HUSKY_CODER_ASCII) return (uint8_t)((code >> (56 - 7 * b)) & 0x7F);
-  uint32_t u = (uint32_t)(((code << 1) >> (48 - 16 * (b >> 1))) & 0xFFFF);
-  return (uint8_t)(b & 1 ? u >> 8 : u);
-}
-
-// 8 bytes at an arbitrary byte offset of the stage (little-endian), from three
-// aligned 32-bit words (the stage has 32 bytes of slack past its end)
-__device__ __forceinline__ uint64_t stage_load8(const uint8_t *stage, uint32_t off) {
-  const uint32_t *sw = reinterpret_cast<const uint32_t *>(stage) + (off >> 2);
-  const uint32_t sh = (off & 3) * 8;
-  const uint32_t x0 = sw[0], x1 = sw[1], x2 = sw[2];
-  return (uint64_t)__funnelshift_r(x0, x1, sh) | ((uint64_t)__funnelshift_r(x1, x2, sh) << 32);
-}
-
 // PACKED: perm holds index | min(len,15) << 28 (written by the encoder, carried
 // through the radix as the payload).  Strings whose length is <= PL are then
 // rebuilt from their sorted code (sequential reads only); perm is unpacked in

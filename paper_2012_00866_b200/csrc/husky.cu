@@ -226,8 +226,8 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
       GroupScope grp(ST_ENCODE, s);
       launch_encode(coder, false, d_units, d_offsets, n, S.keysA(), st, S.sms, s, packed_payload);
     }
-    launch_hist8(S.keysA(), n, st, S.sms, s);
-    launch_hist_scan(n, st, s);
+    launch_hist_slots(S.keysA(), n, st, S.sms, s);
+    launch_hist_scan(n, st, s, kSlotBits);
 
     // ---- A2 key sort, LSD onesweep: (code, index) -> sorted codes, perm.  The
     // pass plan (which digits are not shared by all keys) is made on device, so

@@ -56,10 +56,26 @@ constexpr uint32_t kNotPerfect = 1u, kDomainBad = 2u, kOffsetsBad = 4u;
 constexpr uint32_t kNotLower = 8u, kNotUpper = 16u;
 
 // ------------------------------------------------------ device-resident state
+// Digit width of the device-planned passes (the main key sort).  9-bit digits
+// cover the 63 bits every husky code uses (9 x 7, 4 x 16 >>> 1,
+// 12 x 5, 10 x 6) in 7 passes instead of 8 (digit 7 is then bit 63 alone), but
+// each 512-bin pass measured ~14% slower, so the sort time came out equal on
+// C2-C4; 8 stays the default.  Host-planned passes (A6 re-key,
+// multi-GPU partition) always use 8-bit digits.  hist / digit_start rows hold
+// kMaxBins entries either way.
+#ifndef HUSKY_SLOT_BITS
+#define HUSKY_SLOT_BITS 8
+#endif
+constexpr int kSlotBits = HUSKY_SLOT_BITS;
+constexpr int kMaxBins = 512;
+static_assert(kSlotBits == 8 || kSlotBits == 9, "slot digits are 8 or 9 bits");
 // Lives at the start of the caller's workspace; zeroed once per husky_sort.
 struct DevState {
-  uint32_t hist[8][256];      // digit histograms of the 64-bit keys (A1 / A6 re-key)
-  uint32_t digit_start[8][256];
+  // digit histograms of the 64-bit keys: rows of kMaxBins; the device-planned
+  // passes use 9-bit digits (512 bins), the host-planned ones (A6 re-key,
+  // multi-GPU partition) 8-bit digits in the first 256 bins of each row
+  uint32_t hist[8][kMaxBins];
+  uint32_t digit_start[8][kMaxBins];
   uint32_t trivial_mask;      // bit d: all keys share digit d
   uint32_t violations;        // kNotPerfect | kDomainBad | kOffsetsBad
   uint32_t tile_counter[64];  // dynamic tile ids, one per launch slot
@@ -102,10 +118,11 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 // Lanes holding the same 8-bit label as this lane (converged warp): one ballot
 // per label bit -- an alternative to __match_any_sync whose cost on sm_100a
 // depends on the label distribution.
-__device__ __forceinline__ uint32_t match_ballot8(uint32_t label) {
+template <int BITS>
+__device__ __forceinline__ uint32_t match_ballot(uint32_t label) {
   uint32_t m = 0xFFFFFFFFu;
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
+  for (int b = 0; b < BITS; ++b) {
     const bool bit = (label >> b) & 1u;
     const uint32_t v = __ballot_sync(0xFFFFFFFFu, bit);
     m &= bit ? v : ~v;
@@ -319,6 +336,24 @@ __device__ __forceinline__ int cmp_units_from(const void *units, int64_t oa, int
   }
   if (la != lb) return la < lb ? -1 : 1;
   return 0;
+}
+
+// Byte b of a string whose units are fully determined by its husky code (ASCII
+// length <= 9, UNICODE length <= 3): the inverse of Alg. 4's packing.
+template <int CODER>
+__device__ __forceinline__ uint8_t decode_byte(uint64_t code, int b) {
+  if (CODER == HUSKY_CODER_ASCII) return (uint8_t)((code >> (56 - 7 * b)) & 0x7F);
+  uint32_t u = (uint32_t)(((code << 1) >> (48 - 16 * (b >> 1))) & 0xFFFF);
+  return (uint8_t)(b & 1 ? u >> 8 : u);
+}
+
+// 8 bytes at an arbitrary byte offset of the stage (little-endian), from three
+// aligned 32-bit words (the stage has 32 bytes of slack past its end)
+__device__ __forceinline__ uint64_t stage_load8(const uint8_t *stage, uint32_t off) {
+  const uint32_t *sw = reinterpret_cast<const uint32_t *>(stage) + (off >> 2);
+  const uint32_t sh = (off & 3) * 8;
+  const uint32_t x0 = sw[0], x1 = sw[1], x2 = sw[2];
+  return (uint64_t)__funnelshift_r(x0, x1, sh) | ((uint64_t)__funnelshift_r(x1, x2, sh) << 32);
 }
 
 // Exact comparator with no assumption on the codes (general cleanup, NEXT-4):

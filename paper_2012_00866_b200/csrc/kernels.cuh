@@ -17,8 +17,8 @@ constexpr int kEncThreads = 256, kEncBlocksPerSM = 8;
 constexpr uint64_t kPackMaxN = 1ull << 28;
 void launch_encode(int coder, bool hist, const void *units, const int64_t *offsets, uint64_t n,
                    uint64_t *codes, DevState *st, int num_sms, cudaStream_t s, uint32_t *packed = nullptr);
-// 8 x 256 digit histograms of n keys into DevState::hist (accumulates)
-void launch_hist8(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s);
+// 8 digit histograms (kSlotBits-bit digits) of n keys into DevState::hist (accumulates)
+void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s);
 
 // A2 onesweep radix
 // 512 threads x 8 keys = 4096-key tiles, 64 KB smem, <= 64 registers -> 2 CTAs
@@ -29,18 +29,19 @@ void launch_hist8(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, c
 constexpr int kRadixThreads = 512, kRadixItems = 8, kRadixTile = kRadixThreads * kRadixItems;
 constexpr int kRadixMinBlocks = 2;
 inline uint64_t radix_tiles(uint64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
-// look-back words are stored transposed, [digit][tile], rows of an even length
-// (16-byte aligned pair loads); the buffer holds 256 rows
+// look-back words: one per (tile, digit), tile-major, up to kMaxBins per tile
 inline uint64_t radix_lb_stride(uint64_t n) { return (radix_tiles(n) + 1) & ~1ull; }
-inline uint64_t radix_lb_words(uint64_t n) { return radix_lb_stride(n) * 256 + 2; }
-void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s);
+inline uint64_t radix_lb_words(uint64_t n) { return radix_lb_stride(n) * kMaxBins + 2; }
+// exclusive scans of DevState::hist -> digit_start, trivial_mask, digit_spread
+// for `bits`-bit digits (8: host-planned passes; kSlotBits: the slots)
+void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s, int bits = 8);
 // One stable LSD pass on digit `digit` (bits 8*digit..8*digit+7).  vals_in == NULL
 // synthesises payload = index.  lb: radix_tiles(n)*256 look-back words.
 void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,
                      uint32_t *vals_out, uint64_t n, int digit, DevState *st,
                      unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
 void launch_iota(uint32_t *perm, uint64_t n, cudaStream_t s);
-// Device-planned passes (no host sync): k_radix_plan turns the trivial-digit
+// Device-planned passes (kSlotBits-bit digits, no host sync): k_radix_plan turns the trivial-digit
 // mask into DevState::np / pass_digit / sorted_keys; slots 0..7 are launched
 // unconditionally and resolve their digit and ping-pong buffers on device (the
 // last planned pass writes vals_final); finalize copies the payload when np == 0.

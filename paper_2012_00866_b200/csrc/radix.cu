@@ -3,22 +3,25 @@
 // Role in the paper: step 2 of Alg. 1, "Sort array longs ... in such a way that
 // when elements i, j of longs are exchanged, then elements i, j of xs are also
 // exchanged".  Introsort's comparisons are replaced
-// by an 8-bit-digit LSD radix sort whose payload is the string index, so the
-// co-swap is the payload scatter.  Being stable, it leaves equal codes in index
-// order (R7), which the fix-up (A5) relies on.
+// by an LSD radix sort whose payload is the string index, so the co-swap is the
+// payload scatter.  Being stable, it leaves equal codes in index order
+// (R7), which the fix-up (A5) relies on.
 //
-// A pass (one 8-bit digit) works on tiles of 4096 keys (512 threads x 8,
-// warp-striped so every load/store instruction is a coalesced 256-B access).
-// Each tile is ranked in shared memory with warp-level label matching
-// (__match_any_sync, or per-bit ballots when the plan says the digit is spread
-// out) + popc into per-warp digit counters, exchanged through shared memory
-// into digit order, and written out as runs of consecutive addresses.  The
-// tile's global base per digit comes from one of two schemes:
+// Digit width: 8 bits (kernels are templated on it; the device-planned slots
+// can be built with 9-bit digits, HUSKY_SLOT_BITS=9: 7 passes for the 63-bit
+// codes, measured no faster -- husky_internal.cuh).
+// A pass works on tiles of 4096 keys (512 threads x 8, warp-striped so every
+// load/store instruction is a coalesced 256-B access).  Each tile is ranked in
+// shared memory with warp-level label matching (__match_any_sync, or per-bit
+// ballots when the plan says the digit is spread out) + popc into per-warp
+// digit counters, exchanged through shared memory into digit order, and written
+// out as runs of consecutive addresses.  The tile's global base per digit comes
+// from one of two schemes:
 //   * onesweep (default): per-(tile, digit) decoupled look-back (Adinets &
-//     Merrill), global digit starts from the 8 x 256 histograms of the codes
-//     (k_hist8).  One read of the keys per pass, but the look-back is a chain of
-//     dependent L2 round trips (~1 us each with the memory system saturated;
-//     measured per-tile phases in DESIGN.md).
+//     Merrill), global digit starts from the 8 digit histograms of the codes
+//     (k_hist_slots).  One read of the keys per pass, but the look-back is a
+//     chain of dependent L2 round trips (~1 us each with the memory system
+//     saturated; measured per-tile phases in DESIGN.md).
 //   * reduce-then-scan (HUSKY_RADIX=rts, host-planned passes only): an upsweep
 //     writes each tile's digit counts (8 B/key read), a digit-parallel scan
 //     turns them into per-tile bases, and the downsweep ranks/exchanges/scatters
@@ -33,13 +36,15 @@ namespace husky {
 // one digit value holds all n keys (that pass is the identity and is skipped).
 // Also digit_spread[d]: the largest bin holds < 5% of the keys (many distinct
 // labels per warp: rank that digit with per-bit ballots).
-__global__ void __launch_bounds__(256) k_hist_scan(uint64_t n, DevState *st) {
-  __shared__ uint32_t wt[9];
-  __shared__ uint32_t s_max[8];
+template <int BITS>
+__global__ void __launch_bounds__(1 << BITS) k_hist_scan(uint64_t n, DevState *st) {
+  constexpr int R = 1 << BITS;
+  __shared__ uint32_t wt[R / 32 + 1];
+  __shared__ uint32_t s_max[R / 32];
   const int d = blockIdx.x;
   uint32_t v = st->hist[d][threadIdx.x];
   uint32_t total;
-  uint32_t ex = block_exclusive_scan<uint32_t, 256>(v, &total, wt);
+  uint32_t ex = block_exclusive_scan<uint32_t, R>(v, &total, wt);
   st->digit_start[d][threadIdx.x] = ex;
   if ((uint64_t)v == n) atomicOr(&st->trivial_mask, 1u << d);
   const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, v);
@@ -47,14 +52,15 @@ __global__ void __launch_bounds__(256) k_hist_scan(uint64_t n, DevState *st) {
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t mx = 0;
-    for (int w = 0; w < 8; ++w) mx = s_max[w] > mx ? s_max[w] : mx;
+    for (int w = 0; w < R / 32; ++w) mx = s_max[w] > mx ? s_max[w] : mx;
     st->digit_spread[d] = (uint64_t)mx * 20 < n;
   }
 }
 
-void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s) {
+void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s, int bits) {
   Scope sc_(ST_HIST_SCAN, s, n);
-  k_hist_scan<<<8, 256, 0, s>>>(n, st);
+  if (bits == 9) k_hist_scan<9><<<8, 512, 0, s>>>(n, st);
+  else k_hist_scan<8><<<8, 256, 0, s>>>(n, st);
 }
 
 constexpr int kRadixWarps = kRadixThreads / 32;
@@ -76,7 +82,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #else
 #define HT(tile, i) do { } while (0)
 #endif
-constexpr int kExchangeBytes = kRadixTile * (8 + 4) + kRadixWarps * 256 * 4;
+// dynamic smem of a pass: key/value exchange buffer + per-warp digit counters
+template <int BITS>
+constexpr int exchange_bytes() { return kRadixTile * (8 + 4) + kRadixWarps * (1 << BITS) * 4; }
 
 // Device-side pass plan: lets the host launch all 8 pass slots without
 // reading the trivial-digit mask back (no host synchronisation).  Also picks
@@ -116,7 +124,7 @@ struct SlotPtrs {
 // written by k_rs_scan) and nothing waits on other tiles.  plan != NULL: this
 // is pass slot `slot` of the device-side plan (buffers, digit resolved here;
 // slots beyond the plan exit at once).
-template <bool SYNTH_VALS, bool LOOKBACK>
+template <bool SYNTH_VALS, bool LOOKBACK, int BITS>
 __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     k_onesweep(const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint64_t n, int shift,
@@ -125,13 +133,15 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
                int slot, SlotPtrs sp) {
   // host-planned passes (refinement, multi-GPU partition): the digit's spread
   // as measured by k_hist_scan; planned slots: the plan's choice
-  bool use_ballot = !plan && sp.st && sp.st->digit_spread[shift >> 3];
+  constexpr uint32_t R = 1u << BITS, MASK = R - 1;
+  static_assert(R <= kRadixThreads, "one digit per thread");
+  bool use_ballot = !plan && sp.st && sp.st->digit_spread[shift / BITS];
   if (plan) {
     const uint32_t np = plan->np;
     if ((uint32_t)slot >= np) return;
     const uint32_t digit = plan->pass_digit[slot];
     use_ballot = plan->pass_ballot[slot] != 0;
-    shift = 8 * digit;
+    shift = BITS * digit;
     digit_start = plan->digit_start[digit];
     keys_in = (slot & 1) ? sp.kB : sp.kA;
     keys_out = (slot & 1) ? sp.kA : sp.kB;
@@ -139,20 +149,20 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     vals_out = ((np - 1 - slot) & 1) == 0 ? sp.v_final : sp.v_tmp;
   }
   extern __shared__ __align__(16) uint8_t smem[];
-  // key/value exchange buffer, then per-warp digit counters [warps][256]
+  // key/value exchange buffer, then per-warp digit counters [warps][R]
   uint64_t *xk = reinterpret_cast<uint64_t *>(smem);
   uint32_t *xv = reinterpret_cast<uint32_t *>(smem + kRadixTile * 8);
   uint32_t *cnt = reinterpret_cast<uint32_t *>(smem + kRadixTile * 12);
   __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_local_start[256];
-  __shared__ uint32_t s_gbase[256];
+  __shared__ uint32_t s_local_start[R];
+  __shared__ uint32_t s_gbase[R];
   __shared__ uint32_t s_wt[kRadixWarps + 1];
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   if (LOOKBACK) {  // dynamic tile ids: every predecessor a tile waits on is resident
     if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   }
-  for (int i = tid; i < kRadixWarps * 256; i += kRadixThreads) cnt[i] = 0;
+  for (int i = tid; i < kRadixWarps * (int)R; i += kRadixThreads) cnt[i] = 0;
   __syncthreads();
   const uint32_t tile = LOOKBACK ? s_tile : blockIdx.x;
   const uint64_t tile_base = (uint64_t)tile * kRadixTile;
@@ -168,23 +178,23 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
       k[r] = __ldg(keys_in + idx);
       v[r] = SYNTH_VALS ? (uint32_t)idx : __ldg(vals_in + idx);
     } else {
-      k[r] = ~0ull;  // ranks last in digit 255; never stored
+      k[r] = ~0ull;  // ranks last (the largest digit value at this shift); never stored
       v[r] = 0;
     }
   }
   // ---- the tile's bases (reduce-then-scan): independent of everything above
-  const bool is_dg = tid < 256;  // threads 0..255 own one digit each
-  const uint32_t dg = tid & 255;
+  const bool is_dg = tid < R;  // threads 0..R-1 own one digit each
+  const uint32_t dg = tid & MASK;
   uint32_t pre_base = 0;
   if (!LOOKBACK && is_dg) pre_base = __ldg(prefix + (uint64_t)dg * num_tiles + tile);
 
   // ---- warp-level match ranking into per-warp counters (stable: (r, lane) order)
-  uint32_t *wc = cnt + warp * 256;
+  uint32_t *wc = cnt + warp * R;
   uint32_t rank[kRadixItems];
 #pragma unroll
   for (int r = 0; r < kRadixItems; ++r) {
-    uint32_t d = (uint32_t)(k[r] >> shift) & 0xFF;
-    uint32_t peers = use_ballot ? match_ballot8(d) : __match_any_sync(0xFFFFFFFFu, d);
+    uint32_t d = (uint32_t)(k[r] >> shift) & MASK;
+    uint32_t peers = use_ballot ? match_ballot<BITS>(d) : __match_any_sync(0xFFFFFFFFu, d);
     if (r == 0) HT(tile, 1);
     uint32_t pre = wc[d];
     rank[r] = pre + __popc(peers & lanemask_lt());
@@ -201,14 +211,15 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   if (is_dg) {
 #pragma unroll
     for (int w = 0; w < kRadixWarps; ++w) {
-      uint32_t c = cnt[w * 256 + dg];
-      cnt[w * 256 + dg] = tot;
+      uint32_t c = cnt[w * R + dg];
+      cnt[w * R + dg] = tot;
       tot += c;
     }
   }
   uint64_t tile_end = tile_base + kRadixTile;
-  if (is_dg && dg == 255 && tile_end > n) tot -= (uint32_t)(tile_end - n);  // padding keys
-  unsigned long long *my_flag = lb + (uint64_t)tile * 256 + dg;
+  const uint32_t pad_dg = (uint32_t)(~0ull >> shift) & MASK;  // the padding keys' digit
+  if (is_dg && dg == pad_dg && tile_end > n) tot -= (uint32_t)(tile_end - n);
+  unsigned long long *my_flag = lb + (uint64_t)tile * R + dg;
   if (LOOKBACK && is_dg) {
     if (tile == 0) st_relaxed_u64(my_flag, make_flag(kFlagInc, epoch, (unsigned long long)digit_start[dg] + tot));
     else st_relaxed_u64(my_flag, make_flag(kFlagAgg, epoch, tot));
@@ -222,7 +233,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   // ---- exchange through shared memory into tile-local digit order
 #pragma unroll
   for (int r = 0; r < kRadixItems; ++r) {
-    uint32_t d = (uint32_t)(k[r] >> shift) & 0xFF;
+    uint32_t d = (uint32_t)(k[r] >> shift) & MASK;
     uint32_t pos = s_local_start[d] + wc[d] + rank[r];
     xk[pos] = k[r];
     xv[pos] = v[r];
@@ -235,10 +246,10 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
 #ifdef HUSKY_TIMING
       uint32_t lbst[2] = {0, 0};
       excl = tile == 0 ? (unsigned long long)digit_start[dg]
-                       : lookback_window<RADIX_LB_W>(lb + dg, tile, 256, epoch, lbst);
+                       : lookback_window<RADIX_LB_W>(lb + dg, tile, R, epoch, lbst);
       if (tid == 0 && tile < kTimingTiles) g_tile_times[tile][7] = lbst[0] | ((unsigned long long)lbst[1] << 32);
 #else
-      excl = tile == 0 ? (unsigned long long)digit_start[dg] : lookback_window<RADIX_LB_W>(lb + dg, tile, 256, epoch);
+      excl = tile == 0 ? (unsigned long long)digit_start[dg] : lookback_window<RADIX_LB_W>(lb + dg, tile, R, epoch);
 #endif
       if (tile != 0) st_relaxed_u64(my_flag, make_flag(kFlagInc, epoch, excl + tot));
     } else {
@@ -255,7 +266,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
 #pragma unroll 4
   for (uint32_t i = tid; i < n_valid; i += kRadixThreads) {
     uint64_t key = xk[i];
-    uint32_t d = (uint32_t)(key >> shift) & 0xFF;
+    uint32_t d = (uint32_t)(key >> shift) & MASK;
     uint32_t g = s_gbase[d] + i;
     keys_out[g] = key;
     vals_out[g] = xv[i];
@@ -312,55 +323,6 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
-// Reduce-then-scan for a device-planned pass slot (HUSKY_RADIX=rts): per-tile
-// counts of the slot's digit with plain shared-memory atomics (warp-private
-// copies), then a digit-parallel scan turns them into per-tile bases; the
-// downsweep is k_onesweep<.., false>, which waits on nothing.
-__global__ void __launch_bounds__(256)
-    k_rs_upsweep_slot(const DevState *plan, int slot, const uint64_t *kA, const uint64_t *kB, uint64_t n,
-                      uint32_t *__restrict__ counts, uint32_t num_tiles) {
-  if ((uint32_t)slot >= plan->np) return;
-  __shared__ uint32_t h[8][256];
-  const uint32_t tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < 8 * 256; i += 256) (&h[0][0])[i] = 0;
-  __syncthreads();
-  const int shift = 8 * (int)plan->pass_digit[slot];
-  const uint64_t *keys = (slot & 1) ? kB : kA;
-  const uint32_t tile = blockIdx.x;
-  const uint64_t tb = (uint64_t)tile * kRadixTile;
-  uint64_t k[kRadixTile / 256];
-#pragma unroll
-  for (int r = 0; r < kRadixTile / 256; ++r) {
-    const uint64_t i = tb + r * 256 + tid;
-    k[r] = i < n ? __ldg(keys + i) : 0;
-  }
-#pragma unroll
-  for (int r = 0; r < kRadixTile / 256; ++r)
-    if (tb + r * 256 + tid < n) atomicAdd(&h[warp][(uint32_t)(k[r] >> shift) & 0xFF], 1u);
-  __syncthreads();
-  uint32_t c = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) c += h[w][tid];
-  counts[(uint64_t)tid * num_tiles + tile] = c;
-}
-
-__global__ void __launch_bounds__(1024)
-    k_rs_scan_slot(const DevState *plan, int slot, uint32_t *__restrict__ counts, uint32_t num_tiles) {
-  if ((uint32_t)slot >= plan->np) return;
-  __shared__ uint32_t wt[33];
-  uint32_t *row = counts + (uint64_t)blockIdx.x * num_tiles;
-  uint32_t running = plan->digit_start[plan->pass_digit[slot]][blockIdx.x];
-  for (uint32_t c = 0; c < num_tiles; c += 1024) {
-    uint32_t i = c + threadIdx.x;
-    uint32_t v = i < num_tiles ? row[i] : 0u;
-    uint32_t total;
-    uint32_t ex = block_exclusive_scan<uint32_t, 1024>(v, &total, wt);
-    if (i < num_tiles) row[i] = running + ex;
-    running += total;
-    __syncthreads();
-  }
-}
-
 // instrumented builds: copy the per-tile phase timestamps of the last pass
 extern "C" int husky_debug_tile_times(unsigned long long *out, int max_tiles) {
 #ifdef HUSKY_TIMING
@@ -379,12 +341,13 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
                      uint32_t *vals_out, uint64_t n, int digit, DevState *st,
                      unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s) {
   if (n == 0) return;
+  constexpr int kX = exchange_bytes<8>();
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_onesweep<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
-    cudaFuncSetAttribute(k_onesweep<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
-    cudaFuncSetAttribute(k_onesweep<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
-    cudaFuncSetAttribute(k_onesweep<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
+    cudaFuncSetAttribute(k_onesweep<true, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
+    cudaFuncSetAttribute(k_onesweep<false, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
+    cudaFuncSetAttribute(k_onesweep<true, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
+    cudaFuncSetAttribute(k_onesweep<false, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
     configured = true;
   }
   static const bool onesweep = [] {
@@ -394,14 +357,15 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
   Scope sc_(ST_RADIX, s, n);
   const uint32_t *ds = st->digit_start[digit];
   const uint32_t tiles = (uint32_t)radix_tiles(n);
+  const SlotPtrs sp{nullptr, nullptr, nullptr, nullptr, nullptr, st};
   dim3 g(tiles), b(kRadixThreads);
   if (onesweep) {
     if (vals_in == nullptr)
-      k_onesweep<true, true><<<g, b, kExchangeBytes, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds,
-                                                          lb, tile_counter, epoch, nullptr, tiles, nullptr, 0, SlotPtrs{nullptr, nullptr, nullptr, nullptr, nullptr, st});
+      k_onesweep<true, true, 8><<<g, b, kX, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds, lb,
+                                                 tile_counter, epoch, nullptr, tiles, nullptr, 0, sp);
     else
-      k_onesweep<false, true><<<g, b, kExchangeBytes, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds,
-                                                           lb, tile_counter, epoch, nullptr, tiles, nullptr, 0, SlotPtrs{nullptr, nullptr, nullptr, nullptr, nullptr, st});
+      k_onesweep<false, true, 8><<<g, b, kX, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds, lb,
+                                                  tile_counter, epoch, nullptr, tiles, nullptr, 0, sp);
     return;
   }
   // reduce-then-scan: the look-back buffer (tiles*256 u64) holds counts[256][tiles] u32
@@ -409,11 +373,11 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
   k_rs_upsweep<<<tiles, kUpThreads, 0, s>>>(keys_in, n, 8 * digit, counts, tiles);
   k_rs_scan<<<256, 1024, 0, s>>>(counts, tiles, ds);
   if (vals_in == nullptr)
-    k_onesweep<true, false><<<g, b, kExchangeBytes, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                         tile_counter, epoch, counts, tiles, nullptr, 0, SlotPtrs{nullptr, nullptr, nullptr, nullptr, nullptr, st});
+    k_onesweep<true, false, 8><<<g, b, kX, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds, lb,
+                                                tile_counter, epoch, counts, tiles, nullptr, 0, sp);
   else
-    k_onesweep<false, false><<<g, b, kExchangeBytes, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                          tile_counter, epoch, counts, tiles, nullptr, 0, SlotPtrs{nullptr, nullptr, nullptr, nullptr, nullptr, st});
+    k_onesweep<false, false, 8><<<g, b, kX, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds, lb,
+                                                 tile_counter, epoch, counts, tiles, nullptr, 0, sp);
 }
 
 void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint64_t n, cudaStream_t s) {
@@ -428,48 +392,27 @@ void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint64_t 
   k_radix_plan<<<1, 1, 0, s>>>(st, keysA, keysB, force_ballot, force_match);
 }
 
-// Pass slot `slot` (0..7) of the device-side plan, onesweep variant.  Launched
-// unconditionally; the kernel resolves digit and buffers from DevState.
+// Pass slot `slot` (0..7) of the device-side plan (kSlotBits-bit digits).
+// Launched unconditionally; the kernel resolves digit and buffers from DevState.
 void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint32_t *vals_init,
                           uint32_t *vals_final, uint32_t *vals_tmp, uint64_t n, DevState *st,
                           unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s) {
   if (n == 0) return;
+  constexpr int kX = exchange_bytes<kSlotBits>();
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_onesweep<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
-    cudaFuncSetAttribute(k_onesweep<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
+    cudaFuncSetAttribute(k_onesweep<true, true, kSlotBits>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
+    cudaFuncSetAttribute(k_onesweep<false, true, kSlotBits>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
     configured = true;
   }
   Scope sc_(ST_RADIX, s, n);
   const uint32_t tiles = (uint32_t)radix_tiles(n);
   SlotPtrs sp{keysA, keysB, vals_init, vals_final, vals_tmp, nullptr};
-  static const bool rts = [] {
-    const char *v = getenv("HUSKY_RADIX");
-    return v && v[0] == 'r';
-  }();
-  if (rts) {
-    static bool cfg2 = false;
-    if (!cfg2) {
-      cudaFuncSetAttribute(k_onesweep<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
-      cudaFuncSetAttribute(k_onesweep<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExchangeBytes);
-      cfg2 = true;
-    }
-    uint32_t *counts = reinterpret_cast<uint32_t *>(lb);  // 256 x tiles u32 (the look-back words are unused)
-    k_rs_upsweep_slot<<<tiles, 256, 0, s>>>(st, slot, keysA, keysB, n, counts, tiles);
-    k_rs_scan_slot<<<256, 1024, 0, s>>>(st, slot, counts, tiles);
-    if (slot == 0 && vals_init == nullptr)
-      k_onesweep<true, false><<<tiles, kRadixThreads, kExchangeBytes, s>>>(
-          nullptr, nullptr, nullptr, nullptr, n, 0, nullptr, lb, tile_counter, epoch, counts, tiles, st, slot, sp);
-    else
-      k_onesweep<false, false><<<tiles, kRadixThreads, kExchangeBytes, s>>>(
-          nullptr, nullptr, nullptr, nullptr, n, 0, nullptr, lb, tile_counter, epoch, counts, tiles, st, slot, sp);
-    return;
-  }
   if (slot == 0 && vals_init == nullptr)
-    k_onesweep<true, true><<<tiles, kRadixThreads, kExchangeBytes, s>>>(
+    k_onesweep<true, true, kSlotBits><<<tiles, kRadixThreads, kX, s>>>(
         nullptr, nullptr, nullptr, nullptr, n, 0, nullptr, lb, tile_counter, epoch, nullptr, tiles, st, slot, sp);
   else
-    k_onesweep<false, true><<<tiles, kRadixThreads, kExchangeBytes, s>>>(
+    k_onesweep<false, true, kSlotBits><<<tiles, kRadixThreads, kX, s>>>(
         nullptr, nullptr, nullptr, nullptr, n, 0, nullptr, lb, tile_counter, epoch, nullptr, tiles, st, slot, sp);
 }
 
