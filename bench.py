@@ -133,6 +133,10 @@ def cpu_baseline(name, n_sample):
                       f"1 thread), {dt:.2f} s wall in total"}
 
 
+EXCHANGE = {1: "send buffers + ncclSend/ncclRecv",
+            2: "gather stores straight into the peers' NCCL symmetric windows (NVLink), 4-byte all-reduce barrier"}
+
+
 def make_config(args, n, coder, world):
     return {"workload": DESCR[args.config], "n_per_gpu": n, "coder": "ascii" if coder == 0 else "unicode",
             "outputs": "perm + sorted units + sorted offsets",
@@ -412,7 +416,9 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u8" if ub == 1 else "u16",
                 "data": "synthetic",
-                "config": make_config(args, n, w.coder, world),
+                "config": dict(make_config(args, n, w.coder, world),
+                               **({"exchange": EXCHANGE.get(outc.get("exchange", 0), "?")}
+                                  if isinstance(outc, dict) and outc.get("exchange") else {})),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "stages": stages, "outcome": outc}
         print(json.dumps(line), flush=True)

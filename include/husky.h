@@ -87,7 +87,19 @@ typedef struct {
                                (A6) passes are added                                     */
   uint64_t keys_partitioned;/* keys moved by the main key sort's passes, summed          */
   uint64_t keys_local;      /* keys sorted in shared memory by the MSD local sort        */
+  uint32_t exchange;        /* multi-GPU transport of the strings (husky_exchange)       */
 } husky_outcome;
+
+/* How a sample sort moved the strings between ranks (husky_outcome.exchange). */
+typedef enum {
+  HUSKY_EXCHANGE_NONE = 0,          /* single-GPU call                                    */
+  HUSKY_EXCHANGE_NCCL = 1,          /* send buffers + grouped ncclSend/ncclRecv           */
+  HUSKY_EXCHANGE_PEER = 2,          /* the gather stores straight into the destinations'
+                                       NCCL symmetric windows over NVLink (NEXT-2)        */
+  HUSKY_EXCHANGE_LOOPBACK_COPY = 3, /* loopback driver, device-to-device copies           */
+  HUSKY_EXCHANGE_LOOPBACK_PEER = 4  /* loopback driver, the same peer-store gather into
+                                       per-virtual-rank windows                           */
+} husky_exchange;
 
 /* 1 for ASCII / ENGLISH5 / ENGLISH6 (uint8 units), 2 for UNICODE, 0 for an unknown coder. */
 size_t husky_unit_bytes(int coder);
@@ -205,8 +217,17 @@ husky_status husky_sort_multi_plan(void *comm, int coder, const void *d_units,
                                    const int64_t *d_offsets, uint64_t n_local, uint64_t global_base,
                                    void *d_ws, size_t ws_bytes, void **plan, uint64_t *h_n_out,
                                    uint64_t *h_units_out, void *stream);
-/* Phase 2: exchange strings (NCCL grouped send/recv) and sort the received
- * bucket.  d_perm_out: h_n_out entries (global indices); d_sorted_units_out:
+/* Phase 2: exchange strings and sort the received bucket.  Transport: the
+ * partitioning gather stores every string straight into its destination
+ * rank's receive window -- an NCCL symmetric window (ncclMemAlloc +
+ * ncclCommWindowRegister, owned by the communicator, grown collectively by
+ * the plan call) written through NVLink peer addresses -- followed by a 4-byte
+ * all-reduce barrier; with HUSKY_EXCHANGE=nccl in the environment (or if the
+ * window cannot be registered on every rank) send buffers + grouped
+ * ncclSend/ncclRecv.  h_out->exchange says which ran.  The receive window
+ * is reused across calls: the plan of a call must not start on one rank while
+ * another rank's exec of the previous call runs (exec synchronizes its stream
+ * before returning, so sequential calls per rank satisfy this).  d_perm_out: h_n_out entries (global indices); d_sorted_units_out:
  * h_units_out units (nullable -> perm-only); d_sorted_offsets_out: h_n_out+1
  * (nullable iff d_sorted_units_out is), local offsets starting at 0.
  * d_recv_ws must hold husky_sort_multi_recv_workspace(plan) bytes. */

@@ -46,14 +46,16 @@ class husky_outcome(ctypes.Structure):
                 ("n_runs", ctypes.c_uint64), ("n_in_runs", ctypes.c_uint64),
                 ("max_run", ctypes.c_uint64), ("runs_by_class", ctypes.c_uint64 * 4),
                 ("refine_rounds", ctypes.c_uint32), ("radix_passes", ctypes.c_uint32),
-                ("keys_partitioned", ctypes.c_uint64), ("keys_local", ctypes.c_uint64)]
+                ("keys_partitioned", ctypes.c_uint64), ("keys_local", ctypes.c_uint64),
+                ("exchange", ctypes.c_uint32)]
 
     def as_dict(self):
         return {"perfect": bool(self.perfect), "domain_ok": bool(self.domain_ok),
                 "n_runs": self.n_runs, "n_in_runs": self.n_in_runs, "max_run": self.max_run,
                 "runs_by_class": list(self.runs_by_class), "refine_rounds": self.refine_rounds,
                 "radix_passes": self.radix_passes,
-                "keys_partitioned": self.keys_partitioned, "keys_local": self.keys_local}
+                "keys_partitioned": self.keys_partitioned, "keys_local": self.keys_local,
+                "exchange": self.exchange}
 
 
 if not os.path.exists(LIB_PATH):

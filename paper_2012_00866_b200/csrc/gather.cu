@@ -50,7 +50,7 @@ struct GatherRuns {
   DevState *st;            // n_runs
 };
 
-template <int CODER, bool PACKED, bool CHECK>
+template <int CODER, bool PACKED, bool CHECK, bool PEER>
 // 5 CTAs/SM (48 registers): measured 280 vs 289 us (4/SM) and 298 us (6/SM) on C2
 #ifndef HUSKY_GATHER_MINB
 #define HUSKY_GATHER_MINB 5
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
              const int64_t *__restrict__ offsets, void *__restrict__ sorted_units,
              int64_t *__restrict__ sorted_offsets, unsigned long long *lb, uint32_t *tile_counter,
              uint32_t epoch, const int64_t *base_ptr, int dbg, const uint64_t *__restrict__ codes,
-             const DevState *st, GatherRuns runs) {
+             const DevState *st, GatherRuns runs, const PeerTable *peer) {
   using T = CoderTraits<CODER>;
   constexpr int W = T::kUnitBytes;
   constexpr uint32_t PL = T::kPL;
@@ -71,7 +71,15 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   // CHECK: each thread's last item (code, length, index, tile-local unit offset)
   __shared__ unsigned long long s_lcode[CHECK ? kGatherThreads : 1], s_loff[CHECK ? kGatherThreads : 1];
   __shared__ uint32_t s_llen[CHECK ? kGatherThreads : 1], s_lidx[CHECK ? kGatherThreads : 1];
+  // PEER: the buckets' start positions / units in the partitioned order
+  __shared__ unsigned long long s_sn[PEER ? kMaxPeers + 1 : 1], s_su[PEER ? kMaxPeers + 1 : 1];
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  if (PEER) {
+    for (uint32_t b = tid; b <= peer->world; b += kGatherThreads) {
+      s_sn[b] = peer->start_n[b];
+      s_su[b] = peer->start_u[b];
+    }
+  }
   if (st) {
     if (st->violations & kOffsetsBad) return;  // invalid input: reported by the caller
     if ((PACKED || CHECK) && codes == nullptr) codes = reinterpret_cast<const uint64_t *>(st->sorted_keys);
@@ -137,7 +145,7 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
         sv[j] = (uint64_t)a;
         len[j] = (uint32_t)(b - a);
         // the staging reads these units after the block scan: start the fetch now
-        if (sorted_units && len[j]) {
+        if ((PEER || sorted_units) && len[j]) {
           const uint8_t *pa = (const uint8_t *)units + (uint64_t)a * W;
           asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
           if ((((uintptr_t)pa & 127) + (uint64_t)len[j] * W) > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 127));
@@ -192,7 +200,8 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   const uint8_t *ub = (const uint8_t *)units;
   uint8_t *ob = (uint8_t *)sorted_units;
   const uint64_t tile_bytes = tile_total * W;
-  const bool direct = (dbg & 1) != 0;
+  const bool direct = !PEER && (dbg & 1) != 0;
+  const bool want_units = PEER || sorted_units != nullptr;
 
   // stage tile-local output bytes [w0, w1) of this thread's strings at stage[x - w0]
   auto stage_window = [&](uint64_t w0, uint64_t w1) {
@@ -216,17 +225,18 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       d += nb;
     }
   };
-  // write tile-local bytes [w0, w1) (staged at stage[x - w0]) to g0 + x
-  auto write_window = [&](uint8_t *g0, uint64_t w0, uint64_t w1) {
+  // write tile-local bytes [lo, hi) of the window staged from w0 (byte x at
+  // stage[x - w0]) to g0 + x
+  auto write_range = [&](uint8_t *g0, uint64_t w0, uint64_t lo_x, uint64_t hi_x) {
     const uint32_t align = (uint32_t)((uintptr_t)g0 & 15);
     uint8_t *a0 = g0 - align;  // 16-aligned; tile byte x lives at a0 + align + x
-    const uint64_t lo_b = align + w0, hi_b = align + w1;
+    const uint64_t lo_b = align + lo_x, hi_b = align + hi_x, st_b = align + w0;  // st_b: address of stage[0]
     const uint64_t c0 = lo_b / 16, c1 = (hi_b + 15) / 16;
     const uint32_t *sw = reinterpret_cast<const uint32_t *>(stage);
     for (uint64_t ch = c0 + tid; ch < c1; ch += kGatherThreads) {
       uint64_t lo = ch * 16, hi = lo + 16;
       if (lo >= lo_b && hi <= hi_b) {
-        uint32_t so = (uint32_t)(lo - lo_b);  // stage offset of the chunk
+        uint32_t so = (uint32_t)(lo - st_b);  // stage offset of the chunk
         uint32_t wi = so >> 2, sh = (so & 3) * 8;
         uint32_t x0 = sw[wi], x1 = sw[wi + 1], x2 = sw[wi + 2], x3 = sw[wi + 3], x4 = sw[wi + 4];
         uint4 o;
@@ -236,13 +246,28 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
         o.w = __funnelshift_r(x3, x4, sh);
         *reinterpret_cast<uint4 *>(a0 + lo) = o;
       } else {
-        for (uint64_t b = (lo > lo_b ? lo : lo_b); b < (hi < hi_b ? hi : hi_b); ++b) a0[b] = stage[b - lo_b];
+        for (uint64_t b = (lo > lo_b ? lo : lo_b); b < (hi < hi_b ? hi : hi_b); ++b) a0[b] = stage[b - st_b];
       }
+    }
+  };
+  // PEER: the window's bytes bucket by bucket, each to its destination
+  auto write_window = [&](uint8_t *g0, uint64_t w0, uint64_t w1) {
+    if (!PEER) {
+      write_range(g0, w0, w0, w1);
+      return;
+    }
+    const uint64_t v0 = s_base * W;  // virtual byte of tile byte 0 (s_base: units before the tile)
+    uint32_t b = 0;
+    while (b + 1 < peer->world && s_su[b + 1] * W <= v0 + w0) ++b;
+    for (; b < peer->world && s_su[b] * W < v0 + w1; ++b) {
+      const uint64_t blo = s_su[b] * W, bhi = s_su[b + 1] * W;
+      const uint64_t lo = blo > v0 + w0 ? blo - v0 : w0, hi = bhi < v0 + w1 ? bhi - v0 : w1;
+      if (lo < hi) write_range(reinterpret_cast<uint8_t *>(peer->units[b] + v0), w0, lo, hi);
     }
   };
 
   const uint64_t first_w1 = tile_bytes < (uint64_t)kGatherStage ? tile_bytes : (uint64_t)kGatherStage;
-  if (sorted_units && !direct) stage_window(0, first_w1);  // overlaps the look-back
+  if (want_units && !direct) stage_window(0, first_w1);  // overlaps the look-back
   GT(tile, 2);
 
   if (CHECK) {
@@ -257,7 +282,7 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
     if (lane == 0) {
       if (tile != 0) st_relaxed_u64(lb + tile, make_flag(kFlagInc, epoch, ex + tile_total));
       s_base = ex;
-      if ((uint64_t)(tile + 1) * kGatherTile >= n) sorted_offsets[n] = (int64_t)(gbase + ex + tile_total);
+      if (!PEER && (uint64_t)(tile + 1) * kGatherTile >= n) sorted_offsets[n] = (int64_t)(gbase + ex + tile_total);
     }
   } else if (CHECK && warp == 1) {  // the run-count scan's look-back, next to warp 0's
     unsigned long long ex = tile == 0 ? 0ull : warp_lookback(runs.lb, tile, epoch);
@@ -270,12 +295,25 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   __syncthreads();
   GT(tile, 3);
   const unsigned long long tbase = gbase + s_base;  // units before this tile
-  {
+  if (!PEER) {
     unsigned long long d = tbase + excl_t;
 #pragma unroll
     for (int j = 0; j < kGatherItems; ++j) {
       if (p0 + j < n) sorted_offsets[p0 + j] = (int64_t)d;
       d += len[j];
+    }
+  } else if (p0 < n) {
+    // length and global index of each string, into its destination's arrays
+    uint32_t b = 0;
+    while (b + 1 < peer->world && s_sn[b + 1] <= p0) ++b;
+#pragma unroll
+    for (int j = 0; j < kGatherItems; ++j) {
+      const uint64_t p = p0 + j;
+      if (p < n) {
+        while (s_sn[b + 1] <= p) ++b;
+        reinterpret_cast<uint32_t *>(peer->lens[b])[p] = len[j];
+        reinterpret_cast<uint32_t *>(peer->gidx[b])[p] = peer->gbase + ix[j];
+      }
     }
   }
   if (CHECK) {
@@ -342,7 +380,7 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
     }
   }
   GT(tile, 4);
-  if (sorted_units == nullptr) return;
+  if (!want_units) return;
 
   uint8_t *g0 = ob + tbase * W;  // first output byte of the tile
   if (!direct) {
@@ -384,7 +422,7 @@ void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, con
   constexpr int kSmem = kGatherStage + 32;
   static bool configured = false;
   if (!configured) {
-#define G_ATTR(C, P, K) cudaFuncSetAttribute(k_gather<C, P, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem)
+#define G_ATTR(C, P, K) cudaFuncSetAttribute(k_gather<C, P, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem)
     G_ATTR(HUSKY_CODER_ASCII, true, false); G_ATTR(HUSKY_CODER_ASCII, false, false);
     G_ATTR(HUSKY_CODER_UNICODE, true, false); G_ATTR(HUSKY_CODER_UNICODE, false, false);
     G_ATTR(HUSKY_CODER_ASCII, true, true); G_ATTR(HUSKY_CODER_ASCII, false, true);
@@ -402,26 +440,52 @@ void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, con
   GatherRuns runs{};
   if (runs_out) runs = GatherRuns{runs_out->run_start, runs_out->run_end, runs_out->dirty, runs_out->lb, runs_out->st};
 #define G_ARGS \
-  perm, n, units, offsets, sorted_units, sorted_offsets, lb, tile_counter, epoch, base_ptr, dbg, packed_codes, st, runs
+  perm, n, units, offsets, sorted_units, sorted_offsets, lb, tile_counter, epoch, base_ptr, dbg, packed_codes, st, runs, nullptr
   const bool chk = runs_out != nullptr;
   if (coder == HUSKY_CODER_ASCII) {
     if (packed) {
-      if (chk) k_gather<HUSKY_CODER_ASCII, true, true><<<g, b, kSmem, s>>>(G_ARGS);
-      else k_gather<HUSKY_CODER_ASCII, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) k_gather<HUSKY_CODER_ASCII, true, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+      else k_gather<HUSKY_CODER_ASCII, true, false, false><<<g, b, kSmem, s>>>(G_ARGS);
     } else {
-      if (chk) k_gather<HUSKY_CODER_ASCII, false, true><<<g, b, kSmem, s>>>(G_ARGS);
-      else k_gather<HUSKY_CODER_ASCII, false, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) k_gather<HUSKY_CODER_ASCII, false, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+      else k_gather<HUSKY_CODER_ASCII, false, false, false><<<g, b, kSmem, s>>>(G_ARGS);
     }
   } else {
     if (packed) {
-      if (chk) k_gather<HUSKY_CODER_UNICODE, true, true><<<g, b, kSmem, s>>>(G_ARGS);
-      else k_gather<HUSKY_CODER_UNICODE, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) k_gather<HUSKY_CODER_UNICODE, true, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+      else k_gather<HUSKY_CODER_UNICODE, true, false, false><<<g, b, kSmem, s>>>(G_ARGS);
     } else {
-      if (chk) k_gather<HUSKY_CODER_UNICODE, false, true><<<g, b, kSmem, s>>>(G_ARGS);
-      else k_gather<HUSKY_CODER_UNICODE, false, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) k_gather<HUSKY_CODER_UNICODE, false, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+      else k_gather<HUSKY_CODER_UNICODE, false, false, false><<<g, b, kSmem, s>>>(G_ARGS);
     }
   }
 #undef G_ARGS
+}
+
+void launch_gather_peer(int coder, const uint32_t *perm, uint64_t n, const void *units, const int64_t *offsets,
+                        unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, const PeerTable *d_table,
+                        cudaStream_t s) {
+  if (n == 0) return;
+  constexpr int kSmem = kGatherStage + 32;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_gather<HUSKY_CODER_ASCII, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmem);
+    cudaFuncSetAttribute(k_gather<HUSKY_CODER_UNICODE, false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    configured = true;
+  }
+  Scope sc_(ST_MULTI, s, n);
+  dim3 g((unsigned)gather_tiles(n)), b(kGatherThreads);
+  uint32_t *pm = const_cast<uint32_t *>(perm);  // read only (PACKED = false)
+  if (coder == HUSKY_CODER_ASCII)
+    k_gather<HUSKY_CODER_ASCII, false, false, true><<<g, b, kSmem, s>>>(
+        pm, n, units, offsets, nullptr, nullptr, lb, tile_counter, epoch, nullptr, 0, nullptr, nullptr, GatherRuns{},
+        d_table);
+  else
+    k_gather<HUSKY_CODER_UNICODE, false, false, true><<<g, b, kSmem, s>>>(
+        pm, n, units, offsets, nullptr, nullptr, lb, tile_counter, epoch, nullptr, 0, nullptr, nullptr, GatherRuns{},
+        d_table);
 }
 
 // perm-only mode with a packed payload: strip the length bits

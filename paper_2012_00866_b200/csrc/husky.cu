@@ -311,6 +311,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
     h_out->radix_passes = S.radix_passes;
     h_out->keys_partitioned = use_msd ? hs.msd_keys_part : (uint64_t)hs.np * n;
     h_out->keys_local = hs.msd_keys_local;
+    h_out->exchange = HUSKY_EXCHANGE_NONE;
   }
   return HUSKY_OK;
 }

@@ -141,6 +141,23 @@ struct GatherRunsOut {
   unsigned long long *lb;
   DevState *st;
 };
+// Multi-GPU exchange fused into the gather (NEXT-2): the partitioned order's
+// strings go straight into the destination ranks' receive windows (NVLink peer
+// memory, or the loopback driver's per-rank regions).  Position j of the
+// partitioned order belongs to bucket b with start_n[b] <= j < start_n[b+1]
+// (units: start_u); its length goes to lens[b] + 4 j, its global index to
+// gidx[b] + 4 j and its units to units[b] + w * (virtual unit offset), every
+// base pre-shifted by the bucket start and this rank's displacement in the
+// destination (modular uint64 address arithmetic).
+constexpr int kMaxPeers = 256;
+struct PeerTable {
+  uint32_t world, gbase;
+  uint64_t start_n[kMaxPeers + 1], start_u[kMaxPeers + 1];
+  uint64_t units[kMaxPeers], lens[kMaxPeers], gidx[kMaxPeers];
+};
+void launch_gather_peer(int coder, const uint32_t *perm, uint64_t n, const void *units, const int64_t *offsets,
+                        unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, const PeerTable *d_table,
+                        cudaStream_t s);
 void launch_unpack_perm(uint32_t *perm, uint64_t n, cudaStream_t s);
 void launch_regather_runs(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                           const uint32_t *perm, const void *units, const int64_t *offsets,

@@ -17,14 +17,23 @@
 //      the samples) and picks the same P-1 splitters (the rule of
 //      husky_select_splitters); bucket(x) = #splitters <= x (binary search,
 //      strings compared only on code ties); per-destination string/unit
-//      counts; all-to-all of the counts (grouped send/recv);
+//      counts; all-gather of the P x P count matrix;
 //   3. stable partition by bucket = one onesweep pass on the bucket digit, then
-//      the A4 gather builds the send buffers (units, lengths, global indices);
-//      grouped ncclSend/ncclRecv of the three arrays;
+//      the exchange, one of:
+//      * peer stores (default, NEXT-2): the A4 gather writes every string's
+//        units, length and global index straight into its destination rank's
+//        receive window -- an NCCL symmetric window (ncclMemAlloc +
+//        ncclCommWindowRegister) whose peer mappings (ncclGetPeerPointer) are
+//        NVLink / NVSwitch load-store addresses -- at the rank's displacement
+//        in that window (from the count matrix); one 4-byte all-reduce then
+//        orders the stores before any rank reads its window;
+//      * HUSKY_EXCHANGE=nccl (or a failed window registration): the gather
+//        builds send buffers, then grouped ncclSend/ncclRecv of the three arrays;
 //   4. lengths -> offsets scan, the single-GPU husky_sort on the received bucket
 //      (received order = ascending global index, so the index tie-break holds),
 //      perm remapped to global indices.
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <algorithm>
 #include <chrono>
@@ -253,6 +262,11 @@ __global__ void k_add_base(int64_t *o, uint64_t n, int64_t add) {
     o[i] += add;
 }
 
+// peer base addresses of a symmetric window (NVLink load/store mappings)
+__global__ void k_win_ptrs(ncclWindow_t w, int world, unsigned long long *out) {
+  for (int p = threadIdx.x; p < world; p += blockDim.x) out[p] = (unsigned long long)ncclGetPeerPointer(w, 0, p);
+}
+
 static unsigned grid_for(uint64_t n) {
   uint64_t b = (n + 255) / 256;
   return (unsigned)(b < 1 ? 1 : (b > 4096 ? 4096 : b));
@@ -283,12 +297,38 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Comm {
   ncclComm_t nccl = nullptr;
   int rank = 0, world = 1;
+  // receive window for the peer-store exchange (grown collectively on demand)
+  void *win_buf = nullptr;
+  size_t win_bytes = 0;
+  ncclWindow_t win = nullptr;
+  bool win_failed = false;                // registration failed on some rank: NCCL send/recv
+  std::vector<unsigned long long> peer;   // peer base address of the window, per rank
+  unsigned long long *d_tmp = nullptr;    // world words (peer addresses, barrier word)
 };
+
+// Where a rank receives: units at 0, lengths and global indices after them.
+// Window offsets are the same on every rank (sized by the largest shard).
+struct WinLayout {
+  size_t units = 0, lens = 0, gidx = 0, total = 0;
+};
+static WinLayout make_win_layout(size_t w, uint64_t cap_n, uint64_t cap_u) {
+  WinLayout W;
+  W.units = 0;
+  W.lens = align_up(cap_u * w + 16, 256);
+  W.gidx = W.lens + align_up(cap_n * 4 + 4, 256);
+  W.total = W.gidx + align_up(cap_n * 4 + 4, 256);
+  return W;
+}
+
+static bool exchange_by_nccl() {
+  const char *v = getenv("HUSKY_EXCHANGE");
+  return v && (v[0] == 'n' || v[0] == 'c');  // "nccl" / "copy" (loopback)
+}
 
 struct MultiLayout {
   Layout L;  // state, keysA (= codes), keysB, vals, lb_radix, lb_scan used by the Sorter
   size_t send_perm = 0, samples = 0, splitters = 0, counts = 0, rcounts = 0, send_units = 0,
-         send_offsets = 0, send_gidx = 0, send_lens = 0, total = 0;
+         send_offsets = 0, send_gidx = 0, send_lens = 0, peer_table = 0, total = 0;
   // composite splitters: gathered sample records, their packed strings, the
   // GPU sort of the samples (perm + workspace), the non-empty rank list
   size_t recs = 0, smp_units = 0, smp_offsets = 0, smp_lens = 0, smp_lb = 0, smp_perm = 0, smp_ws = 0, ranks = 0;
@@ -323,7 +363,8 @@ static MultiLayout make_multi_layout(int coder, uint64_t n, uint64_t units, int 
   M.smp_ws = take(make_layout(ms).total);
   M.ranks = take((size_t)world * 4);
   M.counts = take((size_t)world * 16);
-  M.rcounts = take((size_t)world * 16);
+  M.rcounts = take((size_t)world * world * 16);  // the all-gathered count matrix [src][dst]
+  M.peer_table = take(sizeof(PeerTable));
   M.send_units = take(units * w + 16);
   M.send_offsets = take((n + 1) * 8);
   M.send_gidx = take(n * 4 + 4);
@@ -336,15 +377,16 @@ static MultiLayout make_multi_layout(int coder, uint64_t n, uint64_t units, int 
 struct RecvLayout {
   size_t units = 0, offsets = 0, lens = 0, gidx = 0, lb = 0, sort_ws = 0, total = 0;
 };
-static RecvLayout make_recv_layout(int coder, uint64_t n_out, uint64_t units_out) {
+// data = false: the received arrays live in the peer-store window instead
+static RecvLayout make_recv_layout(int coder, uint64_t n_out, uint64_t units_out, bool data = true) {
   RecvLayout R;
   size_t off = 0;
   auto take = [&](size_t b) { size_t o = off; off = align_up(off + b, 256); return o; };
   size_t w = coder_unit_bytes(coder);
-  R.units = take(units_out * w + 16);
+  R.units = take(data ? units_out * w + 16 : 0);
   R.offsets = take((n_out + 1) * 8);
-  R.lens = take(n_out * 4 + 4);
-  R.gidx = take(n_out * 4 + 4);
+  R.lens = take(data ? n_out * 4 + 4 : 0);
+  R.gidx = take(data ? n_out * 4 + 4 : 0);
   R.lb = take(scan_tiles(n_out) * 8 + 8);
   R.sort_ws = take(make_layout(n_out).total);
   R.total = off;
@@ -363,8 +405,12 @@ struct Plan {
   cudaStream_t s = nullptr;
   Sorter S;
   std::vector<uint64_t> send_cnt, send_u, recv_cnt, recv_u;  // per peer
+  std::vector<uint64_t> disp_n, disp_u;  // this rank's offset in each destination's received arrays
   uint64_t n_out = 0, units_out = 0;
+  uint64_t cap_n = 0, cap_u = 0;  // the largest shard (strings, units): sizes the receive windows
   bool general = false;  // some rank saw off-domain units (readings R5, R15)
+  bool peer = false;     // exchange by peer stores into the receive windows (NEXT-2)
+  PeerTable table;
 
   template <typename T> T *at(size_t o) const { return reinterpret_cast<T *>(ws + o); }
   DevState *st() const { return at<DevState>(M.L.state); }
@@ -472,30 +518,46 @@ struct Plan {
     return HUSKY_OK;
   }
 
+  // counts[p] = (strings, units) this rank sends to p; rcounts = the all-gathered
+  // matrix, row q = rank q's counts
   husky_status read_counts() {
-    std::vector<uint64_t> c((size_t)world * 2), rc((size_t)world * 2);
+    std::vector<uint64_t> c((size_t)world * 2), mat((size_t)world * world * 2);
     HCHECK(cudaMemcpyAsync(c.data(), at<uint64_t>(M.counts), c.size() * 8, cudaMemcpyDeviceToHost, s));
-    HCHECK(cudaMemcpyAsync(rc.data(), at<uint64_t>(M.rcounts), rc.size() * 8, cudaMemcpyDeviceToHost, s));
+    HCHECK(cudaMemcpyAsync(mat.data(), at<uint64_t>(M.rcounts), mat.size() * 8, cudaMemcpyDeviceToHost, s));
     HCHECK(cudaStreamSynchronize(s));
-    send_cnt.resize(world); send_u.resize(world); recv_cnt.resize(world); recv_u.resize(world);
-    n_out = units_out = 0;
+    send_cnt.assign(world, 0); send_u.assign(world, 0); recv_cnt.assign(world, 0); recv_u.assign(world, 0);
+    disp_n.assign(world, 0); disp_u.assign(world, 0);
+    n_out = units_out = cap_n = cap_u = 0;
+    auto m = [&](int q, int p, int k) { return mat[((size_t)q * world + p) * 2 + k]; };
     for (int p = 0; p < world; ++p) {
       send_cnt[p] = c[2 * p]; send_u[p] = c[2 * p + 1];
-      recv_cnt[p] = rc[2 * p]; recv_u[p] = rc[2 * p + 1];
+      recv_cnt[p] = m(p, rank, 0); recv_u[p] = m(p, rank, 1);
       n_out += recv_cnt[p];
       units_out += recv_u[p];
+      uint64_t tn = 0, tu = 0;
+      for (int q = 0; q < world; ++q) {
+        if (q == rank) { disp_n[p] = tn; disp_u[p] = tu; }
+        tn += m(q, p, 0);
+        tu += m(q, p, 1);
+      }
+      cap_n = std::max(cap_n, tn);
+      cap_u = std::max(cap_u, tu);
     }
     return HUSKY_OK;
   }
 
-  // phase 3: stable partition by bucket + send buffers
-  husky_status phase3() {
+  // phase 3a: stable partition by bucket (one onesweep pass on the bucket digit)
+  husky_status partition() {
     if (n == 0) return HUSKY_OK;
     uint64_t *sorted_keys = nullptr;
     // bucket ids only occupy digit 0
-    if (husky_status e = S.radix(at<uint64_t>(M.L.keysB), nullptr, n, 0xFEu, at<uint32_t>(M.send_perm),
-                                 at<uint32_t>(M.L.vals), &sorted_keys))
-      return e;
+    return S.radix(at<uint64_t>(M.L.keysB), nullptr, n, 0xFEu, at<uint32_t>(M.send_perm), at<uint32_t>(M.L.vals),
+                   &sorted_keys);
+  }
+
+  // phase 3b (NCCL exchange): send buffers -- units, lengths, global indices
+  husky_status build_send() {
+    if (n == 0) return HUSKY_OK;
     HUSKY_SCOPE(ST_MULTI, s, 0);
     k_send_meta<<<grid_for(n), 256, 0, s>>>(at<uint32_t>(M.send_perm), n, offsets, (uint32_t)gbase,
                                             at<uint32_t>(M.send_gidx), at<uint32_t>(M.send_lens));
@@ -505,8 +567,34 @@ struct Plan {
     return HUSKY_OK;
   }
 
+  // phase 3b (peer stores): the gather writes each bucket straight into its
+  // destination's window; du / dl / dg [p] = addresses of rank p's received
+  // units / lengths / global indices (its NVLink mapping, or a loopback region)
+  husky_status scatter_peer(const std::vector<unsigned long long> &du, const std::vector<unsigned long long> &dl,
+                            const std::vector<unsigned long long> &dg) {
+    if (n == 0) return HUSKY_OK;
+    table.world = (uint32_t)world;
+    table.gbase = (uint32_t)gbase;
+    table.start_n[0] = table.start_u[0] = 0;
+    for (int p = 0; p < world; ++p) {
+      table.start_n[p + 1] = table.start_n[p] + send_cnt[p];
+      table.start_u[p + 1] = table.start_u[p] + send_u[p];
+      // modular address arithmetic: base + (displacement - bucket start) * size
+      table.units[p] = du[p] + (disp_u[p] - table.start_u[p]) * w();
+      table.lens[p] = dl[p] + (disp_n[p] - table.start_n[p]) * 4;
+      table.gidx[p] = dg[p] + (disp_n[p] - table.start_n[p]) * 4;
+    }
+    HCHECK(cudaMemcpyAsync(at<PeerTable>(M.peer_table), &table, sizeof table, cudaMemcpyHostToDevice, s));
+    launch_gather_peer(kernel_coder(coder), at<uint32_t>(M.send_perm), n, units, offsets, S.lb_scan(),
+                       S.next_counter(), S.next_epoch(), at<PeerTable>(M.peer_table), s);
+    HCHECK(cudaGetLastError());
+    return HUSKY_OK;
+  }
+
   // phase 4 on the received bucket (recv buffers already filled)
-  husky_status phase4(uint8_t *rws, const RecvLayout &R, uint32_t *d_perm_out, void *d_sorted_units_out,
+  // r_units / r_lens / r_gidx: the received arrays (receive workspace or window)
+  husky_status phase4(const uint8_t *r_units, const uint32_t *r_lens, const uint32_t *r_gidx, uint8_t *rws,
+                      const RecvLayout &R, uint32_t *d_perm_out, void *d_sorted_units_out,
                       int64_t *d_sorted_offsets_out, husky_outcome *h_out) {
     if (n_out == 0) {
       if (h_out) { memset(h_out, 0, sizeof *h_out); h_out->perfect = 1; h_out->domain_ok = 1; }
@@ -517,7 +605,7 @@ struct Plan {
     HCHECK(cudaMemsetAsync(&st()->tile_counter[63], 0, 4, s));
     HUSKY_SCOPE(ST_MULTI, s, 0);
     k_lens_to_offsets<<<(unsigned)scan_tiles(n_out), kScanThreads, 0, s>>>(
-        (const uint32_t *)(rws + R.lens), n_out, (int64_t *)(rws + R.offsets), (unsigned long long *)(rws + R.lb),
+        r_lens, n_out, (int64_t *)(rws + R.offsets), (unsigned long long *)(rws + R.lb),
         &st()->tile_counter[63], 1, 0);
     HCHECK(cudaGetLastError());
     if (debug_sync()) {
@@ -526,17 +614,17 @@ struct Plan {
       HCHECK(cudaStreamSynchronize(s));
       HCHECK(cudaMemcpy(&ends[0], rws + R.offsets, 8, cudaMemcpyDeviceToHost));
       HCHECK(cudaMemcpy(&ends[1], (int64_t *)(rws + R.offsets) + n_out, 8, cudaMemcpyDeviceToHost));
-      HCHECK(cudaMemcpy(l0, rws + R.lens, 16, cudaMemcpyDeviceToHost));
+      HCHECK(cudaMemcpy(l0, r_lens, 16, cudaMemcpyDeviceToHost));
       fprintf(stderr, "[husky] rank %d recv n=%llu units=%llu offsets[0]=%lld offsets[n]=%lld lens %u %u %u %u\n",
               rank, (unsigned long long)n_out, (unsigned long long)units_out, (long long)ends[0],
               (long long)ends[1], l0[0], l0[1], l0[2], l0[3]);
     }
-    husky_status e = sort_impl(coder, rws + R.units, (const int64_t *)(rws + R.offsets), n_out, d_perm_out,
+    husky_status e = sort_impl(coder, r_units, (const int64_t *)(rws + R.offsets), n_out, d_perm_out,
                                d_sorted_units_out, d_sorted_offsets_out, rws + R.sort_ws,
                                make_layout(n_out).total, h_out, s);
     if (e) return e;
     HUSKY_SCOPE(ST_MULTI, s, 0);
-    k_remap<<<grid_for(n_out), 256, 0, s>>>(d_perm_out, n_out, (const uint32_t *)(rws + R.gidx));
+    k_remap<<<grid_for(n_out), 256, 0, s>>>(d_perm_out, n_out, r_gidx);
     HCHECK(cudaGetLastError());
     return HUSKY_OK;
   }
@@ -554,14 +642,64 @@ static husky_status nccl_allgather_samples(Plan &P) {
   return HUSKY_OK;
 }
 
-static husky_status nccl_alltoall_counts(Plan &P) {
-  uint64_t *c = P.at<uint64_t>(P.M.counts), *rc = P.at<uint64_t>(P.M.rcounts);
-  NCHECK(ncclGroupStart());
-  for (int p = 0; p < P.world; ++p) {
-    NCHECK(ncclSend(c + 2 * p, 2, ncclUint64, p, P.comm->nccl, P.s));
-    NCHECK(ncclRecv(rc + 2 * p, 2, ncclUint64, p, P.comm->nccl, P.s));
+// every rank gets the whole P x P count matrix (its displacements in the
+// destinations' windows and the window size need the other ranks' rows)
+static husky_status nccl_allgather_counts(Plan &P) {
+  NCHECK(ncclAllGather(P.at<uint64_t>(P.M.counts), P.at<uint64_t>(P.M.rcounts), (size_t)P.world * 2, ncclUint64,
+                       P.comm->nccl, P.s));
+  return HUSKY_OK;
+}
+
+// AND of a flag over the ranks (synchronous)
+static husky_status all_ranks_ok(Comm *c, cudaStream_t s, bool mine, bool *all) {
+  unsigned long long v = mine ? 1ull : 0ull;
+  HCHECK(cudaMemcpyAsync(c->d_tmp + c->world, &v, 8, cudaMemcpyHostToDevice, s));
+  NCHECK(ncclAllReduce(c->d_tmp + c->world, c->d_tmp + c->world, 1, ncclUint64, ncclMin, c->nccl, s));
+  HCHECK(cudaMemcpyAsync(&v, c->d_tmp + c->world, 8, cudaMemcpyDeviceToHost, s));
+  HCHECK(cudaStreamSynchronize(s));
+  *all = v != 0;
+  return HUSKY_OK;
+}
+
+static void release_window(Comm *c) {
+  if (c->win) ncclCommWindowDeregister(c->nccl, c->win);
+  if (c->win_buf) ncclMemFree(c->win_buf);
+  c->win = nullptr;
+  c->win_buf = nullptr;
+  c->win_bytes = 0;
+}
+
+// Make the receive window hold `need` bytes on every rank.  Collective: all
+// ranks see the same count matrix, hence the same `need`, and take the same
+// branches.  A failure anywhere turns the exchange into NCCL send/recv for the
+// communicator's lifetime (*ok = false on every rank).
+static husky_status ensure_window(Comm *c, size_t need, cudaStream_t s, bool *ok) {
+  *ok = false;
+  if (c->win_failed) return HUSKY_OK;
+  if (c->win && c->win_bytes >= need) { *ok = true; return HUSKY_OK; }
+  HCHECK(cudaStreamSynchronize(s));
+  release_window(c);
+  const size_t bytes = align_up(need + need / 4 + 4096, (size_t)2 << 20);  // headroom for the next call
+  bool mine = ncclMemAlloc(&c->win_buf, bytes) == ncclSuccess, all = false;
+  if (!mine) c->win_buf = nullptr;
+  if (husky_status e = all_ranks_ok(c, s, mine, &all)) return e;
+  if (all) {
+    mine = ncclCommWindowRegister(c->nccl, c->win_buf, bytes, &c->win, NCCL_WIN_COLL_SYMMETRIC) == ncclSuccess;
+    if (!mine) c->win = nullptr;
+    if (husky_status e = all_ranks_ok(c, s, mine, &all)) return e;
   }
-  NCHECK(ncclGroupEnd());
+  if (!all) {
+    release_window(c);
+    c->win_failed = true;
+    fprintf(stderr, "[husky] symmetric window registration failed: exchanging by NCCL send/recv\n");
+    return HUSKY_OK;
+  }
+  c->win_bytes = bytes;
+  k_win_ptrs<<<1, 256, 0, s>>>(c->win, c->world, c->d_tmp);
+  c->peer.assign(c->world, 0);
+  HCHECK(cudaMemcpyAsync(c->peer.data(), c->d_tmp, (size_t)c->world * 8, cudaMemcpyDeviceToHost, s));
+  HCHECK(cudaStreamSynchronize(s));
+  *ok = true;
   return HUSKY_OK;
 }
 
@@ -641,6 +779,11 @@ husky_status husky_comm_create(int rank, int world, const uint8_t id[128], void 
     delete c;
     return fail(HUSKY_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
   }
+  if (cudaMalloc(&c->d_tmp, ((size_t)world + 1) * 8) != cudaSuccess) {
+    ncclCommDestroy(c->nccl);
+    delete c;
+    return fail(HUSKY_ERR_CUDA, "cudaMalloc of the communicator scratch failed");
+  }
   *comm = c;
   return HUSKY_OK;
 }
@@ -648,6 +791,8 @@ husky_status husky_comm_create(int rank, int world, const uint8_t id[128], void 
 husky_status husky_comm_destroy(void *comm) {
   if (!comm) return HUSKY_OK;
   Comm *c = (Comm *)comm;
+  release_window(c);
+  if (c->d_tmp) cudaFree(c->d_tmp);
   ncclResult_t r = ncclCommDestroy(c->nccl);
   delete c;
   if (r != ncclSuccess) return fail(HUSKY_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
@@ -701,9 +846,16 @@ husky_status husky_sort_multi_plan(void *comm, int coder, const void *d_units, c
   pc.mark("splitters");
   if (!e) e = P->phase2();
   pc.mark("bucket");
-  if (!e) e = nccl_alltoall_counts(*P);
+  if (!e) e = nccl_allgather_counts(*P);
   if (!e) e = P->read_counts();
   pc.mark("counts");
+  // exchange mode: peer stores into the receive windows unless disabled / failed
+  if (!e && !exchange_by_nccl()) {
+    bool ok = false;
+    e = ensure_window(c, make_win_layout(P->w(), P->cap_n, P->cap_u).total, s, &ok);
+    P->peer = ok;
+  }
+  pc.mark("window");
   if (e) { delete P; return e; }
   if (h_n_out) *h_n_out = P->n_out;
   if (h_units_out) *h_units_out = P->units_out;
@@ -714,7 +866,7 @@ husky_status husky_sort_multi_plan(void *comm, int coder, const void *d_units, c
 husky_status husky_sort_multi_recv_workspace(void *plan, size_t *bytes) {
   if (!plan || !bytes) return fail(HUSKY_ERR_INVALID_ARG, "null pointer");
   Plan *P = (Plan *)plan;
-  *bytes = make_recv_layout(P->coder, P->n_out, P->units_out).total;
+  *bytes = make_recv_layout(P->coder, P->n_out, P->units_out, !P->peer).total;
   return HUSKY_OK;
 }
 
@@ -728,16 +880,43 @@ husky_status husky_sort_multi_exec(void *plan, uint32_t *d_perm_out, void *d_sor
   Plan *P = (Plan *)plan;
   P->s = (cudaStream_t)stream;
   P->S.s = P->s;
-  RecvLayout R = make_recv_layout(P->coder, P->n_out, P->units_out);
+  RecvLayout R = make_recv_layout(P->coder, P->n_out, P->units_out, !P->peer);
   if (recv_ws_bytes < R.total) return fail(HUSKY_ERR_WORKSPACE, "recv workspace %zu < %zu", recv_ws_bytes, R.total);
   if ((uintptr_t)d_recv_ws % 256) return fail(HUSKY_ERR_INVALID_ARG, "workspace not 256-byte aligned");
+  uint8_t *rws = (uint8_t *)d_recv_ws;
+  Comm *c = P->comm;
   PhaseClock pc(P->s);
-  if (husky_status e = P->phase3()) return e;
-  pc.mark("partition+send buffers");
-  if (husky_status e = nccl_exchange(*P, (uint8_t *)d_recv_ws, R)) return e;
-  pc.mark("exchange");
-  if (husky_status e = P->phase4((uint8_t *)d_recv_ws, R, d_perm_out, d_sorted_units_out, d_sorted_offsets_out, h_out))
+  if (husky_status e = P->partition()) return e;
+  pc.mark("partition");
+  const uint8_t *r_units = rws + R.units;
+  const uint32_t *r_lens = (const uint32_t *)(rws + R.lens), *r_gidx = (const uint32_t *)(rws + R.gidx);
+  if (P->peer) {
+    const WinLayout WL = make_win_layout(P->w(), P->cap_n, P->cap_u);
+    std::vector<unsigned long long> du(P->world), dl(P->world), dg(P->world);
+    for (int q = 0; q < P->world; ++q) {
+      du[q] = c->peer[q] + WL.units;
+      dl[q] = c->peer[q] + WL.lens;
+      dg[q] = c->peer[q] + WL.gidx;
+    }
+    if (husky_status e = P->scatter_peer(du, dl, dg)) return e;
+    pc.mark("scatter to peers");
+    // every rank's stores are done before any rank reads its window
+    NCHECK(ncclAllReduce(c->d_tmp + c->world, c->d_tmp + c->world, 1, ncclUint64, ncclSum, c->nccl, P->s));
+    pc.mark("barrier");
+    const uint8_t *wb = (const uint8_t *)c->win_buf;
+    r_units = wb + WL.units;
+    r_lens = (const uint32_t *)(wb + WL.lens);
+    r_gidx = (const uint32_t *)(wb + WL.gidx);
+  } else {
+    if (husky_status e = P->build_send()) return e;
+    pc.mark("send buffers");
+    if (husky_status e = nccl_exchange(*P, rws, R)) return e;
+    pc.mark("exchange");
+  }
+  if (husky_status e = P->phase4(r_units, r_lens, r_gidx, rws, R, d_perm_out, d_sorted_units_out,
+                                 d_sorted_offsets_out, h_out))
     return e;
+  if (h_out) h_out->exchange = P->peer ? HUSKY_EXCHANGE_PEER : HUSKY_EXCHANGE_NCCL;
   pc.mark("local sort");
   HCHECK(cudaStreamSynchronize(P->s));
   return HUSKY_OK;
@@ -773,7 +952,8 @@ husky_status husky_sort_multi(void *comm, int coder, const void *d_units, const 
     return e;
   if (h_n_out) *h_n_out = n_out;
   if (h_units_out) *h_units_out = u_out;
-  size_t rb = make_recv_layout(coder, n_out, u_out).total;
+  size_t rb = 0;
+  husky_sort_multi_recv_workspace(plan, &rb);
   husky_status e = HUSKY_OK;
   if (n_out > cap_n || u_out > cap_units) e = fail(HUSKY_ERR_CAPACITY, "shard needs %llu strings / %llu units",
                                                    (unsigned long long)n_out, (unsigned long long)u_out);
@@ -804,6 +984,8 @@ husky_status husky_sort_multi_loopback_workspace(int coder, int world, uint64_t 
     tot += align_up(make_multi_layout(coder, nr, total_units, world).total, 256);  // units bound per rank
   }
   tot += align_up(make_recv_layout(coder, n, total_units).total, 256);  // shared recv + sort ws (worst case)
+  // peer-store mode: every virtual rank's receive window (sum of the shards)
+  tot += align_up(total_units * coder_unit_bytes(coder) + n * 8 + (size_t)world * 1024, 256);
   tot += align_up((size_t)world * 256, 256) * world;
   *bytes = tot;
   return HUSKY_OK;
@@ -857,24 +1039,60 @@ husky_status husky_sort_multi_loopback(int coder, int world, const void *d_units
       }
   for (auto &p : P) if (husky_status e = p.choose_splitters()) return e;
   for (auto &p : P) if (husky_status e = p.phase2()) return e;
-  // "all-to-all" of the counts: rcounts[r][q] = counts[q][r]
+  // "all-gather" of the counts: row q of every rank's matrix = rank q's counts
   for (int r = 0; r < world; ++r)
     for (int q = 0; q < world; ++q)
-      HCHECK(cudaMemcpyAsync(P[r].at<uint64_t>(P[r].M.rcounts) + 2 * q, P[q].at<uint64_t>(P[q].M.counts) + 2 * r, 16,
-                             cudaMemcpyDeviceToDevice, s));
+      HCHECK(cudaMemcpyAsync(P[r].at<uint64_t>(P[r].M.rcounts) + (size_t)q * world * 2, P[q].at<uint64_t>(P[q].M.counts),
+                             (size_t)world * 16, cudaMemcpyDeviceToDevice, s));
   for (auto &p : P) if (husky_status e = p.read_counts()) return e;
-  for (auto &p : P) if (husky_status e = p.phase3()) return e;
-  // data exchange + local sorts, one destination rank at a time (shared recv ws)
+  for (auto &p : P) if (husky_status e = p.partition()) return e;
   const size_t w = coder_unit_bytes(coder);
+  // peer-store mode (default): the gather of every virtual rank writes straight
+  // into the destinations' windows (regions of this workspace), exactly as the
+  // NCCL path writes into the NVLink mappings; HUSKY_EXCHANGE=copy: send
+  // buffers + device-to-device copies
+  const bool peer = !exchange_by_nccl();
+  uint8_t *win_all = rws_all + align_up(make_recv_layout(coder, n, total_units).total, 256);
+  std::vector<size_t> win_off(world);
+  std::vector<WinLayout> WLs(world);
+  {
+    size_t o = 0;
+    for (int r = 0; r < world; ++r) {
+      WLs[r] = make_win_layout(w, P[r].n_out, P[r].units_out);
+      win_off[r] = o;
+      o += WLs[r].total;
+    }
+  }
+  if (peer) {
+    std::vector<unsigned long long> du(world), dl(world), dg(world);
+    for (int r = 0; r < world; ++r) {
+      const unsigned long long base = (unsigned long long)(uintptr_t)(win_all + win_off[r]);
+      du[r] = base + WLs[r].units;
+      dl[r] = base + WLs[r].lens;
+      dg[r] = base + WLs[r].gidx;
+    }
+    for (auto &p : P) if (husky_status e = p.scatter_peer(du, dl, dg)) return e;
+  } else {
+    for (auto &p : P) if (husky_status e = p.build_send()) return e;
+  }
+  // data exchange (copy mode) + local sorts, one destination rank at a time (shared recv ws)
   uint64_t out_n = 0, out_u = 0;
   husky_outcome agg;
   memset(&agg, 0, sizeof agg);
   agg.perfect = 1; agg.domain_ok = 1;
   for (int r = 0; r < world; ++r) {
     Plan &dst = P[r];
-    RecvLayout R = make_recv_layout(coder, dst.n_out, dst.units_out);
+    RecvLayout R = make_recv_layout(coder, dst.n_out, dst.units_out, !peer);
+    const uint8_t *r_units = rws_all + R.units;
+    const uint32_t *r_lens = (const uint32_t *)(rws_all + R.lens), *r_gidx = (const uint32_t *)(rws_all + R.gidx);
+    if (peer) {
+      uint8_t *wb = win_all + win_off[r];
+      r_units = wb + WLs[r].units;
+      r_lens = (const uint32_t *)(wb + WLs[r].lens);
+      r_gidx = (const uint32_t *)(wb + WLs[r].gidx);
+    }
     uint64_t ro = 0, ru = 0;
-    for (int q = 0; q < world; ++q) {
+    for (int q = 0; q < world && !peer; ++q) {
       Plan &src = P[q];
       uint64_t so = 0, su = 0;
       for (int k = 0; k < r; ++k) { so += src.send_cnt[k]; su += src.send_u[k]; }
@@ -894,7 +1112,8 @@ husky_status husky_sort_multi_loopback(int coder, int world, const void *d_units
     void *su_out = (d_sorted_units && dst.n_out) ? (uint8_t *)d_sorted_units + out_u * w : nullptr;
     int64_t *so_out = (d_sorted_offsets && dst.n_out) ? d_sorted_offsets + out_n : nullptr;
     // offsets slot out_n is shared with the previous shard's end: write it first
-    if (husky_status e = dst.phase4(rws_all, R, d_perm + out_n, su_out, so_out, &o)) return e;
+    if (husky_status e = dst.phase4(r_units, r_lens, r_gidx, rws_all, R, d_perm + out_n, su_out, so_out, &o))
+      return e;
     if (so_out && out_u && dst.n_out) {
       HUSKY_SCOPE(ST_MULTI, s, 0);
       k_add_base<<<grid_for(dst.n_out + 1), 256, 0, s>>>(so_out, dst.n_out + 1, (int64_t)out_u);
@@ -911,6 +1130,7 @@ husky_status husky_sort_multi_loopback(int coder, int world, const void *d_units
   if (n == 0 && d_sorted_offsets) HCHECK(cudaMemsetAsync(d_sorted_offsets, 0, 8, s));
   HCHECK(cudaStreamSynchronize(s));
   HCHECK(cudaGetLastError());
+  agg.exchange = peer ? HUSKY_EXCHANGE_LOOPBACK_PEER : HUSKY_EXCHANGE_LOOPBACK_COPY;
   if (h_out) *h_out = agg;
   return HUSKY_OK;
 }

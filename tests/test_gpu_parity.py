@@ -300,12 +300,15 @@ def test_sort_repeatable_and_workspace_reuse(torch, h):
 
 
 # ------------------------------------------------------- sharded (loopback)
+@pytest.mark.parametrize("exchange", ["peer", "copy"])
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
 @pytest.mark.parametrize("name,n", [("C1", 60_000), ("C3", 100_000), ("C4", 50_000), ("C2", 80_000)])
-def test_multi_loopback_vs_oracle(torch, h, oracle_mod, world, name, n):
+def test_multi_loopback_vs_oracle(torch, h, oracle_mod, monkeypatch, exchange, world, name, n):
     """Sample sort over `world` virtual ranks on one GPU: concatenation of the
     shards == oracle; equal strings never straddle shards; shard sizes follow
-    the splitter rule; C4 (all codes equal) spreads evenly."""
+    the splitter rule; C4 (all codes equal) spreads evenly.  Both transports:
+    the peer-store gather into per-rank windows (NEXT-2) and copies."""
+    monkeypatch.setenv("HUSKY_EXCHANGE", exchange)
     w = W.make(name, n)
     u, o = to_dev(torch, w)
     tot = w.units.size
@@ -315,6 +318,7 @@ def test_multi_loopback_vs_oracle(torch, h, oracle_mod, world, name, n):
     su = torch.empty(tot + 8, dtype=u.dtype, device="cuda")
     so = torch.empty(w.n + 1, dtype=torch.int64, device="cuda")
     shards, outc = h.husky_sort_multi_loopback(w.coder, world, u, o, perm, su, so, ws)
+    assert outc["exchange"] == (4 if exchange == "peer" else 3)
     assert sum(shards) == w.n
     p = perm.cpu().numpy().view(np.uint32)
     ref = oracle_mod.sort(w.coder, w.units, w.offsets)
@@ -362,19 +366,64 @@ def expected_shards(h, w, world, s=4096, cap=32):
     return counts
 
 
-def test_multi_nccl_single_rank(torch, h, oracle_mod):
-    """The NCCL plan/exec path with a one-rank communicator."""
-    w = W.make("C1", 30_000)
-    u, o = to_dev(torch, w)
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+def test_multi_nccl_single_rank(torch, h, oracle_mod, monkeypatch, exchange):
+    """The NCCL plan/exec path with a one-rank communicator, through the
+    symmetric-window peer stores (NEXT-2) and through ncclSend/ncclRecv; the
+    window is reused and grown across calls of different sizes."""
+    monkeypatch.setenv("HUSKY_EXCHANGE", exchange)
     uid = h.husky_comm_unique_id()
     comm = h.husky_comm_create(0, 1, uid)
     try:
-        perm, su, so, outc = h.sort_multi(comm, w.coder, u, o, 0)
-        torch.cuda.synchronize()
-        ref = oracle_mod.sort(w.coder, w.units, w.offsets)
-        assert np.array_equal(perm.cpu().numpy().view(np.uint32), ref)
+        for name, n in (("C1", 30_000), ("C3", 20_000), ("C2", 90_000)):
+            w = W.make(name, n)
+            u, o = to_dev(torch, w)
+            perm, su, so, outc = h.sort_multi(comm, w.coder, u, o, 0)
+            torch.cuda.synchronize()
+            assert outc["exchange"] == (2 if exchange == "peer" else 1)
+            ref = oracle_mod.sort(w.coder, w.units, w.offsets)
+            assert np.array_equal(perm.cpu().numpy().view(np.uint32), ref)
+            rsu, rso = oracle_mod.gather(w.coder, w.units, w.offsets, ref)
+            s_u = su.cpu().numpy()
+            if w.coder == UNICODE:
+                s_u = s_u.view(np.uint16)
+            assert np.array_equal(so.cpu().numpy(), rso) and np.array_equal(s_u[:rsu.size], rsu)
     finally:
         h.husky_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("world", [3, 7])
+def test_multi_loopback_peer_edges(torch, h, oracle_mod, monkeypatch, world):
+    """Peer-store exchange edge cases: empty buckets (half the strings equal),
+    empty strings, strings longer than the gather's shared-memory window (one
+    tile over several windows, bucket boundaries inside a window)."""
+    monkeypatch.setenv("HUSKY_EXCHANGE", "peer")
+    rng = np.random.default_rng(world)
+    strings = []
+    for i in range(30_000):
+        r = rng.random()
+        if r < 0.5:
+            strings.append([0x61, 0x62, 0x63])
+        elif r < 0.55:
+            strings.append([])
+        elif r < 0.56:
+            strings.append(rng.integers(0x61, 0x7B, size=int(rng.integers(2000, 9000))).tolist())
+        else:
+            strings.append(rng.integers(0x61, 0x65, size=int(rng.integers(1, 30))).tolist())
+    w = W.from_strings(strings, ASCII)
+    u, o = to_dev(torch, w)
+    tot = w.units.size
+    ws = torch.empty(h.husky_sort_multi_loopback_workspace(w.coder, world, w.n, tot), dtype=torch.uint8,
+                     device="cuda")
+    perm = torch.empty(w.n, dtype=torch.int32, device="cuda")
+    su = torch.empty(tot + 8, dtype=u.dtype, device="cuda")
+    so = torch.empty(w.n + 1, dtype=torch.int64, device="cuda")
+    shards, outc = h.husky_sort_multi_loopback(w.coder, world, u, o, perm, su, so, ws)
+    assert outc["exchange"] == 4 and sum(shards) == w.n
+    ref = oracle_mod.sort(w.coder, w.units, w.offsets)
+    assert np.array_equal(perm.cpu().numpy().view(np.uint32), ref)
+    rsu, rso = oracle_mod.gather(w.coder, w.units, w.offsets, ref)
+    assert np.array_equal(so.cpu().numpy(), rso) and np.array_equal(su[:tot].cpu().numpy(), rsu)
 
 
 def test_sort_host_many_pipelined(torch, h, oracle_mod):
