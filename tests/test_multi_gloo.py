@@ -14,6 +14,7 @@ import socket
 
 import numpy as np
 import pytest
+import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -61,13 +62,35 @@ def _worker(rank, world, port, name, n, q):
             idx = np.nonzero(bucket == d)[0]
             strs = [units[off[i]:off[i + 1]] for i in idx]
             send.append((strs, (lo + idx).astype(np.int64)))
-        recv = [None] * world
+        # the count matrix is all-gathered (row q = rank q's (strings, units) per
+        # destination); a rank's displacement in destination d's window is the
+        # sum of rows q < rank, column d -- the peer-store exchange (NEXT-2)
+        cnt = torch.tensor([[len(send[d][0]), int(sum(len(x) for x in send[d][0]))] for d in range(world)],
+                           dtype=torch.int64)
+        mat = [torch.zeros_like(cnt) for _ in range(world)]
+        dist.all_gather(mat, cnt)
+        mat = torch.stack(mat).numpy()  # [src][dst][2]
+        disp_n = mat[:rank, :, 0].sum(axis=0)
+        disp_u = mat[:rank, :, 1].sum(axis=0)
+        n_in, u_in = int(mat[:, rank, 0].sum()), int(mat[:, rank, 1].sum())
+        # window of this rank, filled by every source at its displacement
+        win_lens = np.full(n_in, -1, np.int64)
+        win_gidx = np.full(n_in, -1, np.int64)
+        win_units = np.full(u_in, -1, np.int64)
         for src in range(world):
-            obj = [send] if src == rank else [None]
+            obj = [[(disp_n[d], disp_u[d], send[d]) for d in range(world)]] if src == rank else [None]
             dist.broadcast_object_list(obj, src=src)
-            recv[src] = obj[0][rank]
-        strs = [s for r in recv for s in r[0]]
-        gidx = np.concatenate([r[1] for r in recv]) if strs else np.zeros(0, np.int64)
+            dn, du, (strs_s, gidx_s) = obj[0][rank]
+            for k, x in enumerate(strs_s):
+                assert win_lens[dn + k] == -1  # no overlap
+                win_lens[dn + k] = len(x)
+                win_gidx[dn + k] = gidx_s[k]
+                win_units[du:du + len(x)] = x
+                du += len(x)
+        assert (win_lens >= 0).all() and (win_units >= 0).all()  # no gap
+        ends = np.concatenate([[0], np.cumsum(win_lens)])
+        strs = [win_units[ends[i]:ends[i + 1]].astype(units.dtype) for i in range(n_in)]
+        gidx = win_gidx
         assert np.all(np.diff(gidx) > 0)  # source-rank order == ascending global index
         lw = W.from_strings([list(s) for s in strs], wl.coder)
         lperm = oracle.sort(wl.coder, lw.units, lw.offsets) if strs else np.zeros(0, np.uint32)
