@@ -52,6 +52,11 @@ struct GatherRuns {
 
 template <int CODER, bool PACKED, bool CHECK, bool PEER>
 // 5 CTAs/SM (48 registers): measured 280 vs 289 us (4/SM) and 298 us (6/SM) on C2
+// L1 prefetch of the long strings' units: 0 = as soon as the offset is loaded
+// (before the block scan), 1 = after the tile's aggregate is published, 2 = none
+#ifndef HUSKY_GATHER_PF
+#define HUSKY_GATHER_PF 1
+#endif
 #ifndef HUSKY_GATHER_MINB
 #define HUSKY_GATHER_MINB 5
 #endif
@@ -141,15 +146,20 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
         len[j] = lc;
         sv[j] = CHECK ? cc[j] : __ldg(codes + p0 + j);
       } else {
-        int64_t a = __ldg(offsets + idx), b = __ldg(offsets + idx + 1);
+        const int64_t a = __ldg(offsets + idx);
         sv[j] = (uint64_t)a;
-        len[j] = (uint32_t)(b - a);
+        // a packed length below 15 is exact: the scan need not wait for the
+        // offsets load, whose value is first used by the staging
+        if (PACKED && lc < 15) len[j] = lc;
+        else len[j] = (uint32_t)(__ldg(offsets + idx + 1) - a);
+#if HUSKY_GATHER_PF == 0
         // the staging reads these units after the block scan: start the fetch now
         if ((PEER || sorted_units) && len[j]) {
           const uint8_t *pa = (const uint8_t *)units + (uint64_t)a * W;
           asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
           if ((((uintptr_t)pa & 127) + (uint64_t)len[j] * W) > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 127));
         }
+#endif
       }
     }
     mine += len[j];
@@ -197,6 +207,19 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
     if (CHECK) st_relaxed_u64(runs.lb + tile, make_flag(tile == 0 ? kFlagInc : kFlagAgg, epoch, tile_runs));
   }
 
+#if HUSKY_GATHER_PF == 1
+  // the long strings' units, for the staging below (issued after the publish)
+  if (PEER || sorted_units) {
+#pragma unroll
+    for (int j = 0; j < kGatherItems; ++j) {
+      if (p0 + j < n && !((dec >> j) & 1) && len[j]) {
+        const uint8_t *pa = (const uint8_t *)units + sv[j] * W;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
+        if ((((uintptr_t)pa & 127) + (uint64_t)len[j] * W) > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 127));
+      }
+    }
+  }
+#endif
   const uint8_t *ub = (const uint8_t *)units;
   uint8_t *ob = (uint8_t *)sorted_units;
   const uint64_t tile_bytes = tile_total * W;
@@ -276,6 +299,21 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
     s_lidx[tid] = ix[kGatherItems - 1];
     s_loff[tid] = excl_t + mine - len[kGatherItems - 1];
   }
+  // CHECK: the order check needs the stage and the neighbours' last items but
+  // no look-back.  Warps 0 / 1 (the look-back warps) only signal that their
+  // strings are staged (bar.arrive) and start walking at once; warps 2.. wait
+  // for every warp's stage (bar.sync on the same named barrier) and compare
+  // meanwhile; warps 0 / 1 compare after their walks
+  uint32_t bad = 0;
+  if (CHECK) {
+    static_assert(kGatherThreads == 256, "named-barrier thread counts");
+    if (warp < 2) {
+      asm volatile("bar.arrive 1, 256;" ::: "memory");
+      asm volatile("bar.sync 2, 64;" ::: "memory");  // warp 1's first pair reads warp 0's last string
+    } else {
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
+  }
   if (warp == 0) {
     unsigned long long ex =
         tile == 0 ? 0ull : ((dbg & 2) ? lookback(lb, tile, 1, epoch) : warp_lookback(lb, tile, epoch));
@@ -290,30 +328,6 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       if (tile != 0) st_relaxed_u64(runs.lb + tile, make_flag(kFlagInc, epoch, ex + tile_runs));
       s_rbase = ex;
       if ((uint64_t)(tile + 1) * kGatherTile >= n) runs.st->n_runs = (uint32_t)(ex + tile_runs);
-    }
-  }
-  __syncthreads();
-  GT(tile, 3);
-  const unsigned long long tbase = gbase + s_base;  // units before this tile
-  if (!PEER) {
-    unsigned long long d = tbase + excl_t;
-#pragma unroll
-    for (int j = 0; j < kGatherItems; ++j) {
-      if (p0 + j < n) sorted_offsets[p0 + j] = (int64_t)d;
-      d += len[j];
-    }
-  } else if (p0 < n) {
-    // length and global index of each string, into its destination's arrays
-    uint32_t b = 0;
-    while (b + 1 < peer->world && s_sn[b + 1] <= p0) ++b;
-#pragma unroll
-    for (int j = 0; j < kGatherItems; ++j) {
-      const uint64_t p = p0 + j;
-      if (p < n) {
-        while (s_sn[b + 1] <= p) ++b;
-        reinterpret_cast<uint32_t *>(peer->lens[b])[p] = len[j];
-        reinterpret_cast<uint32_t *>(peer->gidx[b])[p] = peer->gbase + ix[j];
-      }
     }
   }
   if (CHECK) {
@@ -332,7 +346,6 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       pc = ~cc[0]; pl = 0; pi = 0; po = ~0ull;  // position 0: no pair
     }
     unsigned long long d = excl_t;
-    uint32_t bad = 0;
 #pragma unroll
     for (int j = 0; j < kGatherItems; ++j) {
       if ((eqp >> j) & 1) {
@@ -366,6 +379,32 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       pc = cc[j]; pl = len[j]; pi = ix[j]; po = d;
       d += len[j];
     }
+  }
+  __syncthreads();
+  GT(tile, 3);
+  const unsigned long long tbase = gbase + s_base;  // units before this tile
+  if (!PEER) {
+    unsigned long long d = tbase + excl_t;
+#pragma unroll
+    for (int j = 0; j < kGatherItems; ++j) {
+      if (p0 + j < n) sorted_offsets[p0 + j] = (int64_t)d;
+      d += len[j];
+    }
+  } else if (p0 < n) {
+    // length and global index of each string, into its destination's arrays
+    uint32_t b = 0;
+    while (b + 1 < peer->world && s_sn[b + 1] <= p0) ++b;
+#pragma unroll
+    for (int j = 0; j < kGatherItems; ++j) {
+      const uint64_t p = p0 + j;
+      if (p < n) {
+        while (s_sn[b + 1] <= p) ++b;
+        reinterpret_cast<uint32_t *>(peer->lens[b])[p] = len[j];
+        reinterpret_cast<uint32_t *>(peer->gidx[b])[p] = peer->gbase + ix[j];
+      }
+    }
+  }
+  if (CHECK) {
     // runs: the k-th start and the k-th end of the array belong to run k
     if (eqp | eqn) {
       uint32_t rid = (uint32_t)s_rbase + excl_r - 1;
