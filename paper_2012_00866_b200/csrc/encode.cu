@@ -179,36 +179,6 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__
   }
 }
 
-// The 8 digit histograms (kSlotBits-bit digits) of the codes for the LSD
-// onesweep (A2): one read of the codes, plain shared-memory atomics.  Measured on C2: 35 us as a
-// separate pass vs 51 us when fused into the encoder's loop, and 8x slower with
-// __match_any_sync aggregation.
-__global__ void __launch_bounds__(512) k_hist_slots(const uint64_t *__restrict__ keys, uint64_t n, DevState *st) {
-  constexpr int R = 1 << kSlotBits;
-  constexpr uint32_t M = R - 1;
-  __shared__ uint32_t h[8 * R];
-  for (int i = threadIdx.x; i < 8 * R; i += blockDim.x) h[i] = 0;
-  __syncthreads();
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * 4; base < n; base += stride) {
-    uint64_t k[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const uint64_t i = base + threadIdx.x + (uint64_t)r * blockDim.x;
-      k[r] = i < n ? __ldg(keys + i) : 0;
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (base + threadIdx.x + (uint64_t)r * blockDim.x >= n) continue;
-#pragma unroll
-      for (int d = 0; d < 8; ++d) atomicAdd(&h[d * R + ((uint32_t)(k[r] >> (kSlotBits * d)) & M)], 1u);
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 8 * R; i += blockDim.x)
-    if (h[i]) atomicAdd(&st->hist[i / R][i % R], h[i]);
-}
-
 void launch_encode(int coder, bool hist, const void *units, const int64_t *offsets, uint64_t n,
                    uint64_t *codes, DevState *st, int num_sms, cudaStream_t s, uint32_t *packed) {
   if (n == 0) return;
@@ -233,13 +203,6 @@ void launch_encode(int coder, bool hist, const void *units, const int64_t *offse
     }
   }
   if (hist) launch_hist_slots(codes, n, st, num_sms, s);
-}
-
-void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s) {
-  if (n == 0) return;
-  Scope sc_(ST_HIST_SCAN, s, n);
-  const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * 2);
-  k_hist_slots<<<(unsigned)blocks, 512, 0, s>>>(keys, n, st);
 }
 
 }  // namespace husky

@@ -226,15 +226,13 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
       GroupScope grp(ST_ENCODE, s);
       launch_encode(coder, false, d_units, d_offsets, n, S.keysA(), st, S.sms, s, packed_payload);
     }
-    launch_hist_slots(S.keysA(), n, st, S.sms, s);
-    launch_hist_scan(n, st, s, kSlotBits);
+    launch_hist_plan(keysA, n, st, keysA, keysB, S.sms, s);
 
     // ---- A2 key sort, LSD onesweep: (code, index) -> sorted codes, perm.  The
     // pass plan (which digits are not shared by all keys) is made on device, so
     // the host enqueues all 8 pass slots without waiting; slots beyond the plan
     // exit at once.  Input violations (bad offsets, ASCII domain) make every
     // later kernel a no-op and are reported at the single synchronisation below.
-    launch_radix_plan(st, keysA, keysB, n, s);
     {
       GroupScope grp(ST_RADIX, s);  // profiler mode 2: the 8 pass slots as one timed group
       for (int slot = 0; slot < 8; ++slot)

@@ -86,9 +86,10 @@ struct DevState {
   uint32_t seg_L;             // refinement: common-prefix length of the segment
   uint32_t seg_has_short;     // refinement: segment contains a string with len <= PL
   unsigned long long runs_total; // runs found by the main (code) scan
-  // device-side radix plan (k_radix_plan): the non-trivial digits in pass order
+  // device-side radix plan (launch_hist_plan): the non-trivial digits in pass order
   // and which ping-pong key buffer ends up holding the sorted codes
   uint32_t np;
+  uint32_t hist_done;       // k_hist_slots<true>: CTAs that have added their histograms
   uint32_t pass_digit[8];
   uint32_t pass_ballot[8];  // rank a pass with per-bit ballots instead of __match_any_sync
   uint32_t digit_spread[8]; // k_hist_scan: digit d's largest bin holds < 5% of the keys

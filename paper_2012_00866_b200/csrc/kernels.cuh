@@ -19,6 +19,9 @@ void launch_encode(int coder, bool hist, const void *units, const int64_t *offse
                    uint64_t *codes, DevState *st, int num_sms, cudaStream_t s, uint32_t *packed = nullptr);
 // 8 digit histograms (kSlotBits-bit digits) of n keys into DevState::hist (accumulates)
 void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s);
+// histograms + k_hist_scan + the pass plan fused (the last CTA scans and plans)
+void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *keysA, uint64_t *keysB,
+                      int num_sms, cudaStream_t s);
 
 // A2 onesweep radix
 // 512 threads x 8 keys = 4096-key tiles, 64 KB smem, <= 64 registers -> 2 CTAs
@@ -41,11 +44,11 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
                      uint32_t *vals_out, uint64_t n, int digit, DevState *st,
                      unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
 void launch_iota(uint32_t *perm, uint64_t n, cudaStream_t s);
-// Device-planned passes (kSlotBits-bit digits, no host sync): k_radix_plan turns the trivial-digit
-// mask into DevState::np / pass_digit / sorted_keys; slots 0..7 are launched
-// unconditionally and resolve their digit and ping-pong buffers on device (the
-// last planned pass writes vals_final); finalize copies the payload when np == 0.
-void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint64_t n, cudaStream_t s);
+// Device-planned passes (kSlotBits-bit digits, no host sync): the last CTA of
+// launch_hist_plan turns the trivial-digit mask into DevState::np / pass_digit /
+// sorted_keys; slots 0..7 are launched unconditionally and resolve their digit
+// and ping-pong buffers on device (the last planned pass writes vals_final);
+// finalize copies the payload when np == 0.
 void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint32_t *vals_init,
                           uint32_t *vals_final, uint32_t *vals_tmp, uint64_t n, DevState *st,
                           unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);

@@ -84,9 +84,7 @@ husky_status husky_sort_keys(int key_type, const void *d_keys, uint64_t n, uint3
     HUSKY_SCOPE(ST_ENCODE, s, n);
     k_key_encode<<<grid_n(n, S.sms), 256, 0, s>>>(key_type, (const uint64_t *)d_keys, n, keysA);
   }
-  launch_hist_slots(keysA, n, st, S.sms, s);
-  launch_hist_scan(n, st, s, kSlotBits);
-  launch_radix_plan(st, keysA, keysB, n, s);
+  launch_hist_plan(keysA, n, st, keysA, keysB, S.sms, s);
   for (int slot = 0; slot < 8; ++slot)
     launch_onesweep_slot(slot, keysA, keysB, nullptr, d_perm, S.at<uint32_t>(L.vals), n, st, S.lb_radix(),
                          S.next_counter(), S.next_epoch(), s);

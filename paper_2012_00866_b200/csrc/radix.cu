@@ -27,6 +27,8 @@
 //     turns them into per-tile bases, and the downsweep ranks/exchanges/scatters
 //     with no inter-tile dependency (measured slower).
 // Digits whose histogram puts all keys in one bucket are skipped.
+#include <algorithm>
+
 #include "husky_internal.cuh"
 #include "kernels.cuh"
 
@@ -63,6 +65,104 @@ void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s, int bits) {
   else k_hist_scan<8><<<8, 256, 0, s>>>(n, st);
 }
 
+// The 8 digit histograms (kSlotBits-bit digits) of the codes for the LSD
+// onesweep (A2): one read of the codes, plain shared-memory atomics.  Measured
+// on C2: 35 us as a separate pass vs 51 us when fused into the encoder's loop,
+// and 8x slower with __match_any_sync aggregation.  PLAN: the
+// last CTA to add its histograms (ticket) also does k_hist_scan's scans and
+// the pass plan (which digits to sort, in which order, with which ranking
+// primitive), saving two dependent launches.
+template <bool PLAN>
+__global__ void __launch_bounds__(512) k_hist_slots(const uint64_t *__restrict__ keys, uint64_t n, DevState *st,
+                                                    uint64_t *keysA, uint64_t *keysB, uint32_t force_ballot,
+                                                    uint32_t force_match) {
+  constexpr int R = 1 << kSlotBits;
+  constexpr uint32_t M = R - 1;
+  __shared__ uint32_t h[8 * R];
+  __shared__ uint32_t s_last, s_wt[512 / 32 + 1], s_max[512 / 32];
+  for (int i = threadIdx.x; i < 8 * R; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * 4; base < n; base += stride) {
+    uint64_t k[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint64_t i = base + threadIdx.x + (uint64_t)r * blockDim.x;
+      k[r] = i < n ? __ldg(keys + i) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (base + threadIdx.x + (uint64_t)r * blockDim.x >= n) continue;
+#pragma unroll
+      for (int d = 0; d < 8; ++d) atomicAdd(&h[d * R + ((uint32_t)(k[r] >> (kSlotBits * d)) & M)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 8 * R; i += blockDim.x)
+    if (h[i]) atomicAdd(&st->hist[i / R][i % R], h[i]);
+  if (!PLAN) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&st->hist_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // the last CTA: exclusive scans, trivial digits, spread (as k_hist_scan), then the plan
+  uint32_t trivial = 0, spread = 0;
+  for (int d = 0; d < 8; ++d) {
+    const uint32_t v = threadIdx.x < R ? __ldcg(&st->hist[d][threadIdx.x]) : 0u;
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan<uint32_t, 512>(v, &total, s_wt);
+    if (threadIdx.x < R) st->digit_start[d][threadIdx.x] = ex;
+    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, v);
+    if (lane_id() == 0) s_max[threadIdx.x >> 5] = m;
+    const bool all_here = __syncthreads_or((uint64_t)v == n) != 0;
+    uint32_t mx = 0;
+    for (int w = 0; w < 512 / 32; ++w) mx = s_max[w] > mx ? s_max[w] : mx;
+    trivial |= (uint32_t)all_here << d;
+    spread |= (uint32_t)((uint64_t)mx * 20 < n) << d;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    st->trivial_mask = trivial;
+    uint32_t np = 0;
+    for (int d = 0; d < 8; ++d) {
+      st->digit_spread[d] = (spread >> d) & 1;
+      if (!((trivial >> d) & 1)) {
+        st->pass_ballot[np] = ((force_ballot >> d) & 1) || (((spread >> d) & 1) && !((force_match >> d) & 1));
+        st->pass_digit[np++] = d;
+      }
+    }
+    st->np = np;
+    st->sorted_keys = (unsigned long long)((np & 1) ? keysB : keysA);
+  }
+}
+
+static uint32_t env_mask(const char *name) {
+  const char *v = getenv(name);
+  return v ? (uint32_t)strtoul(v, nullptr, 0) : 0u;
+}
+
+void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s) {
+  if (n == 0) return;
+  Scope sc_(ST_HIST_SCAN, s, n);
+  const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * 2);
+  k_hist_slots<false><<<(unsigned)blocks, 512, 0, s>>>(keys, n, st, nullptr, nullptr, 0, 0);
+}
+
+// histograms + scans + pass plan of the device-planned passes in one launch
+// (DevState::hist_done must be 0: DevState is zeroed per sort)
+void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *keysA, uint64_t *keysB,
+                      int num_sms, cudaStream_t s) {
+  if (n == 0) return;
+  Scope sc_(ST_HIST_SCAN, s, n);
+  // experiments: HUSKY_RANK_BALLOT / HUSKY_RANK_MATCH = digit bit masks that
+  // force one primitive (default: the plan's < 5% largest-bin rule)
+  static const uint32_t force_ballot = env_mask("HUSKY_RANK_BALLOT"), force_match = env_mask("HUSKY_RANK_MATCH");
+  const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * 2);
+  k_hist_slots<true><<<(unsigned)blocks, 512, 0, s>>>(keys, n, st, keysA, keysB, force_ballot, force_match);
+}
+
 constexpr int kRadixWarps = kRadixThreads / 32;
 #ifndef RADIX_LB_W
 #define RADIX_LB_W 8
@@ -85,24 +185,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // dynamic smem of a pass: key/value exchange buffer + per-warp digit counters
 template <int BITS>
 constexpr int exchange_bytes() { return kRadixTile * (8 + 4) + kRadixWarps * (1 << BITS) * 4; }
-
-// Device-side pass plan: lets the host launch all 8 pass slots without
-// reading the trivial-digit mask back (no host synchronisation).  Also picks
-// each pass's ranking primitive from k_hist_scan's digit_spread: a digit whose
-// largest bin holds < 5% of the keys (many distinct labels per warp) is ranked
-// with per-bit ballots, the rest with __match_any_sync -- measured per digit on
-// C2 / C3.
-__global__ void k_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint32_t force_ballot,
-                             uint32_t force_match) {
-  uint32_t m = st->trivial_mask, np = 0;
-  for (int d = 0; d < 8; ++d)
-    if (!((m >> d) & 1)) {
-      st->pass_ballot[np] = ((force_ballot >> d) & 1) || (st->digit_spread[d] && !((force_match >> d) & 1));
-      st->pass_digit[np++] = d;
-    }
-  st->np = np;
-  st->sorted_keys = (unsigned long long)((np & 1) ? keysB : keysA);
-}
 
 // all digits trivial: the permutation is the payload as it stands
 __global__ void k_radix_finalize(const DevState *st, const uint32_t *v_init, uint32_t *v_final, uint64_t n) {
@@ -378,18 +460,6 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
   else
     k_onesweep<false, false, 8><<<g, b, kX, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds, lb,
                                                  tile_counter, epoch, counts, tiles, nullptr, 0, sp);
-}
-
-void launch_radix_plan(DevState *st, uint64_t *keysA, uint64_t *keysB, uint64_t n, cudaStream_t s) {
-  Scope sc_(ST_HIST_SCAN, s, 0);
-  // experiments: HUSKY_RANK_BALLOT / HUSKY_RANK_MATCH = digit bit masks that
-  // force one primitive (default: the plan's < 5% largest-bin rule)
-  auto env_mask = [](const char *name) {
-    const char *v = getenv(name);
-    return v ? (uint32_t)strtoul(v, nullptr, 0) : 0u;
-  };
-  static const uint32_t force_ballot = env_mask("HUSKY_RANK_BALLOT"), force_match = env_mask("HUSKY_RANK_MATCH");
-  k_radix_plan<<<1, 1, 0, s>>>(st, keysA, keysB, force_ballot, force_match);
 }
 
 // Pass slot `slot` (0..7) of the device-side plan (kSlotBits-bit digits).
