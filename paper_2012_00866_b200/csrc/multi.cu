@@ -699,6 +699,15 @@ static husky_status ensure_window(Comm *c, size_t need, cudaStream_t s, bool *ok
   c->peer.assign(c->world, 0);
   HCHECK(cudaMemcpyAsync(c->peer.data(), c->d_tmp, (size_t)c->world * 8, cudaMemcpyDeviceToHost, s));
   HCHECK(cudaStreamSynchronize(s));
+  // every peer must be load/store reachable (one NVLink / NVSwitch domain)
+  mine = std::all_of(c->peer.begin(), c->peer.end(), [](unsigned long long a) { return a != 0; });
+  if (husky_status e = all_ranks_ok(c, s, mine, &all)) return e;
+  if (!all) {
+    release_window(c);
+    c->win_failed = true;
+    fprintf(stderr, "[husky] a peer window is not load/store reachable: exchanging by NCCL send/recv\n");
+    return HUSKY_OK;
+  }
   *ok = true;
   return HUSKY_OK;
 }
