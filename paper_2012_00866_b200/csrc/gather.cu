@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   // PEER: the buckets' start positions / units in the partitioned order
   __shared__ unsigned long long s_sn[PEER ? kMaxPeers + 1 : 1], s_su[PEER ? kMaxPeers + 1 : 1];
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  pdl_wait();  // the main gather is a programmatic dependent of the key sort
   if (PEER) {
     for (uint32_t b = tid; b <= peer->world; b += kGatherThreads) {
       s_sn[b] = peer->start_n[b];
@@ -483,18 +484,18 @@ void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, con
   const bool chk = runs_out != nullptr;
   if (coder == HUSKY_CODER_ASCII) {
     if (packed) {
-      if (chk) k_gather<HUSKY_CODER_ASCII, true, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) launch_pdl(k_gather<HUSKY_CODER_ASCII, true, true, false>, g, b, kSmem, s, G_ARGS);
       else k_gather<HUSKY_CODER_ASCII, true, false, false><<<g, b, kSmem, s>>>(G_ARGS);
     } else {
-      if (chk) k_gather<HUSKY_CODER_ASCII, false, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) launch_pdl(k_gather<HUSKY_CODER_ASCII, false, true, false>, g, b, kSmem, s, G_ARGS);
       else k_gather<HUSKY_CODER_ASCII, false, false, false><<<g, b, kSmem, s>>>(G_ARGS);
     }
   } else {
     if (packed) {
-      if (chk) k_gather<HUSKY_CODER_UNICODE, true, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) launch_pdl(k_gather<HUSKY_CODER_UNICODE, true, true, false>, g, b, kSmem, s, G_ARGS);
       else k_gather<HUSKY_CODER_UNICODE, true, false, false><<<g, b, kSmem, s>>>(G_ARGS);
     } else {
-      if (chk) k_gather<HUSKY_CODER_UNICODE, false, true, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) launch_pdl(k_gather<HUSKY_CODER_UNICODE, false, true, false>, g, b, kSmem, s, G_ARGS);
       else k_gather<HUSKY_CODER_UNICODE, false, false, false><<<g, b, kSmem, s>>>(G_ARGS);
     }
   }

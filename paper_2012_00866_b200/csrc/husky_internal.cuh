@@ -115,6 +115,9 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+// programmatic dependent launch: wait for the preceding kernel's results (a
+// no-op for kernels launched without the PDL attribute)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Lanes holding the same 8-bit label as this lane (converged warp): one ballot
 // per label bit -- an alternative to __match_any_sync whose cost on sm_100a

@@ -167,4 +167,31 @@ void launch_regather_runs(int coder, const uint2 *list_sm, uint64_t cap_sm, cons
                           void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s,
                           uint32_t first_small = 0, uint32_t first_medium = 0);
 
+// Programmatic dependent launch (PDL): the kernel's CTAs may become resident
+// while the previous kernel in the stream drains; the kernel must execute
+// `griddepcontrol.wait` (pdl_wait) before touching that kernel's results.
+// HUSKY_PDL=0 launches plainly (the wait is then a no-op).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("HUSKY_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 }  // namespace husky

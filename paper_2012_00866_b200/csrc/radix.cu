@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(512) k_hist_slots(const uint64_t *__restrict__
                                                     uint32_t force_match) {
   constexpr int R = 1 << kSlotBits;
   constexpr uint32_t M = R - 1;
+  pdl_wait();  // PLAN: launched as a programmatic dependent of the encoder
   __shared__ uint32_t h[8 * R];
   __shared__ uint32_t s_last, s_wt[512 / 32 + 1], s_max[512 / 32];
   for (int i = threadIdx.x; i < 8 * R; i += blockDim.x) h[i] = 0;
@@ -160,7 +161,8 @@ void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *
   // force one primitive (default: the plan's < 5% largest-bin rule)
   static const uint32_t force_ballot = env_mask("HUSKY_RANK_BALLOT"), force_match = env_mask("HUSKY_RANK_MATCH");
   const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * 2);
-  k_hist_slots<true><<<(unsigned)blocks, 512, 0, s>>>(keys, n, st, keysA, keysB, force_ballot, force_match);
+  launch_pdl(k_hist_slots<true>, dim3((unsigned)blocks), dim3(512), 0, s, keys, n, st, keysA, keysB, force_ballot,
+             force_match);
 }
 
 constexpr int kRadixWarps = kRadixThreads / 32;
@@ -188,6 +190,7 @@ constexpr int exchange_bytes() { return kRadixTile * (8 + 4) + kRadixWarps * (1 
 
 // all digits trivial: the permutation is the payload as it stands
 __global__ void k_radix_finalize(const DevState *st, const uint32_t *v_init, uint32_t *v_final, uint64_t n) {
+  pdl_wait();
   if (st->np != 0) return;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     v_final[i] = v_init ? v_init[i] : (uint32_t)i;
@@ -217,6 +220,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   // as measured by k_hist_scan; planned slots: the plan's choice
   constexpr uint32_t R = 1u << BITS, MASK = R - 1;
   static_assert(R <= kRadixThreads, "one digit per thread");
+  pdl_wait();  // the pass slots are programmatic dependents of the previous kernel
   bool use_ballot = !plan && sp.st && sp.st->digit_spread[shift / BITS];
   if (plan) {
     const uint32_t np = plan->np;
@@ -475,15 +479,15 @@ void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint
     cudaFuncSetAttribute(k_onesweep<false, true, kSlotBits>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
     configured = true;
   }
+  // programmatic dependent launch: the pass's CTAs become resident while the
+  // previous kernel's last wave drains and start as soon as it completes
   Scope sc_(ST_RADIX, s, n);
   const uint32_t tiles = (uint32_t)radix_tiles(n);
   SlotPtrs sp{keysA, keysB, vals_init, vals_final, vals_tmp, nullptr};
-  if (slot == 0 && vals_init == nullptr)
-    k_onesweep<true, true, kSlotBits><<<tiles, kRadixThreads, kX, s>>>(
-        nullptr, nullptr, nullptr, nullptr, n, 0, nullptr, lb, tile_counter, epoch, nullptr, tiles, st, slot, sp);
-  else
-    k_onesweep<false, true, kSlotBits><<<tiles, kRadixThreads, kX, s>>>(
-        nullptr, nullptr, nullptr, nullptr, n, 0, nullptr, lb, tile_counter, epoch, nullptr, tiles, st, slot, sp);
+  auto k = (slot == 0 && vals_init == nullptr) ? k_onesweep<true, true, kSlotBits> : k_onesweep<false, true, kSlotBits>;
+  launch_pdl(k, dim3(tiles), dim3(kRadixThreads), kX, s, (const uint64_t *)nullptr, (const uint32_t *)nullptr,
+             (uint64_t *)nullptr, (uint32_t *)nullptr, n, 0, (const uint32_t *)nullptr, lb, tile_counter, epoch,
+             (const uint32_t *)nullptr, tiles, (const DevState *)st, slot, sp);
 }
 
 void launch_radix_finalize(const DevState *st, const uint32_t *vals_init, uint32_t *vals_final, uint64_t n,
@@ -492,7 +496,7 @@ void launch_radix_finalize(const DevState *st, const uint32_t *vals_init, uint32
   Scope sc_(ST_RADIX, s, 0);
   uint64_t blocks = (n + 255) / 256;
   if (blocks > 2048) blocks = 2048;
-  k_radix_finalize<<<(unsigned)blocks, 256, 0, s>>>(st, vals_init, vals_final, n);
+  launch_pdl(k_radix_finalize, dim3((unsigned)blocks), dim3(256), 0, s, (const DevState *)st, vals_init, vals_final, n);
 }
 
 __global__ void k_iota(uint32_t *perm, uint64_t n) {
