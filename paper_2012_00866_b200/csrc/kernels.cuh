@@ -30,7 +30,10 @@ void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *
 // load), so the walk length (tiles between a tile and the inclusive-prefix
 // frontier) is what bounds the pass; measured per-tile phases in DESIGN.md.
 constexpr int kRadixThreads = 512, kRadixItems = 8, kRadixTile = kRadixThreads * kRadixItems;
-constexpr int kRadixMinBlocks = 2;
+#ifndef HUSKY_RADIX_MINB
+#define HUSKY_RADIX_MINB 2
+#endif
+constexpr int kRadixMinBlocks = HUSKY_RADIX_MINB;
 inline uint64_t radix_tiles(uint64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
 // look-back words: one per (tile, digit), tile-major, up to kMaxBins per tile
 inline uint64_t radix_lb_stride(uint64_t n) { return (radix_tiles(n) + 1) & ~1ull; }

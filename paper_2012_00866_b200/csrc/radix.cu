@@ -186,7 +186,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 // dynamic smem of a pass: key/value exchange buffer + per-warp digit counters
 template <int BITS>
-constexpr int exchange_bytes() { return kRadixTile * (8 + 4) + kRadixWarps * (1 << BITS) * 4; }
+constexpr int exchange_bytes() { return kRadixTile * (8 + 4 + 2) + kRadixWarps * (1 << BITS) * 2; }
 
 // all digits trivial: the permutation is the payload as it stands
 __global__ void k_radix_finalize(const DevState *st, const uint32_t *v_init, uint32_t *v_final, uint64_t n) {
@@ -235,10 +235,15 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     vals_out = ((np - 1 - slot) & 1) == 0 ? sp.v_final : sp.v_tmp;
   }
   extern __shared__ __align__(16) uint8_t smem[];
-  // key/value exchange buffer, then per-warp digit counters [warps][R]
+  // key / value exchange buffers, each key's rank then tile-local position
+  // (u16, indexed by its load slot), per-warp digit counters [warps][R] (u16:
+  // at most 4096 per tile).  Ranks and positions live in shared memory and the
+  // values are loaded only after the keys are exchanged, so the kernel fits 40
+  // registers (3 CTAs per SM with kRadixMinBlocks = 3).
   uint64_t *xk = reinterpret_cast<uint64_t *>(smem);
   uint32_t *xv = reinterpret_cast<uint32_t *>(smem + kRadixTile * 8);
-  uint32_t *cnt = reinterpret_cast<uint32_t *>(smem + kRadixTile * 12);
+  uint16_t *rk = reinterpret_cast<uint16_t *>(smem + kRadixTile * 12);
+  uint16_t *cnt = reinterpret_cast<uint16_t *>(smem + kRadixTile * 14);
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_local_start[R];
   __shared__ uint32_t s_gbase[R];
@@ -254,19 +259,13 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   const uint64_t tile_base = (uint64_t)tile * kRadixTile;
   HT(tile, 0);
 
-  // ---- load (warp-striped: element = tile_base + warp*256 + r*32 + lane)
+  // ---- load the keys (warp-striped: slot = warp*256 + r*32 + lane)
+  const uint32_t slot0 = warp * (kRadixItems * 32) + lane;
   uint64_t k[kRadixItems];
-  uint32_t v[kRadixItems];
 #pragma unroll
   for (int r = 0; r < kRadixItems; ++r) {
-    uint64_t idx = tile_base + warp * (kRadixItems * 32) + r * 32 + lane;
-    if (idx < n) {
-      k[r] = __ldg(keys_in + idx);
-      v[r] = SYNTH_VALS ? (uint32_t)idx : __ldg(vals_in + idx);
-    } else {
-      k[r] = ~0ull;  // ranks last (the largest digit value at this shift); never stored
-      v[r] = 0;
-    }
+    const uint64_t idx = tile_base + slot0 + r * 32;
+    k[r] = idx < n ? __ldg(keys_in + idx) : ~0ull;  // padding ranks last (largest digit); never stored
   }
   // ---- the tile's bases (reduce-then-scan): independent of everything above
   const bool is_dg = tid < R;  // threads 0..R-1 own one digit each
@@ -275,17 +274,16 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   if (!LOOKBACK && is_dg) pre_base = __ldg(prefix + (uint64_t)dg * num_tiles + tile);
 
   // ---- warp-level match ranking into per-warp counters (stable: (r, lane) order)
-  uint32_t *wc = cnt + warp * R;
-  uint32_t rank[kRadixItems];
+  uint16_t *wc = cnt + warp * R;
 #pragma unroll
   for (int r = 0; r < kRadixItems; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & MASK;
     uint32_t peers = use_ballot ? match_ballot<BITS>(d) : __match_any_sync(0xFFFFFFFFu, d);
     if (r == 0) HT(tile, 1);
     uint32_t pre = wc[d];
-    rank[r] = pre + __popc(peers & lanemask_lt());
+    rk[slot0 + r * 32] = (uint16_t)(pre + __popc(peers & lanemask_lt()));
     __syncwarp();
-    if (lane == 31 - __clz(peers)) wc[d] = pre + __popc(peers);
+    if (lane == 31 - __clz(peers)) wc[d] = (uint16_t)(pre + __popc(peers));
     __syncwarp();
   }
   __syncthreads();
@@ -298,7 +296,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
 #pragma unroll
     for (int w = 0; w < kRadixWarps; ++w) {
       uint32_t c = cnt[w * R + dg];
-      cnt[w * R + dg] = tot;
+      cnt[w * R + dg] = (uint16_t)tot;
       tot += c;
     }
   }
@@ -316,13 +314,21 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   __syncthreads();
   HT(tile, 3);
 
-  // ---- exchange through shared memory into tile-local digit order
+  // ---- exchange the keys through shared memory into tile-local digit order;
+  // each slot's rank becomes its position (same thread, same slot)
 #pragma unroll
   for (int r = 0; r < kRadixItems; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & MASK;
-    uint32_t pos = s_local_start[d] + wc[d] + rank[r];
+    uint32_t pos = s_local_start[d] + wc[d] + rk[slot0 + r * 32];
     xk[pos] = k[r];
-    xv[pos] = v[r];
+    rk[slot0 + r * 32] = (uint16_t)pos;
+  }
+  // ---- the values: loaded now (the loads overlap the look-back), exchanged after it
+  uint32_t v[kRadixItems];
+#pragma unroll
+  for (int r = 0; r < kRadixItems; ++r) {
+    const uint64_t idx = tile_base + slot0 + r * 32;
+    v[r] = SYNTH_VALS ? (uint32_t)idx : (idx < n ? __ldg(vals_in + idx) : 0u);
   }
 
   // ---- global base of each digit
@@ -344,6 +350,8 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     if (tid == 0) HT(tile, 4);
     s_gbase[dg] = (uint32_t)excl - local_start;  // modular; global = gbase + local position
   }
+#pragma unroll
+  for (int r = 0; r < kRadixItems; ++r) xv[rk[slot0 + r * 32]] = v[r];
   __syncthreads();
   HT(tile, 5);
 

@@ -25,3 +25,8 @@ for i, nm in enumerate(names):
 tot = t[:, 5] - t[:, 0]
 print(f"{'tile total':16s} median {np.median(tot)/1e3:7.2f} us  mean {tot.mean()/1e3:7.2f}")
 print("span us", (t[:, 5].max() - t0) / 1e3, "tiles", len(t))
+print("mean tiles in flight", tot.sum() / (t[:, 5].max() - t0))
+# start-time order vs tile id: how far the look-back chain lags the tile starts
+st = t[:, 0] - t0
+lb_end = t[:, 3] - t0
+print("tile-start rate (tiles/us)", len(t) / (st.max() / 1e3 + 1e-9))
