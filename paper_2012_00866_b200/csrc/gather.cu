@@ -4,7 +4,7 @@
 // here the strings themselves are materialised in sorted order:
 //   sorted_offsets = exclusive scan of len[perm[i]]  (single pass, look-back)
 //   sorted_units   = concatenation of units[offsets[perm[i]] ..)
-// A tile of 4096 sorted positions (512 threads x 8): perm (coalesced) ->
+// A tile of kGatherTile = 1024 sorted positions (256 threads x 4): perm (coalesced) ->
 // lengths -> tile-local scan; the tile's aggregate is published, then the first
 // window of the tile's output bytes is staged in shared memory at tile-local
 // byte offsets (random reads, independent of the look-back), warp 0 resolves

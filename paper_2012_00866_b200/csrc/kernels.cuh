@@ -24,12 +24,17 @@ void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *
                       int num_sms, cudaStream_t s);
 
 // A2 onesweep radix
-// 512 threads x 8 keys = 4096-key tiles, 64 KB smem, <= 64 registers -> 2 CTAs
-// (32 warps) per SM.  Large tiles keep the number of tiles in flight low: each
-// look-back round trip queues behind the SM's bulk DRAM loads (~1 us under
-// load), so the walk length (tiles between a tile and the inclusive-prefix
-// frontier) is what bounds the pass; measured per-tile phases in DESIGN.md.
-constexpr int kRadixThreads = 512, kRadixItems = 8, kRadixTile = kRadixThreads * kRadixItems;
+// 512 threads x 12 keys = 6144-key tiles, 92 KB smem (keys, payloads, u16
+// positions, u16 per-warp counters), <= 64 registers -> 2 CTAs (32 warps) per
+// SM.  Large tiles keep the number of tiles in flight low: each look-back round
+// trip queues behind the SM's bulk DRAM loads (~1 us under load), so the walk
+// length (tiles between a tile and the inclusive-prefix frontier) is what
+// bounds the pass.  Measured on C2 per sort: 8 keys/thread
+// 1115 us, 10: 1067, 12: 1057, 14: 1075, 16 (1 CTA/SM): 1199.
+#ifndef HUSKY_RADIX_ITEMS
+#define HUSKY_RADIX_ITEMS 12
+#endif
+constexpr int kRadixThreads = 512, kRadixItems = HUSKY_RADIX_ITEMS, kRadixTile = kRadixThreads * kRadixItems;
 #ifndef HUSKY_RADIX_MINB
 #define HUSKY_RADIX_MINB 2
 #endif

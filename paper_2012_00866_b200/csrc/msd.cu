@@ -24,7 +24,7 @@
 //                           continue (next list, other scratch buffer), buckets of
 //                           2..kMsdSmall keys register with the local-sort window
 //                           of their start, all-equal segments finish
-//             k_msd_partition  onesweep tile (4096 keys, warp match ranking,
+//             k_msd_partition  onesweep tile (kRadixTile keys, warp match ranking,
 //                           decoupled look-back per (tile, digit) that stops at
 //                           the segment's first tile) scattering each bucket to
 //                           the scratch buffer (continuing) or the home buffer
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(256) k_msd_plan(DevState *st, MsdBufs B, int l
 }
 
 // --------------------------------------------------------------- partition
-// One 4096-key tile of a segment: warp-striped loads, __match_any_sync ranking
+// One kRadixTile-key tile of a segment: warp-striped loads, __match_any_sync ranking
 // into per-warp digit counters (stable), the tile's digit counts published for
 // the decoupled look-back, exchange through shared memory into digit order,
 // scatter in runs of consecutive addresses to the scratch (continuing bucket)

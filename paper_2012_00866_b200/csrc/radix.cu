@@ -10,7 +10,7 @@
 // Digit width: 8 bits (kernels are templated on it; the device-planned slots
 // can be built with 9-bit digits, HUSKY_SLOT_BITS=9: 7 passes for the 63-bit
 // codes, measured no faster -- husky_internal.cuh).
-// A pass works on tiles of 4096 keys (512 threads x 8, warp-striped so every
+// A pass works on tiles of kRadixTile = 6144 keys (512 threads x 12, warp-striped so every
 // load/store instruction is a coalesced 256-B access).  Each tile is ranked in
 // shared memory with warp-level label matching (__match_any_sync, or per-bit
 // ballots when the plan says the digit is spread out) + popc into per-warp
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   extern __shared__ __align__(16) uint8_t smem[];
   // key / value exchange buffers, each key's rank then tile-local position
   // (u16, indexed by its load slot), per-warp digit counters [warps][R] (u16:
-  // at most 4096 per tile).  Ranks and positions live in shared memory and the
+  // at most kRadixTile per tile).  Ranks and positions live in shared memory and the
   // values are loaded only after the keys are exchanged, so the kernel fits 40
   // registers (3 CTAs per SM with kRadixMinBlocks = 3).
   uint64_t *xk = reinterpret_cast<uint64_t *>(smem);

@@ -2,4 +2,3 @@
 bash tools/gpu_tests.sh
 bash tools/gpu_bench_ncu.sh
 for x in peer nccl; do HUSKY_EXCHANGE=$x timeout 300 python bench.py --force-multi --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_fm_$x.json 2> gpurun_out/bench_fm_$x.err; echo fm $x=$?; done
-for d in 2 3 4; do HUSKY_E2E_DEPTH=$d timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_depth$d.json 2>/dev/null; echo depth $d=$?; done
