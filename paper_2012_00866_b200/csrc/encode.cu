@@ -91,7 +91,13 @@ __device__ __forceinline__ uint64_t encode_words(uint64_t w0, uint64_t w1, uint6
 // leaving the caller's buffer.
 constexpr int kEncIT = 4;
 template <int CODER>
-__global__ void __launch_bounds__(kEncThreads) k_encode(const void *__restrict__ units,
+// 4 CTAs per SM (64 registers): measured per C2 / C3 encode 76 / 62 us, against
+// 81 / 71 us unbounded (79 registers, 3 CTAs), 87 / 83 us at 5 and 92 / 89 us at
+// 6 CTAs per SM (spills) -- the kernel is latency-bound on its two dependent loads
+#ifndef HUSKY_ENC_MINB
+#define HUSKY_ENC_MINB 4
+#endif
+__global__ void __launch_bounds__(kEncThreads, HUSKY_ENC_MINB) k_encode(const void *__restrict__ units,
                                                         const int64_t *__restrict__ offsets, uint64_t n,
                                                         uint64_t *__restrict__ codes, DevState *st,
                                                         uint32_t *__restrict__ packed) {
