@@ -72,6 +72,10 @@ void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s, int bits) {
 // last CTA to add its histograms (ticket) also does k_hist_scan's scans and
 // the pass plan (which digits to sort, in which order, with which ranking
 // primitive), saving two dependent launches.
+#ifndef HUSKY_HIST_BPS
+#define HUSKY_HIST_BPS 4
+#endif
+constexpr int kHistBlocksPerSM = HUSKY_HIST_BPS;  // resident CTAs of 512 threads per SM
 template <bool PLAN>
 __global__ void __launch_bounds__(512) k_hist_slots(const uint64_t *__restrict__ keys, uint64_t n, DevState *st,
                                                     uint64_t *keysA, uint64_t *keysB, uint32_t force_ballot,
@@ -147,7 +151,7 @@ static uint32_t env_mask(const char *name) {
 void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s) {
   if (n == 0) return;
   Scope sc_(ST_HIST_SCAN, s, n);
-  const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * 2);
+  const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * kHistBlocksPerSM);
   k_hist_slots<false><<<(unsigned)blocks, 512, 0, s>>>(keys, n, st, nullptr, nullptr, 0, 0);
 }
 
@@ -160,7 +164,7 @@ void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *
   // experiments: HUSKY_RANK_BALLOT / HUSKY_RANK_MATCH = digit bit masks that
   // force one primitive (default: the plan's < 5% largest-bin rule)
   static const uint32_t force_ballot = env_mask("HUSKY_RANK_BALLOT"), force_match = env_mask("HUSKY_RANK_MATCH");
-  const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * 2);
+  const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * kHistBlocksPerSM);
   launch_pdl(k_hist_slots<true>, dim3((unsigned)blocks), dim3(512), 0, s, keys, n, st, keysA, keysB, force_ballot,
              force_match);
 }
