@@ -171,7 +171,7 @@ void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *
 
 constexpr int kRadixWarps = kRadixThreads / 32;
 #ifndef RADIX_LB_W
-#define RADIX_LB_W 8
+#define RADIX_LB_W 12
 #endif
 
 #ifdef HUSKY_TIMING
