@@ -337,9 +337,10 @@ def run_ours(args):
         e_ms /= args.steps
         single = {"value": round(n / (e_ms * 1e-3) / 1e6, 4), "ms_per_step": round(e_ms, 3),
                   "api": "husky_sort_host, one call per step (pinned host buffers)"}
-        # pipelined: the K steps as K batches of husky_sort_host_many (2 workers,
-        # each with its own stream), so one step's copies overlap another's
-        # kernels and the full-duplex PCIe carries H2D and D2H at once
+        # pipelined: the K steps as K batches of husky_sort_host_many (2 device
+        # buffer slots, one stream each for H2D copies, kernels and D2H copies),
+        # so one step's copies overlap another's kernels and the full-duplex
+        # PCIe carries H2D and D2H at once
         depth = int(os.environ.get("HUSKY_E2E_DEPTH", "2"))
         hws = None
         torch.cuda.empty_cache()
@@ -359,8 +360,9 @@ def run_ours(args):
                "h2d_bytes_per_step": int(total_units * ub + (n + 1) * 8),
                "d2h_bytes_per_step": int(n * 4 + total_units * ub + (n + 1) * 8),
                "ms_per_step": round(p_ms, 3),
-               "api": f"husky_sort_host_many: {args.steps} steps as {args.steps} pipelined batches on {depth} "
-                      "workers (pinned host buffers), host wall clock around the call",
+               "api": f"husky_sort_host_many: {args.steps} steps as {args.steps} pipelined batches, {depth} "
+                      "device slots, H2D / kernels / D2H on three streams (pinned host buffers), host wall clock "
+                      "around the call",
                "single_call": single}
     elif world > 1 or args.force_multi:
         # sharded: every step copies the rank's input block from pinned host

@@ -580,6 +580,115 @@ husky_status husky_sort_host(int coder, const void *h_units, const int64_t *h_of
   return HUSKY_OK;
 }
 
+// husky_sort_host_many, one issuing thread and three streams: host->device
+// copies (sh), kernels (sc) and device->host copies (sd), `depth` workspace
+// slots used round robin.  Batch b+1's input copy is enqueued before batch b
+// is sorted (sort_impl synchronises sc once per sort) and batch b's output
+// copy right after, so in steady state both copy directions and the SMs work on
+// three different batches.  Events order the reuse of a slot: its inputs are
+// overwritten only after the sort that read them, its outputs only after the
+// copy-out that read them.
+static husky_status host_many_pipelined(int coder, int k, const void *const *h_units,
+                                        const int64_t *const *h_offsets, const uint64_t *n,
+                                        uint32_t *const *h_perm, void *const *h_sorted_units,
+                                        int64_t *const *h_sorted_offsets, int depth, uint8_t *ws, size_t slice,
+                                        husky_outcome *h_out) {
+  const size_t w = husky_unit_bytes(coder);
+  cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
+  std::vector<cudaEvent_t> evH(depth, nullptr), evC(depth, nullptr), evD(depth, nullptr);
+  husky_status st = HUSKY_OK;
+  auto cleanup = [&]() {
+    if (sh) cudaStreamSynchronize(sh);
+    if (sc) cudaStreamSynchronize(sc);
+    if (sd) cudaStreamSynchronize(sd);
+    for (int i = 0; i < depth; ++i) {
+      if (evH[i]) cudaEventDestroy(evH[i]);
+      if (evC[i]) cudaEventDestroy(evC[i]);
+      if (evD[i]) cudaEventDestroy(evD[i]);
+    }
+    if (sh) cudaStreamDestroy(sh);
+    if (sc) cudaStreamDestroy(sc);
+    if (sd) cudaStreamDestroy(sd);
+  };
+#define HM_CHECK(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      st = fail(HUSKY_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_));                   \
+      cleanup();                                                                            \
+      return st;                                                                            \
+    }                                                                                       \
+  } while (0)
+  HM_CHECK(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking));
+  HM_CHECK(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
+  HM_CHECK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+  for (int i = 0; i < depth; ++i) {
+    HM_CHECK(cudaEventCreateWithFlags(&evH[i], cudaEventDisableTiming));
+    HM_CHECK(cudaEventCreateWithFlags(&evC[i], cudaEventDisableTiming));
+    HM_CHECK(cudaEventCreateWithFlags(&evD[i], cudaEventDisableTiming));
+  }
+  auto total_of = [&](int b) { return n[b] ? (uint64_t)(h_offsets[b][n[b]] - h_offsets[b][0]) : 0ull; };
+  std::vector<bool> used(depth, false);
+  auto issue_in = [&](int b) -> cudaError_t {
+    const int sl = b % depth;
+    uint8_t *base = ws + slice * sl;
+    size_t o_units, o_off, o_perm, o_su, o_so, o_ws;
+    host_layout(coder, n[b], total_of(b), &o_units, &o_off, &o_perm, &o_su, &o_so, &o_ws);
+    cudaError_t e = cudaSuccess;
+    if (used[sl]) e = cudaStreamWaitEvent(sh, evC[sl], 0);  // the previous sort of this slot has read its inputs
+    const int64_t b0 = n[b] ? h_offsets[b][0] : 0;
+    if (e == cudaSuccess && total_of(b))
+      e = cudaMemcpyAsync(base + o_units, (const uint8_t *)h_units[b] + b0 * w, total_of(b) * w,
+                          cudaMemcpyHostToDevice, sh);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(base + o_off, h_offsets[b], (n[b] + 1) * 8, cudaMemcpyHostToDevice, sh);
+    if (e == cudaSuccess) e = cudaEventRecord(evH[sl], sh);
+    return e;
+  };
+  if (k > 0) HM_CHECK(issue_in(0));
+  for (int b = 0; b < k; ++b) {
+    const int sl = b % depth;
+    uint8_t *base = ws + slice * sl;
+    if (b + 1 < k && depth > 1) HM_CHECK(issue_in(b + 1));  // (one slot: after this sort)
+    if (n[b] && h_offsets[b][n[b]] < h_offsets[b][0]) {
+      st = fail(HUSKY_ERR_INVALID_ARG, "batch %d: offsets are not non-decreasing", b);
+      cleanup();
+      return st;
+    }
+    size_t o_units, o_off, o_perm, o_su, o_so, o_ws;
+    host_layout(coder, n[b], total_of(b), &o_units, &o_off, &o_perm, &o_su, &o_so, &o_ws);
+    HM_CHECK(cudaStreamWaitEvent(sc, evH[sl], 0));
+    if (used[sl]) HM_CHECK(cudaStreamWaitEvent(sc, evD[sl], 0));  // outputs of this slot copied out
+    const int64_t b0 = n[b] ? h_offsets[b][0] : 0;
+    const void *du = base + o_units;
+    if (b0 != 0) du = (const uint8_t *)du - b0 * (int64_t)w;  // offsets index the original buffer
+    const bool want_units = h_sorted_units && h_sorted_offsets && h_sorted_units[b] && h_sorted_offsets[b];
+    st = sort_impl(coder, du, (const int64_t *)(base + o_off), n[b], (uint32_t *)(base + o_perm),
+                   want_units ? (void *)(base + o_su) : nullptr, want_units ? (int64_t *)(base + o_so) : nullptr,
+                   base + o_ws, slice - o_ws, h_out ? h_out + b : nullptr, sc);
+    if (st != HUSKY_OK) {
+      cleanup();
+      return st;
+    }
+    HM_CHECK(cudaEventRecord(evC[sl], sc));
+    HM_CHECK(cudaStreamWaitEvent(sd, evC[sl], 0));
+    if (n[b]) HM_CHECK(cudaMemcpyAsync(h_perm[b], base + o_perm, n[b] * 4, cudaMemcpyDeviceToHost, sd));
+    if (want_units) {
+      if (total_of(b))
+        HM_CHECK(cudaMemcpyAsync(h_sorted_units[b], base + o_su, total_of(b) * w, cudaMemcpyDeviceToHost, sd));
+      HM_CHECK(cudaMemcpyAsync(h_sorted_offsets[b], base + o_so, (n[b] + 1) * 8, cudaMemcpyDeviceToHost, sd));
+    }
+    HM_CHECK(cudaEventRecord(evD[sl], sd));
+    used[sl] = true;
+    if (b + 1 < k && depth == 1) HM_CHECK(issue_in(b + 1));
+  }
+#undef HM_CHECK
+  cudaError_t e = cudaStreamSynchronize(sd);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sh);
+  cleanup();
+  if (e != cudaSuccess) return fail(HUSKY_ERR_CUDA, "husky_sort_host_many: %s", cudaGetErrorString(e));
+  return HUSKY_OK;
+}
+
 husky_status husky_sort_host_many_workspace(int coder, uint64_t n_max, uint64_t units_max, int depth,
                                             size_t *bytes) {
   if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
@@ -606,6 +715,10 @@ husky_status husky_sort_host_many(int coder, int k, const void *const *h_units, 
   size_t a, bb, c, d, e, f;
   const size_t slice = align_up(host_layout(coder, n_max, u_max, &a, &bb, &c, &d, &e, &f), 256);
   if (ws_bytes < slice * depth) return fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, slice * depth);
+  const char *mode = getenv("HUSKY_HOST_MANY");
+  if (!(mode && mode[0] == 't'))
+    return host_many_pipelined(coder, k, h_units, h_offsets, n, h_perm, h_sorted_units, h_sorted_offsets, depth,
+                               (uint8_t *)d_ws, slice, h_out);
   int dev = 0;
   cudaGetDevice(&dev);
   std::vector<husky_status> st(depth, HUSKY_OK);
