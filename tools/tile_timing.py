@@ -13,7 +13,7 @@ for _ in range(3):
     h.sort(w.coder, u, o)
 lib = h.lib()
 lib.husky_debug_tile_times.restype = ctypes.c_int
-import os; TS = int(os.environ.get("TILE", "4096")); ntiles = (w.n + TS - 1) // TS
+import os; TS = int(os.environ.get("TILE", "6144")); ntiles = (w.n + TS - 1) // TS
 buf = np.zeros((8192, 8), dtype=np.uint64)
 k = lib.husky_debug_tile_times(buf.ctypes.data_as(ctypes.c_void_p), 8192)
 t = buf[:min(ntiles, k)].astype(np.int64)
