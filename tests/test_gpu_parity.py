@@ -7,6 +7,7 @@ full BASELINE.json sizes are checked with the oracle's linear uniqueness
 verifier (bijection + strictly increasing adjacent pairs <=> equal to the
 oracle's sort, because the order is a strict total order).
 """
+import os
 import random
 import zlib
 
@@ -426,12 +427,15 @@ def test_multi_loopback_peer_edges(torch, h, oracle_mod, monkeypatch, world):
     assert np.array_equal(so.cpu().numpy(), rso) and np.array_equal(su[:tot].cpu().numpy(), rsu)
 
 
-def test_sort_host_many_pipelined(torch, h, oracle_mod):
+@pytest.mark.parametrize("mode", ["pipe", "threads"])
+def test_sort_host_many_pipelined(torch, h, oracle_mod, monkeypatch, mode):
     """The pipelined host API: several batches (different configs and sizes,
-    one empty) on 2 and 3 workers, each bit-exact against the oracle."""
+    one empty) through 1, 2 and 3 workspace slots, each bit-exact against the
+    oracle -- the three-stream pipeline and the worker-thread scheme."""
+    monkeypatch.setenv("HUSKY_HOST_MANY", mode)
     wls = [W.make("C1", 50_000), W.make("C3", 70_000), W.make("C2", 120_000),
            W.from_strings([], ASCII), W.make("C1", 3)]
-    for depth in (2, 3):
+    for depth in (1, 2, 3):
         for coder in (ASCII, UNICODE):
             sel = [w for w in wls if w.coder == coder]
             batches = []
@@ -472,3 +476,25 @@ def test_multi_loopback_off_domain(torch, h, oracle_mod, world):
     ref = oracle_mod.sort(w.coder, w.units, w.offsets)
     assert np.array_equal(perm.cpu().numpy().view(np.uint32), ref)
     assert sum(shards) == w.n and max(shards) < w.n
+
+
+def test_programmatic_launch_off_matches(torch, h, tmp_path):
+    """HUSKY_PDL=0 (plain launches, read once per process) sorts exactly like
+    the default programmatic dependent launches: run in a subprocess."""
+    import subprocess
+    import sys
+    w = W.make("C2", 200_000)
+    u, o = to_dev(torch, w)
+    p_pdl = h.sort(w.coder, u, o)[0].cpu().numpy()
+    script = tmp_path / "nopdl.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})\n"
+        "import paper_2012_00866_b200 as h, workloads as W\n"
+        "w = W.make('C2', 200_000)\n"
+        "u = torch.from_numpy(w.units).cuda(); o = torch.from_numpy(w.offsets).cuda()\n"
+        f"np.save({repr(str(tmp_path / 'p.npy'))}, h.sort(w.coder, u, o)[0].cpu().numpy())\n")
+    env = dict(os.environ, HUSKY_PDL="0")
+    r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert np.array_equal(np.load(tmp_path / "p.npy"), p_pdl)
