@@ -44,8 +44,9 @@ inline uint64_t radix_tiles(uint64_t n) { return (n + kRadixTile - 1) / kRadixTi
 inline uint64_t radix_lb_stride(uint64_t n) { return (radix_tiles(n) + 1) & ~1ull; }
 inline uint64_t radix_lb_words(uint64_t n) { return radix_lb_stride(n) * kMaxBins + 2; }
 // exclusive scans of DevState::hist -> digit_start, trivial_mask, digit_spread
-// for `bits`-bit digits (8: host-planned passes; kSlotBits: the slots)
-void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s, int bits = 8);
+// for the 8-bit digits of the host-planned passes (the pass slots get theirs
+// from launch_hist_plan)
+void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s);
 // One stable LSD pass on digit `digit` (bits 8*digit..8*digit+7).  vals_in == NULL
 // synthesises payload = index.  lb: radix_tiles(n)*256 look-back words.
 void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,

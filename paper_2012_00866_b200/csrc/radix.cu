@@ -59,10 +59,9 @@ __global__ void __launch_bounds__(1 << BITS) k_hist_scan(uint64_t n, DevState *s
   }
 }
 
-void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s, int bits) {
+void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s) {
   Scope sc_(ST_HIST_SCAN, s, n);
-  if (bits == 9) k_hist_scan<9><<<8, 512, 0, s>>>(n, st);
-  else k_hist_scan<8><<<8, 256, 0, s>>>(n, st);
+  k_hist_scan<8><<<8, 256, 0, s>>>(n, st);
 }
 
 // The 8 digit histograms (kSlotBits-bit digits) of the codes for the LSD
