@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(256)
     k_fix_small(const uint2 *__restrict__ list, const DevState *st, uint32_t *perm,
                 const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t first) {
   using T = CoderTraits<CODER>;
+  pdl_wait();
   if (st->violations & kOffsetsBad) return;
   const uint32_t lane = lane_id();
   const uint32_t nsmall = st->n_small;
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(1024)
                  const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t first) {
   using T = CoderTraits<CODER>;
   __shared__ uint32_t s[kMediumMax];
+  pdl_wait();
   if (st->violations & kOffsetsBad) return;
   const uint32_t nmed = st->n_medium;
   const bool general = st->general != 0;
@@ -94,9 +96,9 @@ void launch_fix_small(int coder, const uint2 *list_sm, const DevState *st, uint3
   Scope sc_(ST_FIX_SMALL, s, 0);
   dim3 g(num_sms * 4), b(256);
   if (coder == HUSKY_CODER_ASCII)
-    k_fix_small<HUSKY_CODER_ASCII><<<g, b, 0, s>>>(list_sm, st, perm, units, offsets, first);
+    launch_pdl(k_fix_small<HUSKY_CODER_ASCII>, g, b, 0, s, list_sm, st, perm, units, offsets, first);
   else
-    k_fix_small<HUSKY_CODER_UNICODE><<<g, b, 0, s>>>(list_sm, st, perm, units, offsets, first);
+    launch_pdl(k_fix_small<HUSKY_CODER_UNICODE>, g, b, 0, s, list_sm, st, perm, units, offsets, first);
 }
 
 void launch_fix_medium(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
@@ -105,9 +107,9 @@ void launch_fix_medium(int coder, const uint2 *list_sm, uint64_t cap_sm, const D
   Scope sc_(ST_FIX_MEDIUM, s, 0);
   dim3 g(num_sms), b(1024);
   if (coder == HUSKY_CODER_ASCII)
-    k_fix_medium<HUSKY_CODER_ASCII><<<g, b, 0, s>>>(list_sm, cap_sm, st, perm, units, offsets, first);
+    launch_pdl(k_fix_medium<HUSKY_CODER_ASCII>, g, b, 0, s, list_sm, cap_sm, st, perm, units, offsets, first);
   else
-    k_fix_medium<HUSKY_CODER_UNICODE><<<g, b, 0, s>>>(list_sm, cap_sm, st, perm, units, offsets, first);
+    launch_pdl(k_fix_medium<HUSKY_CODER_UNICODE>, g, b, 0, s, list_sm, cap_sm, st, perm, units, offsets, first);
 }
 
 // ------------------------------------------------------------------ A6

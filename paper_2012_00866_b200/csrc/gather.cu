@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(256)
                     int64_t *__restrict__ sorted_offsets, uint32_t first_small, uint32_t first_medium) {
   constexpr int W = CoderTraits<CODER>::kUnitBytes;
   __shared__ unsigned long long s_wt[256 / 32 + 1];
+  pdl_wait();
   if (st->violations & kOffsetsBad) return;
   // entries [first_small, n_small) of the small list, then [first_medium, n_medium) of the medium list
   const uint32_t ns = st->n_small - first_small, nm = st->n_medium - first_medium;
@@ -596,11 +597,11 @@ void launch_regather_runs(int coder, const uint2 *list_sm, uint64_t cap_sm, cons
   Scope sc_(ST_FIX_SMALL, s, 0);
   dim3 g(num_sms * 4), b(256);
   if (coder == HUSKY_CODER_ASCII)
-    k_regather_runs<HUSKY_CODER_ASCII><<<g, b, 0, s>>>(list_sm, cap_sm, st, perm, units, offsets, sorted_units,
-                                                       sorted_offsets, first_small, first_medium);
+    launch_pdl(k_regather_runs<HUSKY_CODER_ASCII>, g, b, 0, s, list_sm, cap_sm, st, (const uint32_t *)perm, units,
+               offsets, sorted_units, sorted_offsets, first_small, first_medium);
   else
-    k_regather_runs<HUSKY_CODER_UNICODE><<<g, b, 0, s>>>(list_sm, cap_sm, st, perm, units, offsets, sorted_units,
-                                                         sorted_offsets, first_small, first_medium);
+    launch_pdl(k_regather_runs<HUSKY_CODER_UNICODE>, g, b, 0, s, list_sm, cap_sm, st, (const uint32_t *)perm, units,
+               offsets, sorted_units, sorted_offsets, first_small, first_medium);
 }
 
 }  // namespace husky

@@ -186,6 +186,9 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
 
   HCHECK(cudaMemsetAsync(st, 0, sizeof(DevState), s));
   HCHECK(S.reset_lookback());
+  // the dirty-run flags the main gather sets (cleared here, not between the key
+  // sort and the gather, so the gather stays a programmatic dependent)
+  HCHECK(cudaMemsetAsync(S.at<uint8_t>(L.dirty), 0, L.cap_sm, s));
 
   // ---- A1 encode (+ digit histograms, flags) and the histogram scan
   // n <= 2^28: the payload carries min(len, 15) in its top 4 bits, so the
@@ -251,8 +254,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // adjacent equal-code pair on the strings it stages (perm-only mode runs the
   // separate run scan below instead).
   uint32_t *run_start = S.at<uint32_t>(L.run_start), *run_end = S.at<uint32_t>(L.run_end);
-  uint8_t *dirty = S.at<uint8_t>(L.dirty);
-  HCHECK(cudaMemsetAsync(dirty, 0, L.cap_sm, s));
+  uint8_t *dirty = S.at<uint8_t>(L.dirty);  // zeroed with the DevState at the start
   if (d_sorted_units) {
     GatherRunsOut ro{run_start, run_end, dirty, S.lb_scan2(), st};
     launch_gather(kc, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),

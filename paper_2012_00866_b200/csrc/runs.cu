@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(256)
                     const uint8_t *__restrict__ dirty, DevState *st, uint2 *list_sm, uint64_t cap_sm,
                     uint2 *list_g, int count_stats) {
   __shared__ unsigned long long s_sum[4], s_in, s_max;
+  pdl_wait();
   if (threadIdx.x < 4) s_sum[threadIdx.x] = 0;
   if (threadIdx.x == 0) { s_in = 0; s_max = 0; }
   __syncthreads();
@@ -205,8 +206,8 @@ void launch_runs_classify(const uint32_t *run_start, const uint32_t *run_end, co
                           DevState *st, uint2 *list_sm, uint64_t cap_sm, uint2 *list_g,
                           bool count_stats, int num_sms, cudaStream_t s) {
   Scope sc_(ST_CLASSIFY, s, 0);
-  k_runs_classify<<<num_sms * 2, 256, 0, s>>>(run_start, run_end, dirty, st, list_sm, cap_sm, list_g,
-                                              count_stats ? 1 : 0);
+  launch_pdl(k_runs_classify, dim3(num_sms * 2), dim3(256), 0, s, run_start, run_end, dirty, st, list_sm, cap_sm,
+             list_g, count_stats ? 1 : 0);
 }
 
 }  // namespace husky
