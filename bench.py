@@ -424,6 +424,9 @@ def run_ours(args):
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "stages": stages, "outcome": outc}
         print(json.dumps(line), flush=True)
+    if world > 1 or args.force_multi:
+        torch.cuda.synchronize()
+        h.husky_comm_destroy(comm)  # releases the receive window (collective) before the NCCL comm
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
