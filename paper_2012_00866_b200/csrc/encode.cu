@@ -89,7 +89,10 @@ __device__ __forceinline__ uint64_t encode_words(uint64_t w0, uint64_t w1, uint6
 // cover units[offsets[0] .. offsets[n]): for valid offsets the words a window
 // needs are always inside, so they are issued unconditionally without ever
 // leaving the caller's buffer.
-constexpr int kEncIT = 4;
+#ifndef HUSKY_ENC_IT
+#define HUSKY_ENC_IT 4
+#endif
+constexpr int kEncIT = HUSKY_ENC_IT;
 template <int CODER>
 // 4 CTAs per SM (64 registers): measured per C2 / C3 encode 76 / 62 us, against
 // 81 / 71 us unbounded (79 registers, 3 CTAs), 87 / 83 us at 5 and 92 / 89 us at

@@ -10,7 +10,10 @@ int device_sm_count();  // husky.cu
 
 // A1 encode
 // 256 threads x 4 strings in flight per CTA iteration, persistent grid
-constexpr int kEncThreads = 256, kEncBlocksPerSM = 8;
+#ifndef HUSKY_ENC_BPS
+#define HUSKY_ENC_BPS 8
+#endif
+constexpr int kEncThreads = 256, kEncBlocksPerSM = HUSKY_ENC_BPS;  // grid (resident: HUSKY_ENC_MINB)
 // packed (nullable, n <= 2^28): also writes the initial radix payload
 // index | min(len, 15) << 28, so the gather knows short strings' lengths
 // without a random offsets read.
