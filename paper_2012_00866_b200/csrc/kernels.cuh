@@ -42,7 +42,21 @@ constexpr int kRadixThreads = 512, kRadixItems = HUSKY_RADIX_ITEMS, kRadixTile =
 #define HUSKY_RADIX_MINB 2
 #endif
 constexpr int kRadixMinBlocks = HUSKY_RADIX_MINB;
-inline uint64_t radix_tiles(uint64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
+// Small inputs (n below kRadixSmallN) use 2048-key tiles (4 keys per thread):
+// a 1e5-string sort has 17 large tiles for 148 SMs.  Measured per C2-like sort
+// (small / large tiles): 1e5 140 / 165 us, 3e5 158 / 174, 1e6 248 / 235,
+// 2e6 367 / 321 us -- the crossover lies between 3e5 and 1e6
+constexpr int kRadixItemsSmall = 4;
+#ifndef HUSKY_RADIX_SMALL_N
+#define HUSKY_RADIX_SMALL_N 500000
+#endif
+constexpr uint64_t kRadixSmallN = HUSKY_RADIX_SMALL_N;
+inline int radix_items(uint64_t n) { return n < kRadixSmallN ? kRadixItemsSmall : kRadixItems; }
+inline uint64_t radix_tiles(uint64_t n) {
+  const uint64_t t = (uint64_t)kRadixThreads * radix_items(n);
+  return (n + t - 1) / t;
+}
+inline uint64_t radix_tiles_large(uint64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
 // look-back words: one per (tile, digit), tile-major, up to kMaxBins per tile
 inline uint64_t radix_lb_stride(uint64_t n) { return (radix_tiles(n) + 1) & ~1ull; }
 inline uint64_t radix_lb_words(uint64_t n) { return radix_lb_stride(n) * kMaxBins + 2; }
@@ -81,7 +95,7 @@ struct MsdSeg {
   uint32_t flags;
 };
 inline uint64_t msd_max_segs(uint64_t n) { return n / (kMsdSmall + 1) + 2; }
-inline uint64_t msd_max_tiles(uint64_t n) { return radix_tiles(n) + msd_max_segs(n) + 1; }
+inline uint64_t msd_max_tiles(uint64_t n) { return radix_tiles_large(n) + msd_max_segs(n) + 1; }
 inline uint64_t msd_windows(uint64_t n) { return (n + kMsdWin - 1) / kMsdWin; }
 struct MsdBufs {
   uint64_t *k[2];            // scratch keys (k[0] holds the codes written by A1)

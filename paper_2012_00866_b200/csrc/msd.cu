@@ -520,7 +520,7 @@ husky_status msd_key_sort(Sorter &S, const MsdBufs &B) {
   }
   int list = 0, level = 0;
   uint32_t nsegs = 1;
-  uint64_t tiles = radix_tiles(n);
+  uint64_t tiles = radix_tiles_large(n);  // the MSD levels use kRadixTile-key tiles
   {
     HUSKY_SCOPE(ST_HIST_SCAN, s, 0);
     k_msd_tiles<<<1, 1024, 0, s>>>(st, B, 0);

@@ -188,8 +188,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define HT(tile, i) do { } while (0)
 #endif
 // dynamic smem of a pass: key/value exchange buffer + per-warp digit counters
-template <int BITS>
-constexpr int exchange_bytes() { return kRadixTile * (8 + 4 + 2) + kRadixWarps * (1 << BITS) * 2; }
+template <int BITS, int ITEMS = kRadixItems>
+constexpr int exchange_bytes() { return kRadixThreads * ITEMS * (8 + 4 + 2) + kRadixWarps * (1 << BITS) * 2; }
 
 // all digits trivial: the permutation is the payload as it stands
 __global__ void k_radix_finalize(const DevState *st, const uint32_t *v_init, uint32_t *v_final, uint64_t n) {
@@ -212,7 +212,7 @@ struct SlotPtrs {
 // written by k_rs_scan) and nothing waits on other tiles.  plan != NULL: this
 // is pass slot `slot` of the device-side plan (buffers, digit resolved here;
 // slots beyond the plan exit at once).
-template <bool SYNTH_VALS, bool LOOKBACK, int BITS>
+template <bool SYNTH_VALS, bool LOOKBACK, int BITS, int ITEMS = kRadixItems>
 __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     k_onesweep(const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint64_t n, int shift,
@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   // host-planned passes (refinement, multi-GPU partition): the digit's spread
   // as measured by k_hist_scan; planned slots: the plan's choice
   constexpr uint32_t R = 1u << BITS, MASK = R - 1;
+  constexpr int TILE = kRadixThreads * ITEMS;
   static_assert(R <= kRadixThreads, "one digit per thread");
   pdl_wait();  // the pass slots are programmatic dependents of the previous kernel
   bool use_ballot = !plan && sp.st && sp.st->digit_spread[shift / BITS];
@@ -240,13 +241,13 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   extern __shared__ __align__(16) uint8_t smem[];
   // key / value exchange buffers, each key's rank then tile-local position
   // (u16, indexed by its load slot), per-warp digit counters [warps][R] (u16:
-  // at most kRadixTile per tile).  Ranks and positions live in shared memory and the
+  // at most TILE per tile).  Ranks and positions live in shared memory and the
   // values are loaded only after the keys are exchanged, so the kernel fits 40
   // registers (3 CTAs per SM with kRadixMinBlocks = 3).
   uint64_t *xk = reinterpret_cast<uint64_t *>(smem);
-  uint32_t *xv = reinterpret_cast<uint32_t *>(smem + kRadixTile * 8);
-  uint16_t *rk = reinterpret_cast<uint16_t *>(smem + kRadixTile * 12);
-  uint16_t *cnt = reinterpret_cast<uint16_t *>(smem + kRadixTile * 14);
+  uint32_t *xv = reinterpret_cast<uint32_t *>(smem + TILE * 8);
+  uint16_t *rk = reinterpret_cast<uint16_t *>(smem + TILE * 12);
+  uint16_t *cnt = reinterpret_cast<uint16_t *>(smem + TILE * 14);
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_local_start[R];
   __shared__ uint32_t s_gbase[R];
@@ -259,14 +260,14 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   for (int i = tid; i < kRadixWarps * (int)R; i += kRadixThreads) cnt[i] = 0;
   __syncthreads();
   const uint32_t tile = LOOKBACK ? s_tile : blockIdx.x;
-  const uint64_t tile_base = (uint64_t)tile * kRadixTile;
+  const uint64_t tile_base = (uint64_t)tile * TILE;
   HT(tile, 0);
 
   // ---- load the keys (warp-striped: slot = warp*256 + r*32 + lane)
-  const uint32_t slot0 = warp * (kRadixItems * 32) + lane;
-  uint64_t k[kRadixItems];
+  const uint32_t slot0 = warp * (ITEMS * 32) + lane;
+  uint64_t k[ITEMS];
 #pragma unroll
-  for (int r = 0; r < kRadixItems; ++r) {
+  for (int r = 0; r < ITEMS; ++r) {
     const uint64_t idx = tile_base + slot0 + r * 32;
     k[r] = idx < n ? __ldg(keys_in + idx) : ~0ull;  // padding ranks last (largest digit); never stored
   }
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   // ---- warp-level match ranking into per-warp counters (stable: (r, lane) order)
   uint16_t *wc = cnt + warp * R;
 #pragma unroll
-  for (int r = 0; r < kRadixItems; ++r) {
+  for (int r = 0; r < ITEMS; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & MASK;
     uint32_t peers = use_ballot ? match_ballot<BITS>(d) : __match_any_sync(0xFFFFFFFFu, d);
     if (r == 0) HT(tile, 1);
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
       tot += c;
     }
   }
-  uint64_t tile_end = tile_base + kRadixTile;
+  uint64_t tile_end = tile_base + TILE;
   const uint32_t pad_dg = (uint32_t)(~0ull >> shift) & MASK;  // the padding keys' digit
   if (is_dg && dg == pad_dg && tile_end > n) tot -= (uint32_t)(tile_end - n);
   unsigned long long *my_flag = lb + (uint64_t)tile * R + dg;
@@ -320,16 +321,16 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   // ---- exchange the keys through shared memory into tile-local digit order;
   // each slot's rank becomes its position (same thread, same slot)
 #pragma unroll
-  for (int r = 0; r < kRadixItems; ++r) {
+  for (int r = 0; r < ITEMS; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & MASK;
     uint32_t pos = s_local_start[d] + wc[d] + rk[slot0 + r * 32];
     xk[pos] = k[r];
     rk[slot0 + r * 32] = (uint16_t)pos;
   }
   // ---- the values: loaded now (the loads overlap the look-back), exchanged after it
-  uint32_t v[kRadixItems];
+  uint32_t v[ITEMS];
 #pragma unroll
-  for (int r = 0; r < kRadixItems; ++r) {
+  for (int r = 0; r < ITEMS; ++r) {
     const uint64_t idx = tile_base + slot0 + r * 32;
     v[r] = SYNTH_VALS ? (uint32_t)idx : (idx < n ? __ldg(vals_in + idx) : 0u);
   }
@@ -354,12 +355,12 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     s_gbase[dg] = (uint32_t)excl - local_start;  // modular; global = gbase + local position
   }
 #pragma unroll
-  for (int r = 0; r < kRadixItems; ++r) xv[rk[slot0 + r * 32]] = v[r];
+  for (int r = 0; r < ITEMS; ++r) xv[rk[slot0 + r * 32]] = v[r];
   __syncthreads();
   HT(tile, 5);
 
   // ---- scatter: consecutive local positions of a digit -> consecutive addresses
-  uint32_t n_valid = (uint32_t)((n - tile_base) < (uint64_t)kRadixTile ? (n - tile_base) : kRadixTile);
+  uint32_t n_valid = (uint32_t)((n - tile_base) < (uint64_t)TILE ? (n - tile_base) : TILE);
 #pragma unroll 4
   for (uint32_t i = tid; i < n_valid; i += kRadixThreads) {
     uint64_t key = xk[i];
@@ -434,38 +435,58 @@ extern "C" int husky_debug_tile_times(unsigned long long *out, int max_tiles) {
 #endif
 }
 
+template <int ITEMS>
+static void onesweep_host(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out, uint32_t *vals_out,
+                          uint64_t n, int digit, const uint32_t *ds, unsigned long long *lb, uint32_t *tile_counter,
+                          uint32_t epoch, const SlotPtrs &sp, cudaStream_t s) {
+  constexpr int kX = exchange_bytes<8, ITEMS>();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_onesweep<true, true, 8, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
+    cudaFuncSetAttribute(k_onesweep<false, true, 8, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
+    configured = true;
+  }
+  const uint64_t t = (uint64_t)kRadixThreads * ITEMS;
+  const uint32_t tiles = (uint32_t)((n + t - 1) / t);
+  if (vals_in == nullptr)
+    k_onesweep<true, true, 8, ITEMS><<<tiles, kRadixThreads, kX, s>>>(keys_in, nullptr, keys_out, vals_out, n,
+                                                                      8 * digit, ds, lb, tile_counter, epoch,
+                                                                      nullptr, tiles, nullptr, 0, sp);
+  else
+    k_onesweep<false, true, 8, ITEMS><<<tiles, kRadixThreads, kX, s>>>(keys_in, vals_in, keys_out, vals_out, n,
+                                                                       8 * digit, ds, lb, tile_counter, epoch,
+                                                                       nullptr, tiles, nullptr, 0, sp);
+}
+
 void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,
                      uint32_t *vals_out, uint64_t n, int digit, DevState *st,
                      unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s) {
   if (n == 0) return;
-  constexpr int kX = exchange_bytes<8>();
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_onesweep<true, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
-    cudaFuncSetAttribute(k_onesweep<false, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
-    cudaFuncSetAttribute(k_onesweep<true, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
-    cudaFuncSetAttribute(k_onesweep<false, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
-    configured = true;
-  }
   static const bool onesweep = [] {
     const char *v = getenv("HUSKY_RADIX");
     return !(v && v[0] == 'r');  // default onesweep; HUSKY_RADIX=rts: reduce-then-scan variant
   }();
   Scope sc_(ST_RADIX, s, n);
   const uint32_t *ds = st->digit_start[digit];
-  const uint32_t tiles = (uint32_t)radix_tiles(n);
   const SlotPtrs sp{nullptr, nullptr, nullptr, nullptr, nullptr, st};
-  dim3 g(tiles), b(kRadixThreads);
   if (onesweep) {
-    if (vals_in == nullptr)
-      k_onesweep<true, true, 8><<<g, b, kX, s>>>(keys_in, nullptr, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                 tile_counter, epoch, nullptr, tiles, nullptr, 0, sp);
+    if (radix_items(n) == kRadixItemsSmall)
+      onesweep_host<kRadixItemsSmall>(keys_in, vals_in, keys_out, vals_out, n, digit, ds, lb, tile_counter, epoch, sp, s);
     else
-      k_onesweep<false, true, 8><<<g, b, kX, s>>>(keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds, lb,
-                                                  tile_counter, epoch, nullptr, tiles, nullptr, 0, sp);
+      onesweep_host<kRadixItems>(keys_in, vals_in, keys_out, vals_out, n, digit, ds, lb, tile_counter, epoch, sp, s);
     return;
   }
-  // reduce-then-scan: the look-back buffer (tiles*256 u64) holds counts[256][tiles] u32
+  // reduce-then-scan (large tiles only): the look-back buffer (tiles*256 u64)
+  // holds counts[256][tiles] u32
+  constexpr int kX = exchange_bytes<8>();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_onesweep<true, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
+    cudaFuncSetAttribute(k_onesweep<false, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
+    configured = true;
+  }
+  const uint32_t tiles = (uint32_t)radix_tiles_large(n);
+  dim3 g(tiles), b(kRadixThreads);
   uint32_t *counts = reinterpret_cast<uint32_t *>(lb);
   k_rs_upsweep<<<tiles, kUpThreads, 0, s>>>(keys_in, n, 8 * digit, counts, tiles);
   k_rs_scan<<<256, 1024, 0, s>>>(counts, tiles, ds);
@@ -479,26 +500,42 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
 
 // Pass slot `slot` (0..7) of the device-side plan (kSlotBits-bit digits).
 // Launched unconditionally; the kernel resolves digit and buffers from DevState.
+template <int ITEMS>
+static void onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint32_t *vals_init,
+                          uint32_t *vals_final, uint32_t *vals_tmp, uint64_t n, DevState *st,
+                          unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s) {
+  constexpr int kX = exchange_bytes<kSlotBits, ITEMS>();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_onesweep<true, true, kSlotBits, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
+    cudaFuncSetAttribute(k_onesweep<false, true, kSlotBits, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
+    configured = true;
+  }
+  const uint64_t t = (uint64_t)kRadixThreads * ITEMS;
+  const uint32_t tiles = (uint32_t)((n + t - 1) / t);
+  SlotPtrs sp{keysA, keysB, vals_init, vals_final, vals_tmp, nullptr};
+  // programmatic dependent launch: the pass's CTAs become resident while the
+  // previous kernel's last wave drains and start as soon as it completes
+  auto k = (slot == 0 && vals_init == nullptr) ? k_onesweep<true, true, kSlotBits, ITEMS>
+                                               : k_onesweep<false, true, kSlotBits, ITEMS>;
+  launch_pdl(k, dim3(tiles), dim3(kRadixThreads), kX, s, (const uint64_t *)nullptr, (const uint32_t *)nullptr,
+             (uint64_t *)nullptr, (uint32_t *)nullptr, n, 0, (const uint32_t *)nullptr, lb, tile_counter, epoch,
+             (const uint32_t *)nullptr, tiles, (const DevState *)st, slot, sp);
+}
+
+// Pass slot `slot` (0..7) of the device-side plan (kSlotBits-bit digits).
+// Launched unconditionally; the kernel resolves digit and buffers from DevState.
 void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint32_t *vals_init,
                           uint32_t *vals_final, uint32_t *vals_tmp, uint64_t n, DevState *st,
                           unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s) {
   if (n == 0) return;
-  constexpr int kX = exchange_bytes<kSlotBits>();
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_onesweep<true, true, kSlotBits>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
-    cudaFuncSetAttribute(k_onesweep<false, true, kSlotBits>, cudaFuncAttributeMaxDynamicSharedMemorySize, kX);
-    configured = true;
-  }
-  // programmatic dependent launch: the pass's CTAs become resident while the
-  // previous kernel's last wave drains and start as soon as it completes
   Scope sc_(ST_RADIX, s, n);
-  const uint32_t tiles = (uint32_t)radix_tiles(n);
-  SlotPtrs sp{keysA, keysB, vals_init, vals_final, vals_tmp, nullptr};
-  auto k = (slot == 0 && vals_init == nullptr) ? k_onesweep<true, true, kSlotBits> : k_onesweep<false, true, kSlotBits>;
-  launch_pdl(k, dim3(tiles), dim3(kRadixThreads), kX, s, (const uint64_t *)nullptr, (const uint32_t *)nullptr,
-             (uint64_t *)nullptr, (uint32_t *)nullptr, n, 0, (const uint32_t *)nullptr, lb, tile_counter, epoch,
-             (const uint32_t *)nullptr, tiles, (const DevState *)st, slot, sp);
+  if (radix_items(n) == kRadixItemsSmall)
+    onesweep_slot<kRadixItemsSmall>(slot, keysA, keysB, vals_init, vals_final, vals_tmp, n, st, lb, tile_counter,
+                                    epoch, s);
+  else
+    onesweep_slot<kRadixItems>(slot, keysA, keysB, vals_init, vals_final, vals_tmp, n, st, lb, tile_counter, epoch,
+                               s);
 }
 
 void launch_radix_finalize(const DevState *st, const uint32_t *vals_init, uint32_t *vals_final, uint64_t n,
