@@ -208,15 +208,22 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
     if (CHECK) st_relaxed_u64(runs.lb + tile, make_flag(tile == 0 ? kFlagInc : kFlagAgg, epoch, tile_runs));
   }
 
-#if HUSKY_GATHER_PF == 1
-  // the long strings' units, for the staging below (issued after the publish)
-  if (PEER || sorted_units) {
+#if HUSKY_GATHER_PF == 1 || HUSKY_GATHER_PF == 3
+  // the long strings' units, for the staging below (issued after the publish).
+  // Main gather only: the re-gathers after a refinement (C4: every string long)
+  // measured faster without it (C4 gather 526 vs 582 us; C2 276 vs 286 us with)
+  if (CHECK && sorted_units) {
 #pragma unroll
     for (int j = 0; j < kGatherItems; ++j) {
       if (p0 + j < n && !((dec >> j) & 1) && len[j]) {
         const uint8_t *pa = (const uint8_t *)units + sv[j] * W;
+#if HUSKY_GATHER_PF == 1
         asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
         if ((((uintptr_t)pa & 127) + (uint64_t)len[j] * W) > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 127));
+#else
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
+        if ((((uintptr_t)pa & 127) + (uint64_t)len[j] * W) > 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + 127));
+#endif
       }
     }
   }
