@@ -162,38 +162,51 @@ __global__ void __launch_bounds__(256)
   // (P = 1, sorted or skewed input): per-lane atomics on one shared address
   // serialise (0.9 ms for 1e7 strings at P = 1)
   const uint32_t lane = lane_id();
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = base + threadIdx.x;
-    const bool valid = i < n;
-    uint32_t b = 0xFFFFFFFFu;
-    unsigned long long L = 0;
-    if (valid) {
-      const uint64_t c = codes[i];
-      const int64_t o = offsets[i];
-      L = (unsigned long long)(offsets[i + 1] - o);
-      const uint8_t *xs = (const uint8_t *)units + o * W;
-      int lo = 0, hi = nsplit;  // number of splitters <= x
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (ge_splitter<W>(c, xs, (int64_t)L, s_split[mid], general != 0)) lo = mid + 1;
-        else hi = mid;
-      }
-      b = (uint32_t)lo;
-      keys[i] = (uint64_t)lo;
-    }
-    const uint32_t b0 = __shfl_sync(0xFFFFFFFFu, b, 0);
-    if (__all_sync(0xFFFFFFFFu, b == b0 || !valid)) {
-      unsigned long long sum = L;
+  // kBucketIT strings per thread per round, their loads issued together (one
+  // string per thread per round left the kernel latency-bound: 87 us for 1e7)
+  constexpr int kBucketIT = 4;
+  const uint64_t step = (uint64_t)gridDim.x * blockDim.x * kBucketIT;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * kBucketIT; base < n; base += step) {
+    uint64_t cc[kBucketIT];
+    int64_t oo[kBucketIT], oe[kBucketIT];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-      const uint32_t nv = __popc(__ballot_sync(0xFFFFFFFFu, valid));
-      if (lane == 0 && nv) {
-        atomicAdd(&s_cnt[b0], (unsigned long long)nv);
-        atomicAdd(&s_units[b0], sum);
+    for (int k = 0; k < kBucketIT; ++k) {
+      const uint64_t i = base + threadIdx.x + (uint64_t)k * blockDim.x;
+      cc[k] = i < n ? codes[i] : 0ull;
+      oo[k] = i < n ? offsets[i] : 0;
+      oe[k] = i < n ? offsets[i + 1] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kBucketIT; ++k) {
+      const uint64_t i = base + threadIdx.x + (uint64_t)k * blockDim.x;
+      const bool valid = i < n;
+      uint32_t b = 0xFFFFFFFFu;
+      const unsigned long long L = valid ? (unsigned long long)(oe[k] - oo[k]) : 0ull;
+      if (valid) {
+        const uint8_t *xs = (const uint8_t *)units + oo[k] * W;
+        int lo = 0, hi = nsplit;  // number of splitters <= x
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (ge_splitter<W>(cc[k], xs, (int64_t)L, s_split[mid], general != 0)) lo = mid + 1;
+          else hi = mid;
+        }
+        b = (uint32_t)lo;
+        keys[i] = (uint64_t)lo;
       }
-    } else if (valid) {  // several buckets: few lanes share an address
-      atomicAdd(&s_cnt[b], 1ull);
-      atomicAdd(&s_units[b], L);
+      const uint32_t b0 = __shfl_sync(0xFFFFFFFFu, b, 0);
+      if (__all_sync(0xFFFFFFFFu, b == b0 || !valid)) {
+        unsigned long long sum = L;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+        const uint32_t nv = __popc(__ballot_sync(0xFFFFFFFFu, valid));
+        if (lane == 0 && nv) {
+          atomicAdd(&s_cnt[b0], (unsigned long long)nv);
+          atomicAdd(&s_units[b0], sum);
+        }
+      } else if (valid) {  // several buckets: few lanes share an address
+        atomicAdd(&s_cnt[b], 1ull);
+        atomicAdd(&s_units[b], L);
+      }
     }
   }
   __syncthreads();
