@@ -562,6 +562,12 @@ struct Plan {
   // phase 3a: stable partition by bucket (one onesweep pass on the bucket digit)
   husky_status partition() {
     if (n == 0) return HUSKY_OK;
+    // every string to one destination: the stable partition is the identity
+    if (std::count_if(send_cnt.begin(), send_cnt.end(), [](uint64_t c) { return c != 0; }) <= 1) {
+      launch_iota(at<uint32_t>(M.send_perm), n, s);
+      HCHECK(cudaGetLastError());
+      return HUSKY_OK;
+    }
     uint64_t *sorted_keys = nullptr;
     // bucket ids only occupy digit 0
     return S.radix(at<uint64_t>(M.L.keysB), nullptr, n, 0xFEu, at<uint32_t>(M.send_perm), at<uint32_t>(M.L.vals),
