@@ -12,9 +12,8 @@
 // codes, measured no faster -- husky_internal.cuh).
 // A pass works on tiles of kRadixTile = 6144 keys (512 threads x 12, warp-striped so every
 // load/store instruction is a coalesced 256-B access).  Each tile is ranked in
-// shared memory with warp-level label matching (__match_any_sync, or per-bit
-// ballots when the plan says the digit is spread out) + popc into per-warp
-// digit counters, exchanged through shared memory into digit order, and written
+// shared memory with warp-level label matching (two 4-bit __match_any_sync per
+// key, HUSKY_RANK_NIBBLE) + popc into per-warp digit counters, exchanged through shared memory into digit order, and written
 // out as runs of consecutive addresses.  The tile's global base per digit comes
 // from one of two schemes:
 //   * onesweep (default): per-(tile, digit) decoupled look-back (Adinets &
@@ -169,6 +168,16 @@ void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *
 }
 
 constexpr int kRadixWarps = kRadixThreads / 32;
+// Ranking primitive of a pass (the per-warp label match).  2 (default): every
+// digit as two 4-bit labels, peers = match_any(d >> 4) & match_any(d & 15) --
+// fewer distinct labels per MATCH and one code path (C2 1033 -> 1020 us, C3
+// 1119 -> 1118, C4 1823 -> 1820 us per sort).  0: the plan's rule, per-bit
+// ballots for spread digits (largest bin < 5%) and one 8-bit match_any for the
+// others; 1 / 3: the nibble pair for spread / for the other digits only (both
+// slower than 2: the two-primitive kernel schedules worse).
+#ifndef HUSKY_RANK_NIBBLE
+#define HUSKY_RANK_NIBBLE 2
+#endif
 #ifndef RADIX_LB_W
 #define RADIX_LB_W 12
 #endif
@@ -282,7 +291,20 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
 #pragma unroll
   for (int r = 0; r < ITEMS; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & MASK;
+#if HUSKY_RANK_NIBBLE == 1
+    // experiment: spread digits matched as two 4-bit labels (fewer distinct values per match)
+    uint32_t peers = use_ballot ? (__match_any_sync(0xFFFFFFFFu, d >> 4) & __match_any_sync(0xFFFFFFFFu, d & 15u))
+                                : __match_any_sync(0xFFFFFFFFu, d);
+#elif HUSKY_RANK_NIBBLE == 2
+    // experiment: every digit matched as two 4-bit labels
+    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> 4) & __match_any_sync(0xFFFFFFFFu, d & 15u);
+#elif HUSKY_RANK_NIBBLE == 3
+    // experiment: spread digits by ballots, the others as two 4-bit matches
+    uint32_t peers = use_ballot ? match_ballot<BITS>(d)
+                                : (__match_any_sync(0xFFFFFFFFu, d >> 4) & __match_any_sync(0xFFFFFFFFu, d & 15u));
+#else
     uint32_t peers = use_ballot ? match_ballot<BITS>(d) : __match_any_sync(0xFFFFFFFFu, d);
+#endif
     if (r == 0) HT(tile, 1);
     uint32_t pre = wc[d];
     rk[slot0 + r * 32] = (uint16_t)(pre + __popc(peers & lanemask_lt()));
