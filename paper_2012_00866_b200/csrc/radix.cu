@@ -12,9 +12,10 @@
 // codes, measured no faster -- husky_internal.cuh).
 // A pass works on tiles of kRadixTile = 6144 keys (512 threads x 12, warp-striped so every
 // load/store instruction is a coalesced 256-B access).  Each tile is ranked in
-// shared memory with warp-level label matching (two 4-bit __match_any_sync per
-// key, HUSKY_RANK_NIBBLE) + popc into per-warp digit counters, exchanged through shared memory into digit order, and written
-// out as runs of consecutive addresses.  The tile's global base per digit comes
+// shared memory with warp-level label matching (three __match_any_sync on the
+// digit's 3 + 3 + 2 bits, HUSKY_RANK_NIBBLE) + popc into per-warp digit
+// counters, exchanged through shared memory into digit order, and written out
+// as runs of consecutive addresses.  The tile's global base per digit comes
 // from one of two schemes:
 //   * onesweep (default): per-(tile, digit) decoupled look-back (Adinets &
 //     Merrill), global digit starts from the 8 digit histograms of the codes
@@ -168,15 +169,15 @@ void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *
 }
 
 constexpr int kRadixWarps = kRadixThreads / 32;
-// Ranking primitive of a pass (the per-warp label match).  2 (default): every
-// digit as two 4-bit labels, peers = match_any(d >> 4) & match_any(d & 15) --
-// fewer distinct labels per MATCH and one code path (C2 1033 -> 1020 us, C3
-// 1119 -> 1118, C4 1823 -> 1820 us per sort).  0: the plan's rule, per-bit
-// ballots for spread digits (largest bin < 5%) and one 8-bit match_any for the
-// others; 1 / 3: the nibble pair for spread / for the other digits only (both
-// slower than 2: the two-primitive kernel schedules worse).
+// Ranking primitive of a pass (the per-warp label match; MATCH costs grow with
+// the number of distinct labels in the warp).  4 (default): three matches of
+// the digit's 3 + 3 + 2 bits, peers = AND of the three.  Measured per sort
+// (C2 / C3 / C4, us): 0 = the plan's rule (ballots for spread
+// digits, one 8-bit match otherwise) 1033 / 1119 / 1823; 2 = two 4-bit matches
+// 1020 / 1119 / 1812; 4 = 3+3+2 bits 1019 / 1070 / 1767; 5 = four 2-bit matches
+// 1024-1031 / 1056-1060 / 1765; 7 = ballots for every digit 1083 / 1080 / 1785.
 #ifndef HUSKY_RANK_NIBBLE
-#define HUSKY_RANK_NIBBLE 2
+#define HUSKY_RANK_NIBBLE 4
 #endif
 #ifndef RADIX_LB_W
 #define RADIX_LB_W 12
@@ -291,18 +292,22 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
 #pragma unroll
   for (int r = 0; r < ITEMS; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & MASK;
-#if HUSKY_RANK_NIBBLE == 1
-    // experiment: spread digits matched as two 4-bit labels (fewer distinct values per match)
-    uint32_t peers = use_ballot ? (__match_any_sync(0xFFFFFFFFu, d >> 4) & __match_any_sync(0xFFFFFFFFu, d & 15u))
-                                : __match_any_sync(0xFFFFFFFFu, d);
+#if HUSKY_RANK_NIBBLE == 4
+    // default: three matches of 3 + 3 + 2 bits
+    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> 5) & __match_any_sync(0xFFFFFFFFu, (d >> 2) & 7u) &
+                     __match_any_sync(0xFFFFFFFFu, d & 3u);
 #elif HUSKY_RANK_NIBBLE == 2
-    // experiment: every digit matched as two 4-bit labels
+    // two 4-bit matches
     uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> 4) & __match_any_sync(0xFFFFFFFFu, d & 15u);
-#elif HUSKY_RANK_NIBBLE == 3
-    // experiment: spread digits by ballots, the others as two 4-bit matches
-    uint32_t peers = use_ballot ? match_ballot<BITS>(d)
-                                : (__match_any_sync(0xFFFFFFFFu, d >> 4) & __match_any_sync(0xFFFFFFFFu, d & 15u));
+#elif HUSKY_RANK_NIBBLE == 5
+    // four 2-bit matches
+    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> 6) & __match_any_sync(0xFFFFFFFFu, (d >> 4) & 3u) &
+                     __match_any_sync(0xFFFFFFFFu, (d >> 2) & 3u) & __match_any_sync(0xFFFFFFFFu, d & 3u);
+#elif HUSKY_RANK_NIBBLE == 7
+    // per-bit ballots for every digit
+    uint32_t peers = match_ballot<BITS>(d);
 #else
+    // the plan's rule: per-bit ballots for spread digits, one 8-bit match otherwise
     uint32_t peers = use_ballot ? match_ballot<BITS>(d) : __match_any_sync(0xFFFFFFFFu, d);
 #endif
     if (r == 0) HT(tile, 1);
