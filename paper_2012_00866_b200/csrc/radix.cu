@@ -293,9 +293,11 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
   for (int r = 0; r < ITEMS; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & MASK;
 #if HUSKY_RANK_NIBBLE == 4
-    // default: three matches of 3 + 3 + 2 bits
-    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> 5) & __match_any_sync(0xFFFFFFFFu, (d >> 2) & 7u) &
-                     __match_any_sync(0xFFFFFFFFu, d & 3u);
+    // default: three matches of 3 + 3 + 2 bits (3 + 3 + 3 for 9-bit digits)
+    constexpr int kLo = BITS - 6;
+    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> (kLo + 3)) &
+                     __match_any_sync(0xFFFFFFFFu, (d >> kLo) & 7u) &
+                     __match_any_sync(0xFFFFFFFFu, d & ((1u << kLo) - 1u));
 #elif HUSKY_RANK_NIBBLE == 2
     // two 4-bit matches
     uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> 4) & __match_any_sync(0xFFFFFFFFu, d & 15u);
