@@ -477,14 +477,10 @@ static void onesweep_host(const uint64_t *keys_in, const uint32_t *vals_in, uint
   }
   const uint64_t t = (uint64_t)kRadixThreads * ITEMS;
   const uint32_t tiles = (uint32_t)((n + t - 1) / t);
-  if (vals_in == nullptr)
-    k_onesweep<true, true, 8, ITEMS><<<tiles, kRadixThreads, kX, s>>>(keys_in, nullptr, keys_out, vals_out, n,
-                                                                      8 * digit, ds, lb, tile_counter, epoch,
-                                                                      nullptr, tiles, nullptr, 0, sp);
-  else
-    k_onesweep<false, true, 8, ITEMS><<<tiles, kRadixThreads, kX, s>>>(keys_in, vals_in, keys_out, vals_out, n,
-                                                                       8 * digit, ds, lb, tile_counter, epoch,
-                                                                       nullptr, tiles, nullptr, 0, sp);
+  // programmatic dependent launches here too (refinement rounds, partitions)
+  auto k = vals_in == nullptr ? k_onesweep<true, true, 8, ITEMS> : k_onesweep<false, true, 8, ITEMS>;
+  launch_pdl(k, dim3(tiles), dim3(kRadixThreads), kX, s, keys_in, vals_in, keys_out, vals_out, n, 8 * digit, ds, lb,
+             tile_counter, epoch, (const uint32_t *)nullptr, tiles, (const DevState *)nullptr, 0, sp);
 }
 
 void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,
