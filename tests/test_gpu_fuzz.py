@@ -25,7 +25,7 @@ def _case(seed):
     coder = int(rng.integers(0, 4))
     alph = ALPHABETS[coder][int(rng.integers(0, len(ALPHABETS[coder])))]
     alph = np.frombuffer(alph, dtype=np.uint8) if isinstance(alph, bytes) else np.asarray(alph, dtype=np.uint16)
-    n = int(rng.choice([0, 1, 2, 31, 33, 1023, 1025, 2049, 4095, 4097, 8193, 12345, 30000]))
+    n = int(rng.choice([0, 1, 2, 31, 33, 1023, 1025, 2049, 4095, 4097, 8193, 12345, 30000, 614401]))
     maxlen = int(rng.choice([0, 3, 9, 10, 13, 24, 40]))
     dup = float(rng.choice([0.0, 0.3, 0.9]))
     strings = []

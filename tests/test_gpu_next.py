@@ -108,7 +108,7 @@ def _keys_case(key_type, n, seed):
 
 
 @pytest.mark.parametrize("key_type", [0, 1, 2])
-@pytest.mark.parametrize("n", [1, 2, 4095, 4097, 6143, 6145, 12289, 300_001, 2_000_000])
+@pytest.mark.parametrize("n", [1, 2, 4095, 4097, 6143, 6145, 12289, 300_001, 614_401, 2_000_000])
 def test_sort_keys_vs_oracle(torch, h, oracle_mod, key_type, n):
     k = _keys_case(key_type, n, 100 + n + key_type)
     dk = torch.from_numpy(k.view(np.int64).copy()).cuda()

@@ -141,7 +141,9 @@ def test_encode_rejects_bad_offsets(torch, h):
 
 # ------------------------------------------------------------ full sort
 @pytest.mark.parametrize("n", [0, 1, 2, 3, 17, 1023, 1024, 1025, 2047, 2049, 4095, 4096, 4097, 6143, 6144, 6145,
-                               12287, 12289, 18433, 70001])
+                               12287, 12289, 18433, 70001, 499_999, 500_000, 614_399, 614_401])
+# (below 5e5 keys the radix uses 2048-key tiles, from 5e5 on 6144-key tiles: the
+# last four sizes straddle the switch and a ragged 6144-key tail)
 def test_sort_sizes_ragged(torch, h, oracle_mod, n):
     w = rand_wl(n, n, range(0x61, 0x65), 0, 14)
     check_against_oracle(torch, h, oracle_mod, w)
