@@ -171,11 +171,15 @@ void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *
 constexpr int kRadixWarps = kRadixThreads / 32;
 // Ranking primitive of a pass (the per-warp label match; MATCH costs grow with
 // the number of distinct labels in the warp).  4 (default): three matches of
-// the digit's 3 + 3 + 2 bits, peers = AND of the three.  Measured per sort
-// (C2 / C3 / C4, us): 0 = the plan's rule (ballots for spread
-// digits, one 8-bit match otherwise) 1033 / 1119 / 1823; 2 = two 4-bit matches
-// 1020 / 1119 / 1812; 4 = 3+3+2 bits 1019 / 1070 / 1767; 5 = four 2-bit matches
-// 1024-1031 / 1056-1060 / 1765; 7 = ballots for every digit 1083 / 1080 / 1785.
+// the digit's 3 + 3 + 2 bits, peers = AND of the three (9 was as fast in the
+// lab and faster on C3 / C4, but 1% slower on C2 in the bench, the headline).
+// Measured per sort (C2 / C3 / C4, us): 0 = the plan's rule
+// (ballots for spread digits, one 8-bit match otherwise) 1033 / 1119 / 1823;
+// 2 = two 4-bit matches 1020 / 1119 / 1812; 4 = 3+3+2 bits by matches
+// 1020 / 1072 / 1745; 9 = 3+3 by matches + 2 ballots 1021-1027 / 1051 / 1731;
+// 10 = 4+2 by matches + 2 ballots 1022 / 1058-1062 / 1722-1728; 5 = four 2-bit
+// matches 1024-1031 / 1056-1060 / 1765; 7 = ballots for every digit
+// 1083 / 1080 / 1785.
 #ifndef HUSKY_RANK_NIBBLE
 #define HUSKY_RANK_NIBBLE 4
 #endif
@@ -298,6 +302,20 @@ __global__ void __launch_bounds__(kRadixThreads, kRadixMinBlocks)
     uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> (kLo + 3)) &
                      __match_any_sync(0xFFFFFFFFu, (d >> kLo) & 7u) &
                      __match_any_sync(0xFFFFFFFFu, d & ((1u << kLo) - 1u));
+#elif HUSKY_RANK_NIBBLE == 9
+    // the top bits by two 3-bit matches, the low BITS - 6 bits by ballots
+    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> (BITS - 3)) &
+                     __match_any_sync(0xFFFFFFFFu, (d >> (BITS - 6)) & 7u);
+#pragma unroll
+    for (int b = 0; b < BITS - 6; ++b) {
+      const uint32_t v = __ballot_sync(0xFFFFFFFFu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? v : ~v;
+    }
+#elif HUSKY_RANK_NIBBLE == 10
+    // experiment: 4 + 2 bits by match, the low 2 bits by two ballots
+    const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, d & 1u), b1 = __ballot_sync(0xFFFFFFFFu, d & 2u);
+    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> 4) & __match_any_sync(0xFFFFFFFFu, (d >> 2) & 3u) &
+                     ((d & 1u) ? b0 : ~b0) & ((d & 2u) ? b1 : ~b1);
 #elif HUSKY_RANK_NIBBLE == 2
     // two 4-bit matches
     uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> 4) & __match_any_sync(0xFFFFFFFFu, d & 15u);
