@@ -31,7 +31,7 @@ def build(force: bool = False) -> str:
     """Compile husky_oracle.c -> liboracle.so with gcc (no CUDA involved)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-pthread", "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -52,6 +52,8 @@ def _load():
         lib.oracle_verify.restype = ctypes.c_int64
         lib.oracle_huskysort_alg1.argtypes = [ctypes.c_int, P, P, U64, P, P, P]
         lib.oracle_huskysort_alg1.restype = ctypes.c_int
+        lib.oracle_sort_mt.argtypes = [ctypes.c_int, P, P, U64, P, ctypes.c_int]
+        lib.oracle_sort_mt.restype = ctypes.c_int
         lib.oracle_sort_keys.argtypes = [ctypes.c_int, P, U64, P]
         lib.oracle_sort_keys.restype = ctypes.c_int
         _lib = lib
@@ -89,6 +91,17 @@ def sort(coder, units, offsets):
     rc = _load().oracle_sort(coder, _p(units), _p(offsets), n, _p(perm))
     if rc:
         raise ValueError(f"oracle_sort rc={rc}")
+    return perm[:n]
+
+
+def sort_mt(coder, units, offsets, threads):
+    """-> perm uint32[n]: the same result as sort(), computed as `threads` chunk
+    merge sorts + pairwise merge rounds (CPU baseline at T = nproc)."""
+    units, offsets, n = _prep(coder, units, offsets)
+    perm = np.zeros(max(n, 1), dtype=np.uint32)
+    rc = _load().oracle_sort_mt(coder, _p(units), _p(offsets), n, _p(perm), int(threads))
+    if rc:
+        raise ValueError(f"oracle_sort_mt rc={rc}")
     return perm[:n]
 
 

@@ -34,6 +34,7 @@
  * the paper / SPEC state, closed forms, brute force over all pairs on tiny
  * alphabets, and Python's library sort.  Nothing is parity-unpinned.
  */
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -200,6 +201,82 @@ int oracle_sort(int coder, const void *units, const int64_t *offsets, uint64_t n
   merge_sort(&c, perm, tmp, 0, n);
   free(tmp);
   return 0;
+}
+
+/* T-thread variant of oracle_sort, for the CPU baseline at T = nproc
+ * (SURVEY.md 8(d)): the same plain definition, split as T chunk merge sorts
+ * (the textbook merge_sort above, one pthread per chunk) followed by rounds of
+ * pairwise merges of adjacent chunks with the same cmp.  Merging adjacent,
+ * individually sorted chunks with "take the right element only if strictly
+ * smaller" is exactly the merge step of merge_sort, so the result equals
+ * oracle_sort's (pinned in tests/test_oracle_pins_next.py).  0 ok, 1 bad arg,
+ * 2 OOM / thread failure. */
+typedef struct {
+  const ctx_t *c;
+  uint32_t *a, *tmp;
+  uint64_t lo, mid, hi;
+  int merge_only;
+} mt_job_t;
+
+static void merge_runs(const ctx_t *c, uint32_t *a, uint32_t *tmp, uint64_t lo, uint64_t mid, uint64_t hi) {
+  uint64_t i = lo, j = mid, k = lo;
+  while (i < mid && j < hi) {
+    if (cmp_idx(c, a[j], a[i]) < 0) tmp[k++] = a[j++];
+    else tmp[k++] = a[i++];
+  }
+  while (i < mid) tmp[k++] = a[i++];
+  while (j < hi) tmp[k++] = a[j++];
+  memcpy(a + lo, tmp + lo, (hi - lo) * sizeof(uint32_t));
+}
+
+static void *mt_worker(void *arg) {
+  mt_job_t *j = (mt_job_t *)arg;
+  if (j->merge_only) merge_runs(j->c, j->a, j->tmp, j->lo, j->mid, j->hi);
+  else merge_sort(j->c, j->a, j->tmp, j->lo, j->hi);
+  return NULL;
+}
+
+int oracle_sort_mt(int coder, const void *units, const int64_t *offsets, uint64_t n, uint32_t *perm, int threads) {
+  if (!known_coder(coder) || threads < 1 || threads > 1024) return 1;
+  if (n > 0xFFFFFFFFull) return 1;
+  if (threads == 1 || n < 2 * (uint64_t)threads) return oracle_sort(coder, units, offsets, n, perm);
+  ctx_t c = {coder, units, offsets};
+  for (uint64_t i = 0; i < n; i++) perm[i] = (uint32_t)i;
+  uint32_t *tmp = (uint32_t *)malloc(n * sizeof(uint32_t));
+  uint64_t *bound = (uint64_t *)malloc((threads + 1) * sizeof(uint64_t));
+  pthread_t *tid = (pthread_t *)malloc(threads * sizeof(pthread_t));
+  mt_job_t *jobs = (mt_job_t *)malloc(threads * sizeof(mt_job_t));
+  int rc = 0;
+  if (!tmp || !bound || !tid || !jobs) { rc = 2; goto out; }
+  for (int t = 0; t <= threads; t++) bound[t] = n * (uint64_t)t / (uint64_t)threads;
+  int runs = threads;
+  for (int t = 0; t < runs; t++) {
+    jobs[t] = (mt_job_t){&c, perm, tmp, bound[t], 0, bound[t + 1], 0};
+    if (pthread_create(&tid[t], NULL, mt_worker, &jobs[t])) { rc = 2; runs = t; break; }
+  }
+  for (int t = 0; t < runs; t++) pthread_join(tid[t], NULL);
+  if (rc) goto out;
+  /* rounds of pairwise merges: runs [bound[2k], bound[2k+1]) + [bound[2k+1], bound[2k+2]) */
+  while (runs > 1) {
+    int pairs = runs / 2, started = 0;
+    for (int k = 0; k < pairs; k++) {
+      jobs[k] = (mt_job_t){&c, perm, tmp, bound[2 * k], bound[2 * k + 1], bound[2 * k + 2], 1};
+      if (pthread_create(&tid[k], NULL, mt_worker, &jobs[k])) { rc = 2; break; }
+      started++;
+    }
+    for (int k = 0; k < started; k++) pthread_join(tid[k], NULL);
+    if (rc) goto out;
+    int m = 0;
+    for (int k = 0; k < runs; k += 2) bound[m++] = bound[k];
+    bound[m] = n;
+    runs = m;
+  }
+out:
+  free(tmp);
+  free(bound);
+  free(tid);
+  free(jobs);
+  return rc;
 }
 
 /* sorted_units = concatenation of strings in perm order; sorted_offsets[0] = 0. */

@@ -139,3 +139,26 @@ def test_sort_keys_doubles_java_order(oracle_mod):
     arr = np.array(xs, dtype=np.float64)
     perm = oracle_mod.sort_keys(2, arr)
     assert perm.tolist() == sorted(range(len(xs)), key=lambda i: _java_double_key(xs[i], i))
+
+
+# ---------------------------------------------- T-thread oracle (CPU baseline)
+@pytest.mark.parametrize("threads", [1, 2, 3, 5, 8, 13])
+def test_sort_mt_matches_library_sort(oracle_mod, threads):
+    """oracle_sort_mt (chunk merge sorts + pairwise merge rounds) reaches the
+    plain definition: pinned against Python's library sort (duplicates across
+    chunk boundaries, empty strings, prefixes), not only against oracle_sort."""
+    rng = random.Random(100 + threads)
+    pool = [bytes(rng.choice(b"ab\x00z") for _ in range(rng.randint(0, 5))) for _ in range(300)]
+    strings = [rng.choice(pool) for _ in range(5000)]
+    w = W.from_strings([list(s) for s in strings], 0)
+    perm = oracle_mod.sort_mt(0, w.units, w.offsets, threads)
+    assert perm.tolist() == sorted(range(len(strings)), key=lambda i: (strings[i], i))
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 7, 16, 17])
+def test_sort_mt_tiny(oracle_mod, n):
+    rng = random.Random(n)
+    strings = [[rng.randint(0, 0xFFFF) for _ in range(rng.randint(0, 3))] for _ in range(n)]
+    w = W.from_strings(strings, 1)
+    for t in (1, 4, 8):
+        assert np.array_equal(oracle_mod.sort_mt(1, w.units, w.offsets, t), oracle_mod.sort(1, w.units, w.offsets))

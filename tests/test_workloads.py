@@ -1,5 +1,6 @@
 """Generators produce the shapes BASELINE.json's configs describe (CPU only)."""
 import numpy as np
+import pytest
 
 import workloads as W
 
@@ -51,7 +52,40 @@ def test_c5_shape():
     w = W.c5(1 << 16)
     L = _lens(w)
     assert L.min() == 8 and L.max() == 24
+    assert abs(L.mean() - 16.0) < 0.1
+    assert set(np.unique(w.units).tolist()) == set(W.ALNUM.tolist())
     n_sorted = w.meta["sorted"]
+    assert n_sorted == (1 << 16) // 10
     s = [w.units[w.offsets[i]:w.offsets[i + 1]].tobytes() for i in range(w.n)]
     assert all(s[i] <= s[i + 1] for i in range(n_sorted - 1))
+    assert not all(s[i] <= s[i + 1] for i in range(n_sorted, w.n - 1))
+    # ~1% Bernoulli targets; each copies a non-target's string
+    assert 0.008 < w.meta["dup"] / w.n < 0.012
     assert w.n - len(set(s)) >= w.meta["dup"] * 0.9
+
+
+def test_c5_recipe_counter_based():
+    """Targets copy the string (length and units) of a non-target position, and
+    the content of a position depends only on its identity."""
+    seed, N = W.MASTER_SEED + 5, 1 << 20
+    pos = np.arange(200_000, 260_000, dtype=np.int64)
+    ident = W.c5_ident(seed, N, pos)
+    t = W.c5_is_target(seed, pos)
+    assert np.array_equal(ident[~t], pos[~t])
+    assert (ident[t] != pos[t]).all() and not W.c5_is_target(seed, ident[t]).any()
+    assert (ident >= 0).all() and (ident < N).all()
+    u1, o1 = W.c5_chars(seed, ident[t][:50], W.c5_len(seed, ident[t][:50]))
+    u2, o2 = W.c5_chars(seed, ident[t][:50].copy(), W.c5_len(seed, ident[t][:50]))
+    assert np.array_equal(u1, u2) and np.array_equal(o1, o2)
+
+
+@pytest.mark.parametrize("base,n", [(0, 1000), (3000, 9000), (6000, 500), (65000, 536)])
+def test_c5_blocks_of_one_dataset(base, n):
+    """Block [base, base + n) of the global dataset equals the same slice of the
+    whole dataset (what each rank of a sharded run generates)."""
+    N = 1 << 16
+    whole = W.c5(N)
+    blk = W.c5(n, base=base, n_total=N)
+    o = whole.offsets
+    assert np.array_equal(blk.units, whole.units[o[base]:o[base + n]])
+    assert np.array_equal(blk.offsets, o[base:base + n + 1] - o[base])

@@ -148,25 +148,78 @@ def c4(n: int = FULL_N["C4"], seed: int = MASTER_SEED + 4) -> Workload:
 
 
 # ------------------------------------------------------------------- C5
+# Counter-based recipe (reading R14): every quantity of global
+# position i is a function of (seed, stream, counter), so any rank can produce
+# block [base, base + n) of ONE global dataset without the others (the CUDA
+# twin in workloads/gen.cu implements the same arithmetic; tests compare them).
+#   len_i      = 8 + hi32(h(0, i)) * 17 >> 32                       (U{8..24})
+#   target_i   = hi32(h(1, i)) < 42949673   (= ceil(0.01 * 2^32))  (Bernoulli 1%)
+#   source_i   = first j_a = hi32(h(2, 64 i + a)) * N >> 32, a = 0, 1, ..., that
+#                is not a target (a < 64)                            (uniform non-target)
+#   ident_i    = source_i if target_i else i;  the string of i is the string of ident_i
+#   char k of identity x = ALNUM[hi32(h(3, 32 x + k)) * 62 >> 32]
+#   positions [0, floor(0.1 N)) then hold their strings in ascending order
+#   (stable: equal strings keep position order).
+# h(s, x) = splitmix64(x + splitmix64(seed * 0x100000001B3 + s)).
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+C5_DUP_THRESH = 42949673      # ceil(0.01 * 2^32)
+C5_SRC_TRIES = 64
 
 
 def _splitmix64(x: np.ndarray) -> np.ndarray:
     """Counter-based generator (splitmix64 finaliser) on uint64 arrays."""
     with np.errstate(over="ignore"):
-        z = x + np.uint64(0x9E3779B97F4A7C15)
+        z = np.asarray(x, dtype=np.uint64) + np.uint64(0x9E3779B97F4A7C15)
         z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         return z ^ (z >> np.uint64(31))
 
 
-def _c5_units(ident: np.ndarray, lens: np.ndarray, seed: int) -> tuple[np.ndarray, np.ndarray]:
-    """String content is a function of (seed, identity, position): copies share identity."""
+def _c5_stream(seed: int, s: int) -> np.uint64:
+    with np.errstate(over="ignore"):
+        return _splitmix64(np.array([seed], dtype=np.uint64) * np.uint64(0x100000001B3) + np.uint64(s))[0]
+
+
+def _h(seed: int, s: int, x: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        return _splitmix64(np.asarray(x, dtype=np.uint64) + _c5_stream(seed, s))
+
+
+def _hi_mul(h: np.ndarray, m: int) -> np.ndarray:
+    """(hi32(h) * m) >> 32 as int64 (m < 2^32)."""
+    return (((h >> np.uint64(32)) * np.uint64(m)) >> np.uint64(32)).astype(np.int64)
+
+
+def c5_len(seed: int, pos: np.ndarray) -> np.ndarray:
+    return 8 + _hi_mul(_h(seed, 0, pos), 17)
+
+
+def c5_is_target(seed: int, pos: np.ndarray) -> np.ndarray:
+    return (_h(seed, 1, pos) >> np.uint64(32)) < np.uint64(C5_DUP_THRESH)
+
+
+def c5_ident(seed: int, N: int, pos: np.ndarray) -> np.ndarray:
+    """Identity (whose string position i carries) before the prefix sort."""
+    pos = np.asarray(pos, dtype=np.int64)
+    ident = pos.copy()
+    t = np.nonzero(c5_is_target(seed, pos))[0]
+    pend = t
+    for a in range(C5_SRC_TRIES):
+        if pend.size == 0:
+            break
+        with np.errstate(over="ignore"):
+            j = _hi_mul(_h(seed, 2, pos[pend].astype(np.uint64) * np.uint64(64) + np.uint64(a)), N)
+        ok = ~c5_is_target(seed, j)
+        ident[pend[ok]] = j[ok]
+        pend = pend[~ok]
+    return ident
+
+
+def c5_chars(seed: int, ident: np.ndarray, lens: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """units + offsets of the strings of the given identities and lengths."""
     off = _offsets(lens)
     units = np.empty(int(off[-1]), dtype=np.uint8)
     step = 1 << 22
-    with np.errstate(over="ignore"):
-        s64 = np.uint64(seed) * np.uint64(0x100000001B3)
     for s in range(0, ident.size, step):
         e = min(ident.size, s + step)
         L = lens[s:e]
@@ -174,50 +227,51 @@ def _c5_units(ident: np.ndarray, lens: np.ndarray, seed: int) -> tuple[np.ndarra
         cnt = int(off[e]) - base
         rel = (np.arange(cnt, dtype=np.int64) - np.repeat(off[s:e] - base, L)).astype(np.uint64)
         with np.errstate(over="ignore"):
-            ctr = (np.repeat(ident[s:e].astype(np.uint64), L) << np.uint64(5)) + rel + s64
-        units[base:base + cnt] = ALNUM[(_splitmix64(ctr) % np.uint64(62)).astype(np.int64)]
+            ctr = (np.repeat(ident[s:e].astype(np.uint64), L) << np.uint64(5)) + rel
+        units[base:base + cnt] = ALNUM[_hi_mul(_h(seed, 3, ctr), 62)]
     return units, off
 
 
-def c5(n: int = FULL_N["C5"], seed: int = MASTER_SEED + 5, dup_frac: float = 0.01,
-       sorted_frac: float = 0.10) -> Workload:
-    """C5: len uniform in [8, 24], chars uniform [0-9A-Za-z]; floor(0.01 n) positions are
-    overwritten with copies of uniformly chosen non-target positions; then the first
-    floor(0.1 n) strings are put in ascending order (partially ordered input)."""
-    g = _rng(seed)
-    lens = g.integers(8, 25, size=n, dtype=np.int64)
-    ident = np.arange(n, dtype=np.int64)
-    n_dup = int(n * dup_frac)
-    if n_dup:
-        is_t = np.zeros(n, dtype=bool)
-        t = np.unique(g.integers(0, n, size=n_dup + n_dup // 4 + 16))
-        while t.size < n_dup:
-            t = np.unique(np.concatenate([t, g.integers(0, n, size=n_dup)]))
-        t = g.permutation(t)[:n_dup]
-        is_t[t] = True
-        src = g.integers(0, n, size=n_dup + n_dup // 8 + 16)
-        src = src[~is_t[src]]
-        while src.size < n_dup:
-            more = g.integers(0, n, size=n_dup)
-            src = np.concatenate([src, more[~is_t[more]]])
-        src = src[:n_dup]
-        ident[t] = ident[src]
-        lens[t] = lens[src]
-    units, off = _c5_units(ident, lens, seed)
-    n_sorted = int(n * sorted_frac)
-    if n_sorted > 1:
-        # input preparation: put the first n_sorted strings in ascending order.
-        # Strings are alphanumeric (no NUL), so NUL-padded fixed-width byte
-        # comparison equals lexicographic order with shorter-prefix-first.
-        fixed = np.zeros((n_sorted, 24), dtype=np.uint8)
-        L = lens[:n_sorted]
-        rel = np.arange(int(off[n_sorted]), dtype=np.int64) - np.repeat(off[:n_sorted], L)
-        fixed[np.repeat(np.arange(n_sorted), L), rel] = units[:off[n_sorted]]
-        order = np.argsort(fixed.view("S24").reshape(-1), kind="stable")
-        ident[:n_sorted] = ident[:n_sorted][order]
-        lens[:n_sorted] = lens[:n_sorted][order]
-        units, off = _c5_units(ident, lens, seed)
-    return Workload("C5", ASCII, units, off, {"seed": seed, "n": n, "dup": n_dup, "sorted": n_sorted})
+def c5_sorted_prefix_ident(seed: int, N: int) -> np.ndarray:
+    """Identities of positions [0, floor(0.1 N)) after the prefix sort."""
+    ns = N // 10
+    ident = c5_ident(seed, N, np.arange(ns, dtype=np.int64))
+    lens = c5_len(seed, ident)
+    units, off = c5_chars(seed, ident, lens)
+    # NUL-padded 24-byte keys: strings are alphanumeric (no NUL), so padded
+    # comparison is lexicographic order with a proper prefix first
+    fixed = np.zeros((ns, 24), dtype=np.uint8)
+    rel = np.arange(int(off[-1]), dtype=np.int64) - np.repeat(off[:-1], lens)
+    fixed[np.repeat(np.arange(ns), lens), rel] = units
+    order = np.argsort(fixed.view("S24").reshape(-1), kind="stable")
+    return ident[order]
+
+
+def c5_block(N: int, base: int, n: int, seed: int = MASTER_SEED + 5) -> tuple[np.ndarray, np.ndarray]:
+    """Identities + lengths of positions [base, base + n) of the global N-string C5."""
+    pos = np.arange(base, base + n, dtype=np.int64)
+    ident = c5_ident(seed, N, pos)
+    ns = N // 10
+    if base < ns and ns > 1:
+        pre = c5_sorted_prefix_ident(seed, N)
+        e = min(ns, base + n)
+        ident[:e - base] = pre[base:e]
+    return ident, c5_len(seed, ident)
+
+
+def c5(n: int = FULL_N["C5"], seed: int = MASTER_SEED + 5, base: int = 0, n_total: int | None = None) -> Workload:
+    """C5: len uniform in [8, 24], chars uniform [0-9A-Za-z], ~1% of positions
+    (Bernoulli) carry a copy of a uniformly chosen non-target position's string,
+    and the first floor(0.1 N) positions are in ascending order (partially
+    ordered input).  base / n_total: block [base, base + n) of an n_total-string
+    dataset (default: the whole dataset of n strings)."""
+    N = n if n_total is None else n_total
+    ident, lens = c5_block(N, base, n, seed)
+    units, off = c5_chars(seed, ident, lens)
+    return Workload("C5", ASCII, units, off,
+                    {"seed": seed, "n": n, "N": N, "base": base,
+                     "dup": int(np.count_nonzero(c5_is_target(seed, np.arange(base, base + n)))),
+                     "sorted": N // 10})
 
 
 GENERATORS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5}
