@@ -82,12 +82,13 @@ typedef struct {
   uint64_t runs_by_class[4];/* [0] already ordered (check only)  [1] warp-sorted (<=32)
                                [2] CTA-sorted (<=4096)           [3] giant (refined)     */
   uint32_t refine_rounds;   /* giant-run refinement rounds (re-key + segment radix)      */
-  uint32_t radix_passes;    /* key-sort partition passes: non-trivial 8-bit LSD passes
-                               (default), or MSD levels (HUSKY_KEYSORT=msd); refinement
-                               (A6) passes are added                                     */
+  uint32_t radix_passes;    /* key-sort partition passes: non-trivial 8-bit LSD passes;
+                               refinement (A6) passes are added                          */
   uint64_t keys_partitioned;/* keys moved by the main key sort's passes, summed          */
-  uint64_t keys_local;      /* keys sorted in shared memory by the MSD local sort        */
   uint32_t exchange;        /* multi-GPU transport of the strings (husky_exchange)       */
+  uint64_t bytes_to_peers;  /* multi-GPU: string bytes + 8 B (length, global index) per
+                               string this rank sent to OTHER ranks (NVLink traffic)      */
+  uint64_t bytes_from_peers;/* multi-GPU: the same, received from other ranks            */
 } husky_outcome;
 
 /* How a sample sort moved the strings between ranks (husky_outcome.exchange). */
@@ -209,6 +210,8 @@ husky_status husky_sort_host_many(int coder, int k, const void *const *h_units, 
 husky_status husky_comm_unique_id(uint8_t id[128]);
 /* Creates the NCCL communicator on the current CUDA device. */
 husky_status husky_comm_create(int rank, int world, const uint8_t id[128], void **comm);
+/* The world size `comm` was created with (for husky_sort_multi_workspace). */
+husky_status husky_comm_world(void *comm, int *world);
 husky_status husky_comm_destroy(void *comm);
 
 /* Phase 1: encode, sample splitters (all-gather), count, exchange counts.
@@ -280,13 +283,19 @@ husky_status husky_select_splitters(int coder, const void *h_units, const int64_
 /* --------------------------------------------------------------- profiling
  * Per-stage accounting (the T1/T2/T3 split of PAPER.md:238-245, per kernel
  * family).  Every kernel launch is counted; with profiling enabled each launch
- * is also bracketed by a CUDA event pair on its own stream.  Stage ids:
+ * is also bracketed by a CUDA event pair on its own stream (mode 1), or only
+ * the encoder, histogram, radix-pass and main-gather groups are (mode 2: four
+ * event pairs per sort, cheap enough inside a timed region).  Stage ids:
  * 0 encode, 1 hist_scan, 2 radix_pass, 3 runs_scan, 4 runs_classify,
  * 5 fix_small, 6 fix_medium, 7 refine, 8 gather, 9 multi.
  * husky_profile_read fills up to max_stages entries (ms = summed device time,
  * launches, elems = summed elements processed) and returns the stage count. */
 void husky_profile_enable(int on);
 void husky_profile_reset(void);
+/* Profiling mode 1 (an event pair per launch) also logs every launch in order:
+ * copies up to max_records (stage id, elements, device ms) and returns how
+ * many are logged (at most 65536 since the last reset). */
+int husky_profile_launches(int *stages, uint64_t *elems, double *ms, int max_records);
 int husky_profile_read(double *ms, uint64_t *launches, uint64_t *elems, int max_stages);
 const char *husky_profile_stage_name(int stage);
 uint64_t husky_launch_count(void);

@@ -46,16 +46,16 @@ class husky_outcome(ctypes.Structure):
                 ("n_runs", ctypes.c_uint64), ("n_in_runs", ctypes.c_uint64),
                 ("max_run", ctypes.c_uint64), ("runs_by_class", ctypes.c_uint64 * 4),
                 ("refine_rounds", ctypes.c_uint32), ("radix_passes", ctypes.c_uint32),
-                ("keys_partitioned", ctypes.c_uint64), ("keys_local", ctypes.c_uint64),
-                ("exchange", ctypes.c_uint32)]
+                ("keys_partitioned", ctypes.c_uint64), ("exchange", ctypes.c_uint32),
+                ("bytes_to_peers", ctypes.c_uint64), ("bytes_from_peers", ctypes.c_uint64)]
 
     def as_dict(self):
         return {"perfect": bool(self.perfect), "domain_ok": bool(self.domain_ok),
                 "n_runs": self.n_runs, "n_in_runs": self.n_in_runs, "max_run": self.max_run,
                 "runs_by_class": list(self.runs_by_class), "refine_rounds": self.refine_rounds,
                 "radix_passes": self.radix_passes,
-                "keys_partitioned": self.keys_partitioned, "keys_local": self.keys_local,
-                "exchange": self.exchange}
+                "keys_partitioned": self.keys_partitioned, "exchange": self.exchange,
+                "bytes_to_peers": self.bytes_to_peers, "bytes_from_peers": self.bytes_from_peers}
 
 
 if not os.path.exists(LIB_PATH):
@@ -97,13 +97,15 @@ EXPORTED = ["husky_unit_bytes", "husky_encode", "husky_sort_workspace", "husky_s
             "husky_sort_multi_loopback", "husky_select_splitters", "husky_last_error",
             "husky_profile_enable", "husky_profile_reset", "husky_profile_read",
             "husky_profile_stage_name", "husky_launch_count", "husky_sort_keys_workspace",
-            "husky_sort_keys", "husky_sort_host_many_workspace", "husky_sort_host_many"]
+            "husky_sort_keys", "husky_sort_host_many_workspace", "husky_sort_host_many",
+            "husky_profile_launches", "husky_comm_world"]
 
 _sig("husky_profile_enable", None, _I)
 _sig("husky_profile_reset", None)
 _sig("husky_profile_read", _I, _P, _P, _P, _I)
 _sig("husky_profile_stage_name", ctypes.c_char_p, _I)
 _sig("husky_launch_count", _U64)
+_sig("husky_profile_launches", _I, _P, _P, _P, _I)
 
 
 def husky_profile_enable(on=True):
@@ -126,6 +128,15 @@ def husky_profile_read() -> dict:
     n = _lib.husky_profile_read(ms, la, el, k)
     return {_lib.husky_profile_stage_name(i).decode(): {"ms": ms[i], "launches": la[i], "elems": el[i]}
             for i in range(min(n, k))}
+
+
+def husky_profile_launches(max_records=65536) -> list:
+    """Mode-1 launch log since the last reset: [(stage_name, elems, ms), ...] in launch order."""
+    st = (ctypes.c_int * max_records)()
+    el = (ctypes.c_uint64 * max_records)()
+    ms = (ctypes.c_double * max_records)()
+    k = min(int(_lib.husky_profile_launches(st, el, ms, max_records)), max_records)
+    return [(_lib.husky_profile_stage_name(st[i]).decode(), int(el[i]), float(ms[i])) for i in range(k)]
 
 
 def husky_launch_count() -> int:
@@ -276,7 +287,7 @@ def husky_sort_host_many(coder, batches, ws, depth=2):
     return [outs[i].as_dict() for i in range(k)]
 
 
-from .multi import (husky_comm_create, husky_comm_destroy, husky_comm_unique_id,  # noqa: E402
+from .multi import (husky_comm_create, husky_comm_destroy, husky_comm_unique_id, husky_comm_world,  # noqa: E402
                     husky_plan_destroy, husky_select_splitters, husky_sort_multi,
                     husky_sort_multi_exec, husky_sort_multi_plan, husky_sort_multi_recv_workspace,
                     husky_sort_multi_loopback, husky_sort_multi_loopback_workspace,

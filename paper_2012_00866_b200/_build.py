@@ -70,5 +70,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_cub_bar(force: bool = False) -> str:
+    """tools/libcubbar.so: cub::DeviceRadixSort::SortPairs, the stage-2 library bar
+    bench.py reports beside the hand-written onesweep (bench infrastructure)."""
+    src = os.path.join(ROOT, "tools", "cub_bar.cu")
+    out = os.path.join(ROOT, "tools", "libcubbar.so")
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
+        tmp = out + f".tmp{os.getpid()}"
+        subprocess.check_call([NVCC, "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", *ARCH, "-o", tmp, src])
+        os.replace(tmp, out)
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

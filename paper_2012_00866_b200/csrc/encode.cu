@@ -6,12 +6,20 @@
 // of asciiToLong is a 3-step mask/shift compaction instead of
 // a 9-step fold, and unicodeToLong's 16-bit packing + ">>> 1"
 // is a half-word swap.  Fused into the same pass (no extra HBM read):
-//   * the OR / NOT-AND of all codes (the MSD key sort's level-0 digit),
 //   * Alg. 3's `perfect` flag as an OR of "not perfect",
 //   * the ASCII domain check (unit > 0x7F inside the code window; reading R5),
-//   * the offsets monotonicity check.
+//   * the offsets monotonicity check,
+//   * the string slab (ASCII / UNICODE, when the caller asks for sorted
+//     strings): a 16-byte record per string -- its length and the units that
+//     follow the code window (ASCII units 9..23, UNICODE units 3..9) -- written
+//     in input order, so the gather (A4) fetches a string of up to 24 / 10
+//     units with ONE random 16-byte read (units [0, S) come back out of the
+//     sorted code) instead of a random offsets read followed by a random units
+//     read.  Random reads past ~2 GB are capped at ~36 G accesses/s whatever
+//     their size (profiles/r02_random_access_probe.txt), so the number of
+//     random accesses per string, not bytes, sets the gather's time.
 // The LSD radix's 8 x 256 digit histograms come from a separate read of the
-// codes (k_hist8), which measured cheaper than fusing them here.
+// codes (k_hist_slots), which measured cheaper than fusing them here.
 #include <algorithm>
 
 #include "husky_internal.cuh"
@@ -80,6 +88,32 @@ __device__ __forceinline__ uint64_t encode_words(uint64_t w0, uint64_t w1, uint6
   }
 }
 
+// Slab record of one string (ASCII / UNICODE): byte 0 = length if it is at
+// most kSlabMax units, else 0xFF (the gather then reads offsets and units);
+// bytes 1..15 = string bytes [S*W, S*W + 15), zero past the end.  `win` holds
+// the string's bytes starting at window byte `sh` (words w0..w3 from the
+// aligned word at or below the string start).
+template <int CODER>
+__device__ __forceinline__ uint4 make_slab(uint64_t w0, uint64_t w1, uint64_t w2, uint64_t w3, int sh, int64_t len) {
+  using T = CoderTraits<CODER>;
+  constexpr int W = T::kUnitBytes, SB = T::kS * W;  // slab's first string byte
+  const uint32_t lcode = (len >= 0 && len <= T::kSlabMax) ? (uint32_t)len : 0xFFu;
+  const int base = sh + SB;            // window byte of string byte SB
+  const int q = base >> 3, r = (base & 7) * 8;
+  const uint64_t a = q == 0 ? w0 : (q == 1 ? w1 : w2);
+  const uint64_t b = q == 0 ? w1 : (q == 1 ? w2 : w3);
+  const uint64_t c = q == 0 ? w2 : w3;
+  uint64_t lo = r ? ((a >> r) | (b << (64 - r))) : a;  // string bytes SB .. SB+7
+  uint64_t hi = r ? ((b >> r) | (c << (64 - r))) : b;  // SB+8 .. SB+15
+  // zero the bytes past the end of the string
+  const int64_t keep = len > T::kS ? (len - T::kS) * W : 0;  // string bytes present from SB
+  if (keep < 8) { lo &= keep > 0 ? ((1ull << (8 * keep)) - 1) : 0ull; hi = 0; }
+  else if (keep < 15) hi &= (1ull << (8 * (keep - 8))) - 1;
+  // record bytes: [0] = lcode, [1..8] = lo, [9..15] = hi bytes 0..6
+  const uint64_t r0 = (uint64_t)lcode | (lo << 8), r1 = (lo >> 56) | (hi << 8);
+  return make_uint4((uint32_t)r0, (uint32_t)(r0 >> 32), (uint32_t)r1, (uint32_t)(r1 >> 32));
+}
+
 // One thread per string, IT strings in flight per thread (grid-stride over a
 // persistent grid).  Lane i of a warp codes string i of 32 consecutive strings,
 // whose units are contiguous, so the window loads of a warp fall in a few
@@ -89,24 +123,22 @@ __device__ __forceinline__ uint64_t encode_words(uint64_t w0, uint64_t w1, uint6
 // cover units[offsets[0] .. offsets[n]): for valid offsets the words a window
 // needs are always inside, so they are issued unconditionally without ever
 // leaving the caller's buffer.
-#ifndef HUSKY_ENC_IT
-#define HUSKY_ENC_IT 4
-#endif
-constexpr int kEncIT = HUSKY_ENC_IT;
+// slab (nullable): the slab records; slab_all: write every string's record
+// (the gather needs every length), else only those longer than PL (the packed
+// payload carries the others' lengths and the code their units).
+constexpr int kEncIT = 4;
 template <int CODER>
 // 4 CTAs per SM (64 registers): measured per C2 / C3 encode 76 / 62 us, against
 // 81 / 71 us unbounded (79 registers, 3 CTAs), 87 / 83 us at 5 and 92 / 89 us at
 // 6 CTAs per SM (spills) -- the kernel is latency-bound on its two dependent loads
-#ifndef HUSKY_ENC_MINB
-#define HUSKY_ENC_MINB 4
-#endif
-__global__ void __launch_bounds__(kEncThreads, HUSKY_ENC_MINB) k_encode(const void *__restrict__ units,
+__global__ void __launch_bounds__(kEncThreads, 4) k_encode(const void *__restrict__ units,
                                                         const int64_t *__restrict__ offsets, uint64_t n,
-                                                        uint64_t *__restrict__ codes, DevState *st,
-                                                        uint32_t *__restrict__ packed) {
+                                                        uint64_t *__restrict__ codes, uint32_t *viol_out,
+                                                        uint32_t *__restrict__ packed, uint4 *__restrict__ slab,
+                                                        int slab_all) {
   constexpr int W = CoderTraits<CODER>::kUnitBytes;
+  constexpr bool kSlabCoder = CODER == HUSKY_CODER_ASCII || CODER == HUSKY_CODER_UNICODE;
   uint32_t viol = 0;
-  unsigned long long kor = 0, knand = 0;  // OR and NOT-AND of the codes (MSD level 0)
   const uint32_t lane = lane_id();
   const uintptr_t ub = (uintptr_t)units;
   const int64_t ofirst = __ldg(offsets), olast = __ldg(offsets + n);
@@ -129,15 +161,18 @@ __global__ void __launch_bounds__(kEncThreads, HUSKY_ENC_MINB) k_encode(const vo
     }
     constexpr bool kThird = CODER == HUSKY_CODER_ENGLISH5 || CODER == HUSKY_CODER_ENGLISH6;
     uint64_t w0[kEncIT], w1[kEncIT], w2[kEncIT];
+    uintptr_t awk[kEncIT];
     int sh[kEncIT];
 #pragma unroll
     for (int k = 0; k < kEncIT; ++k) {
       const uintptr_t a = ub + (uintptr_t)(o0[k] * W);
       sh[k] = (int)(a & 7);
       w2[k] = 0;
+      awk[k] = lo_word;
       if (any_units) {
         uintptr_t aw = a & ~(uintptr_t)7;
         aw = aw < lo_word ? lo_word : (aw > hi_word ? hi_word : aw);
+        awk[k] = aw;
         const uintptr_t aw1 = aw + 8 > hi_word ? hi_word : aw + 8;
         w0[k] = __ldg((const uint64_t *)aw);
         w1[k] = __ldg((const uint64_t *)aw1);
@@ -153,65 +188,60 @@ __global__ void __launch_bounds__(kEncThreads, HUSKY_ENC_MINB) k_encode(const vo
 #pragma unroll
     for (int k = 0; k < kEncIT; ++k) {
       const uint64_t i = base + threadIdx.x + (uint64_t)k * blockDim.x;
-      const uint64_t c = encode_words<CODER>(w0[k], w1[k], w2[k], sh[k], o1[k] - o0[k], viol);
+      const int64_t L = o1[k] - o0[k];
+      const uint64_t c = encode_words<CODER>(w0[k], w1[k], w2[k], sh[k], L, viol);
       if (i < n) {
         codes[i] = c;
-        kor |= c;
-        knand |= ~c;
         // initial radix payload: index | min(len, 15) << 28 (n <= 2^28 only)
-        if (packed) {
-          const int64_t L = o1[k] - o0[k];
-          packed[i] = (uint32_t)i | ((uint32_t)(L < 0 ? 0 : (L > 15 ? 15 : L)) << 28);
+        if (packed) packed[i] = (uint32_t)i | ((uint32_t)(L < 0 ? 0 : (L > 15 ? 15 : L)) << 28);
+        if constexpr (kSlabCoder) {
+          if (slab && (slab_all || L > CoderTraits<CODER>::kPL)) {
+            // the words after the code window (mostly the same lines: L1
+            // hits), only for strings that reach past it
+            uint64_t x2 = 0, x3 = 0;
+            if (L > CoderTraits<CODER>::kS) {
+              const uintptr_t aw2 = awk[k] + 16 > hi_word ? hi_word : awk[k] + 16;
+              const uintptr_t aw3 = awk[k] + 24 > hi_word ? hi_word : awk[k] + 24;
+              x2 = __ldg((const uint64_t *)aw2);
+              x3 = __ldg((const uint64_t *)aw3);
+            }
+            slab[i] = make_slab<CODER>(w0[k], w1[k], x2, x3, sh[k], L);
+          }
         }
       }
     }
   }
-  // reduce violation bits: one atomic per warp that saw any; OR / NOT-AND per CTA
+  // reduce violation bits: one atomic per warp that saw any
   viol = __reduce_or_sync(0xFFFFFFFFu, viol);
-  if (lane == 0 && viol) atomicOr(&st->violations, viol);
-  __shared__ unsigned long long s_ao[2][kEncThreads / 32];
-  const uint32_t a = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)kor), b = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)(kor >> 32));
-  const uint32_t c = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)knand), d = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)(knand >> 32));
-  if (lane == 0) {
-    s_ao[0][threadIdx.x >> 5] = ((unsigned long long)b << 32) | a;
-    s_ao[1][threadIdx.x >> 5] = ((unsigned long long)d << 32) | c;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long x = 0, y = 0;
-    for (int w = 0; w < kEncThreads / 32; ++w) {
-      x |= s_ao[0][w];
-      y |= s_ao[1][w];
-    }
-    if (x) atomicOr(&st->key_or, x);
-    if (y) atomicOr(&st->key_nand, y);
-  }
+  if (lane == 0 && viol) atomicOr(viol_out, viol);
 }
 
-void launch_encode(int coder, bool hist, const void *units, const int64_t *offsets, uint64_t n,
-                   uint64_t *codes, DevState *st, int num_sms, cudaStream_t s, uint32_t *packed) {
+void launch_encode(int coder, const void *units, const int64_t *offsets, uint64_t n, uint64_t *codes,
+                   uint32_t *viol, int num_sms, cudaStream_t s, uint32_t *packed, uint4 *slab, bool slab_all) {
   if (n == 0) return;
-  {
-    Scope sc_(ST_ENCODE, s, n);
-    uint64_t blocks = (n + kEncThreads * kEncIT - 1) / (kEncThreads * kEncIT);
-    const uint64_t cap = (uint64_t)num_sms * kEncBlocksPerSM;
-    if (blocks > cap) blocks = cap;
-    switch (coder) {
-      case HUSKY_CODER_ASCII:
-        k_encode<HUSKY_CODER_ASCII><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, st, packed);
-        break;
-      case HUSKY_CODER_UNICODE:
-        k_encode<HUSKY_CODER_UNICODE><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, st, packed);
-        break;
-      case HUSKY_CODER_ENGLISH5:
-        k_encode<HUSKY_CODER_ENGLISH5><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, st, packed);
-        break;
-      default:
-        k_encode<HUSKY_CODER_ENGLISH6><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, st, packed);
-        break;
-    }
+  Scope sc_(ST_ENCODE, s, n);
+  uint64_t blocks = (n + kEncThreads * kEncIT - 1) / (kEncThreads * kEncIT);
+  const uint64_t cap = (uint64_t)num_sms * kEncBlocksPerSM;
+  if (blocks > cap) blocks = cap;
+  const int sa = slab_all ? 1 : 0;
+  switch (coder) {
+    case HUSKY_CODER_ASCII:
+      k_encode<HUSKY_CODER_ASCII><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, viol, packed,
+                                                                           slab, sa);
+      break;
+    case HUSKY_CODER_UNICODE:
+      k_encode<HUSKY_CODER_UNICODE><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, viol, packed,
+                                                                             slab, sa);
+      break;
+    case HUSKY_CODER_ENGLISH5:
+      k_encode<HUSKY_CODER_ENGLISH5><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, viol, packed,
+                                                                              nullptr, 0);
+      break;
+    default:
+      k_encode<HUSKY_CODER_ENGLISH6><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, viol, packed,
+                                                                              nullptr, 0);
+      break;
   }
-  if (hist) launch_hist_slots(codes, n, st, num_sms, s);
 }
 
 }  // namespace husky

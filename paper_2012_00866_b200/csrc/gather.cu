@@ -65,11 +65,11 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
              const int64_t *__restrict__ offsets, void *__restrict__ sorted_units,
              int64_t *__restrict__ sorted_offsets, unsigned long long *lb, uint32_t *tile_counter,
              uint32_t epoch, const int64_t *base_ptr, int dbg, const uint64_t *__restrict__ codes,
-             const DevState *st, GatherRuns runs, const PeerTable *peer) {
+             const DevState *st, GatherRuns runs, const PeerTable *peer, const uint4 *__restrict__ slab) {
   using T = CoderTraits<CODER>;
   constexpr int W = T::kUnitBytes;
   constexpr uint32_t PL = T::kPL;
-  extern __shared__ __align__(16) uint8_t stage[];  // kGatherStage + 32 bytes
+  extern __shared__ __align__(16) uint8_t stage[];  // kGatherStage + 32 bytes (+ slab records, CHECK)
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_wt[kGatherThreads / 32 + 1];
   __shared__ unsigned long long s_base, s_rbase;
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   const uint32_t tile = s_tile;
   const uint64_t p0 = (uint64_t)tile * kGatherTile + (uint64_t)tid * kGatherItems;
   GT(tile, 0);
-  if (CHECK && st && (st->trivial_mask == 0xFFu || st->msd_all_equal) && n > 1) {
+  if (CHECK && st && st->trivial_mask == 0xFFu && n > 1) {
     // every code is equal: the whole array is one run, which the fix-up or the
     // refinement (A6) reorders and gathers again -- gathering it here in code
     // order would be thrown away (C4).  Unpack perm, record the run as dirty.
@@ -118,13 +118,18 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   }
 
   // per item: len (units) and either the source offset or, for strings rebuilt
-  // from their code, the code itself (bit j of `dec`)
+  // from their code, the code itself (bit j of `dec`); slab strings (bit j of
+  // `slb`): units [0, S) from the code, the rest from the 16-byte slab record
+  // in sl[j] -- one random read instead of offsets + units (encode.cu)
   uint32_t raw[kGatherItems];
 #pragma unroll
   for (int j = 0; j < kGatherItems; ++j) raw[j] = p0 + j < n ? perm[p0 + j] : 0u;
   uint64_t sv[kGatherItems], cc[kGatherItems];
   uint32_t len[kGatherItems], ix[kGatherItems];
-  uint32_t dec = 0;
+  // slab records parked in shared memory ([item][thread]: conflict-free 16-B
+  // accesses) until the staging, so they hold no registers across the scan
+  uint4 *s_slab = reinterpret_cast<uint4 *>(stage + kGatherStage + 32);
+  uint32_t dec = 0, slb = 0;
   unsigned long long mine = 0;
 #pragma unroll
   for (int j = 0; j < kGatherItems; ++j) {
@@ -142,10 +147,16 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       }
       ix[j] = idx;
       if (CHECK) cc[j] = __ldg(codes + p0 + j);
+      uint4 rec = make_uint4(0xFFu, 0, 0, 0);
       if (PACKED && lc <= PL) {
         dec |= 1u << j;
         len[j] = lc;
         sv[j] = CHECK ? cc[j] : __ldg(codes + p0 + j);
+      } else if (CHECK && slab != nullptr && (rec = __ldg(slab + idx), (rec.x & 0xFFu) != 0xFFu)) {
+        slb |= 1u << j;
+        len[j] = rec.x & 0xFFu;
+        sv[j] = cc[j];
+        s_slab[j * kGatherThreads + tid] = rec;
       } else {
         const int64_t a = __ldg(offsets + idx);
         sv[j] = (uint64_t)a;
@@ -215,7 +226,7 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   if (CHECK && sorted_units) {
 #pragma unroll
     for (int j = 0; j < kGatherItems; ++j) {
-      if (p0 + j < n && !((dec >> j) & 1) && len[j]) {
+      if (p0 + j < n && !(((dec | slb) >> j) & 1) && len[j]) {
         const uint8_t *pa = (const uint8_t *)units + sv[j] * W;
 #if HUSKY_GATHER_PF == 1
         asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
@@ -244,6 +255,13 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       if (lo < hi) {
         if (PACKED && ((dec >> j) & 1)) {
           for (uint64_t x = lo; x < hi; ++x) stage[x - w0] = decode_byte<CODER>(sv[j], (int)(x - d));
+        } else if (CHECK && ((slb >> j) & 1)) {
+          constexpr int SB = T::kS * W;  // string bytes [0, SB) come from the code
+          const uint4 rec = s_slab[j * kGatherThreads + tid];
+          for (uint64_t x = lo; x < hi; ++x) {
+            const int b = (int)(x - d);
+            stage[x - w0] = b < SB ? decode_byte<CODER>(sv[j], b) : slab_byte(rec, b - SB + 1);
+          }
         } else {
           const uint8_t *sp = ub + sv[j] * W;
           for (uint64_t x = lo; x < hi; x += 8) {
@@ -450,7 +468,12 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
         uint64_t s = __shfl_sync(0xFFFFFFFFu, sv[j], t);
         uint32_t l = __shfl_sync(0xFFFFFFFFu, len[j], t);
         uint64_t nb = (uint64_t)l * W;
-        if (PACKED && ((dt >> j) & 1)) {
+        if (CHECK && ((__shfl_sync(0xFFFFFFFFu, slb, t) >> j) & 1)) {
+          const uint4 r = s_slab[j * kGatherThreads + (warp * 32 + t)];
+          constexpr int SB = T::kS * W;
+          for (uint64_t b = lane; b < nb; b += 32)
+            ob[d * W + b] = b < SB ? decode_byte<CODER>(s, (int)b) : slab_byte(r, (int)b - SB + 1);
+        } else if (PACKED && ((dt >> j) & 1)) {
           for (uint64_t b = lane; b < nb; b += 32) ob[d * W + b] = decode_byte<CODER>(s, (int)b);
         } else {
           for (uint64_t b = lane; b < nb; b += 32) ob[d * W + b] = ub[s * W + b];
@@ -464,19 +487,9 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
 void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, const int64_t *offsets,
                    void *sorted_units, int64_t *sorted_offsets, unsigned long long *lb,
                    uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, const int64_t *base_ptr,
-                   bool packed, const uint64_t *packed_codes, const DevState *st, const GatherRunsOut *runs_out) {
+                   bool packed, const uint64_t *packed_codes, const DevState *st, const GatherRunsOut *runs_out,
+                   const uint4 *slab) {
   if (n == 0) return;
-  constexpr int kSmem = kGatherStage + 32;
-  static bool configured = false;
-  if (!configured) {
-#define G_ATTR(C, P, K) cudaFuncSetAttribute(k_gather<C, P, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem)
-    G_ATTR(HUSKY_CODER_ASCII, true, false); G_ATTR(HUSKY_CODER_ASCII, false, false);
-    G_ATTR(HUSKY_CODER_UNICODE, true, false); G_ATTR(HUSKY_CODER_UNICODE, false, false);
-    G_ATTR(HUSKY_CODER_ASCII, true, true); G_ATTR(HUSKY_CODER_ASCII, false, true);
-    G_ATTR(HUSKY_CODER_UNICODE, true, true); G_ATTR(HUSKY_CODER_UNICODE, false, true);
-#undef G_ATTR
-    configured = true;
-  }
   Scope sc_(ST_GATHER, s, n);
   dim3 g((unsigned)gather_tiles(n)), b(kGatherThreads);
   // HUSKY_DEBUG_GATHER: bit 0 forces the unstaged copy, bit 1 the serial look-back
@@ -486,27 +499,34 @@ void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, con
   }();
   GatherRuns runs{};
   if (runs_out) runs = GatherRuns{runs_out->run_start, runs_out->run_end, runs_out->dirty, runs_out->lb, runs_out->st};
-#define G_ARGS \
-  perm, n, units, offsets, sorted_units, sorted_offsets, lb, tile_counter, epoch, base_ptr, dbg, packed_codes, st, runs, nullptr
   const bool chk = runs_out != nullptr;
+  if (!chk) slab = nullptr;  // slab records are read by the main (CHECK) gather only
+#define G_LAUNCH(C, P, K)                                                                                         \
+  do {                                                                                                            \
+    constexpr int kSmem = kGatherStage + 32 + (K ? kGatherTile * 16 : 0);                                         \
+    static SmemAttr attr;                                                                                         \
+    attr.ensure(k_gather<C, P, K, false>, kSmem);                                                                 \
+    launch_pdl(k_gather<C, P, K, false>, g, b, kSmem, s, perm, n, units, offsets, sorted_units, sorted_offsets, lb, \
+               tile_counter, epoch, base_ptr, dbg, packed_codes, st, runs, (const PeerTable *)nullptr, slab);     \
+  } while (0)
   if (coder == HUSKY_CODER_ASCII) {
     if (packed) {
-      if (chk) launch_pdl(k_gather<HUSKY_CODER_ASCII, true, true, false>, g, b, kSmem, s, G_ARGS);
-      else k_gather<HUSKY_CODER_ASCII, true, false, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) G_LAUNCH(HUSKY_CODER_ASCII, true, true);
+      else G_LAUNCH(HUSKY_CODER_ASCII, true, false);
     } else {
-      if (chk) launch_pdl(k_gather<HUSKY_CODER_ASCII, false, true, false>, g, b, kSmem, s, G_ARGS);
-      else k_gather<HUSKY_CODER_ASCII, false, false, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) G_LAUNCH(HUSKY_CODER_ASCII, false, true);
+      else G_LAUNCH(HUSKY_CODER_ASCII, false, false);
     }
   } else {
     if (packed) {
-      if (chk) launch_pdl(k_gather<HUSKY_CODER_UNICODE, true, true, false>, g, b, kSmem, s, G_ARGS);
-      else k_gather<HUSKY_CODER_UNICODE, true, false, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) G_LAUNCH(HUSKY_CODER_UNICODE, true, true);
+      else G_LAUNCH(HUSKY_CODER_UNICODE, true, false);
     } else {
-      if (chk) launch_pdl(k_gather<HUSKY_CODER_UNICODE, false, true, false>, g, b, kSmem, s, G_ARGS);
-      else k_gather<HUSKY_CODER_UNICODE, false, false, false><<<g, b, kSmem, s>>>(G_ARGS);
+      if (chk) G_LAUNCH(HUSKY_CODER_UNICODE, false, true);
+      else G_LAUNCH(HUSKY_CODER_UNICODE, false, false);
     }
   }
-#undef G_ARGS
+#undef G_LAUNCH
 }
 
 void launch_gather_peer(int coder, const uint32_t *perm, uint64_t n, const void *units, const int64_t *offsets,
@@ -514,25 +534,22 @@ void launch_gather_peer(int coder, const uint32_t *perm, uint64_t n, const void 
                         cudaStream_t s) {
   if (n == 0) return;
   constexpr int kSmem = kGatherStage + 32;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_gather<HUSKY_CODER_ASCII, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmem);
-    cudaFuncSetAttribute(k_gather<HUSKY_CODER_UNICODE, false, false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    configured = true;
-  }
   Scope sc_(ST_MULTI, s, n);
   dim3 g((unsigned)gather_tiles(n)), b(kGatherThreads);
   uint32_t *pm = const_cast<uint32_t *>(perm);  // read only (PACKED = false)
-  if (coder == HUSKY_CODER_ASCII)
+  if (coder == HUSKY_CODER_ASCII) {
+    static SmemAttr attr;
+    attr.ensure(k_gather<HUSKY_CODER_ASCII, false, false, true>, kSmem);
     k_gather<HUSKY_CODER_ASCII, false, false, true><<<g, b, kSmem, s>>>(
         pm, n, units, offsets, nullptr, nullptr, lb, tile_counter, epoch, nullptr, 0, nullptr, nullptr, GatherRuns{},
-        d_table);
-  else
+        d_table, nullptr);
+  } else {
+    static SmemAttr attr;
+    attr.ensure(k_gather<HUSKY_CODER_UNICODE, false, false, true>, kSmem);
     k_gather<HUSKY_CODER_UNICODE, false, false, true><<<g, b, kSmem, s>>>(
         pm, n, units, offsets, nullptr, nullptr, lb, tile_counter, epoch, nullptr, 0, nullptr, nullptr, GatherRuns{},
-        d_table);
+        d_table, nullptr);
+  }
 }
 
 // perm-only mode with a packed payload: strip the length bits

@@ -16,12 +16,9 @@ namespace husky {
 // Workspace layout of husky_sort for n strings (byte offsets, 256-aligned).
 struct Layout {
   uint64_t n = 0, tiles_r = 0, tiles_s = 0, cap_sm = 0, cap_g = 0;
-  size_t state = 0, keysA = 0, keysB = 0, vals = 0, vals2 = 0, lb_radix = 0, lb_scan = 0, run_start = 0,
+  size_t state = 0, keysA = 0, keysB = 0, vals = 0, vals2 = 0, slab = 0, lb_radix = 0, lb_scan = 0, run_start = 0,
          run_end = 0, dirty = 0, list_sm = 0, list_g = 0, total = 0;
   uint64_t lb_radix_words = 0;
-  // MSD key sort (msd.cu)
-  size_t keysC = 0, vals3 = 0, segs[2] = {0, 0}, tile_seg[2] = {0, 0}, hist = 0, seg_or = 0, seg_nand = 0,
-         cont = 0, win_lo = 0, win_hi = 0;
 };
 Layout make_layout(uint64_t n);
 
@@ -62,6 +59,7 @@ struct Sorter {
   uint32_t epoch = 0;
   uint32_t slot = 0;
   uint32_t radix_passes = 0, refine_rounds = 0;
+  cudaError_t err = cudaSuccess;  // first failure of the bookkeeping resets (checked at the sync points)
 
   template <typename T> T *at(size_t o) const { return reinterpret_cast<T *>(ws + o); }
   uint64_t *keysA() const { return at<uint64_t>(L.keysA); }
@@ -79,14 +77,16 @@ struct Sorter {
   // next look-back epoch (1..255); wraps by clearing the flag arrays
   uint32_t next_epoch() {
     if (++epoch > 255) {
-      reset_lookback();
+      cudaError_t e = reset_lookback();
+      if (err == cudaSuccess) err = e;
       epoch = 1;
     }
     return epoch;
   }
   uint32_t *next_counter() {
     if (slot == 64) {
-      cudaMemsetAsync(st->tile_counter, 0, sizeof(st->tile_counter), s);
+      cudaError_t e = cudaMemsetAsync(st->tile_counter, 0, sizeof(st->tile_counter), s);
+      if (err == cudaSuccess) err = e;
       slot = 0;
     }
     return st->tile_counter + slot++;

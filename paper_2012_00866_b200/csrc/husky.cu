@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <atomic>
 #include <thread>
 #include <utility>
 #include <vector>
@@ -47,13 +48,6 @@ int device_sm_count() {
   return sms > 0 ? sms : 148;
 }
 
-// Key sort variant: LSD onesweep (default) or HUSKY_KEYSORT=msd, the MSD hybrid
-// of msd.cu (measured slower on every config so far: DESIGN.md section 6.2).
-bool keysort_msd() {
-  const char *v = getenv("HUSKY_KEYSORT");
-  return v && v[0] == 'm';
-}
-
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 Layout make_layout(uint64_t n) {
@@ -73,12 +67,11 @@ Layout make_layout(uint64_t n) {
   L.keysA = take(n * 8);
   L.keysB = take(n * 8);
   L.vals = take(n * 4);
-  L.vals2 = take(n * 4);  // packed initial payload (index | len << 28) when n <= 2^28
-  {
-    // the LSD passes and the MSD levels share the look-back words (and their epochs)
-    uint64_t w = radix_lb_words(n), wm = msd_max_tiles(n) * 256 + 2;
-    L.lb_radix_words = w > wm ? w : wm;
-  }
+  // packed initial payload (index | min(len, 15) << 28), only when n <= 2^28
+  L.vals2 = take(n <= kPackMaxN ? n * 4 : 0);
+  // string slab records for the main gather (16 B per string, encode.cu)
+  L.slab = take(n * 16);
+  L.lb_radix_words = radix_lb_words(n);
   L.lb_radix = take(L.lb_radix_words * 8);
   L.lb_scan = take(L.tiles_s * 16);  // two look-back arrays (lengths, run counts)
   L.run_start = take(L.cap_sm * 4);
@@ -86,19 +79,6 @@ Layout make_layout(uint64_t n) {
   L.dirty = take(L.cap_sm);
   L.list_sm = take(L.cap_sm * 8);
   L.list_g = take(L.cap_g * 8);
-  const uint64_t ms = msd_max_segs(n), mt = msd_max_tiles(n), nw = msd_windows(n);
-  L.keysC = take(n * 8);
-  L.vals3 = take(n * 4);
-  for (int i = 0; i < 2; ++i) {
-    L.segs[i] = take(ms * sizeof(MsdSeg));
-    L.tile_seg[i] = take(mt * 4);
-  }
-  L.hist = take(ms * 256 * 4);
-  L.seg_or = take(ms * 8);
-  L.seg_nand = take(ms * 8);
-  L.cont = take(ms * 8 * 4);
-  L.win_lo = take(nw * 4);
-  L.win_hi = take(nw * 4);
   L.total = off;
   return L;
 }
@@ -196,54 +176,31 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // the gather rebuilds short strings from ASCII / UNICODE codes only
   const bool packed = n <= kPackMaxN && (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE);
   uint32_t *packed_payload = packed ? S.at<uint32_t>(L.vals2) : nullptr;
+  // slab records (ASCII / UNICODE) when sorted strings are produced: every
+  // string's when n > 2^28 (no packed lengths), else only the long strings'
+  uint4 *slab = (d_sorted_units && (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE))
+                    ? S.at<uint4>(L.slab) : nullptr;
   uint64_t *keysA = S.keysA(), *keysB = S.keysB();
   uint32_t *vals_tmp = S.at<uint32_t>(L.vals);
-  const bool use_msd = keysort_msd();
-  if (use_msd) {
-    // ---- A2 key sort, MSD hybrid (msd.cu): codes in keysB -> sorted keys in
-    // keysA (DevState::sorted_keys), payload in d_perm.  One host
-    // synchronisation per partition level after the first.
-    launch_encode(coder, false, d_units, d_offsets, n, keysB, st, S.sms, s, packed_payload);
-    MsdBufs B;
-    B.k[0] = keysB;
-    B.k[1] = S.at<uint64_t>(L.keysC);
-    B.v[0] = vals_tmp;
-    B.v[1] = S.at<uint32_t>(L.vals3);
-    B.kh = keysA;
-    B.vh = d_perm;
-    B.v_init = packed_payload;
-    for (int i = 0; i < 2; ++i) {
-      B.segs[i] = S.at<MsdSeg>(L.segs[i]);
-      B.tile_seg[i] = S.at<uint32_t>(L.tile_seg[i]);
-    }
-    B.hist = S.at<uint32_t>(L.hist);
-    B.seg_or = S.at<unsigned long long>(L.seg_or);
-    B.seg_nand = S.at<unsigned long long>(L.seg_nand);
-    B.cont = S.at<uint32_t>(L.cont);
-    B.win_lo = S.at<uint32_t>(L.win_lo);
-    B.win_hi = S.at<uint32_t>(L.win_hi);
-    B.lb = S.lb_radix();
-    if (husky_status e = msd_key_sort(S, B)) return e;
-  } else {
-    {
-      GroupScope grp(ST_ENCODE, s);
-      launch_encode(coder, false, d_units, d_offsets, n, S.keysA(), st, S.sms, s, packed_payload);
-    }
-    launch_hist_plan(keysA, n, st, keysA, keysB, S.sms, s);
-
-    // ---- A2 key sort, LSD onesweep: (code, index) -> sorted codes, perm.  The
-    // pass plan (which digits are not shared by all keys) is made on device, so
-    // the host enqueues all 8 pass slots without waiting; slots beyond the plan
-    // exit at once.  Input violations (bad offsets, ASCII domain) make every
-    // later kernel a no-op and are reported at the single synchronisation below.
-    {
-      GroupScope grp(ST_RADIX, s);  // profiler mode 2: the 8 pass slots as one timed group
-      for (int slot = 0; slot < 8; ++slot)
-        launch_onesweep_slot(slot, keysA, keysB, packed_payload, d_perm, vals_tmp, n, st, S.lb_radix(),
-                             S.next_counter(), S.next_epoch(), s);
-    }
-    launch_radix_finalize(st, packed_payload, d_perm, n, s);
+  {
+    GroupScope grp(ST_ENCODE, s);
+    launch_encode(coder, d_units, d_offsets, n, S.keysA(), &st->violations, S.sms, s, packed_payload, slab,
+                  !packed);
   }
+  launch_hist_plan(keysA, n, st, keysA, keysB, S.sms, s);
+
+  // ---- A2 key sort, LSD onesweep: (code, index) -> sorted codes, perm.  The
+  // pass plan (which digits are not shared by all keys) is made on device, so
+  // the host enqueues all 8 pass slots without waiting; slots beyond the plan
+  // exit at once.  Input violations (bad offsets, ASCII domain) make every
+  // later kernel a no-op and are reported at the single synchronisation below.
+  {
+    GroupScope grp(ST_RADIX, s);  // profiler mode 2: the 8 pass slots as one timed group
+    for (int slot = 0; slot < 8; ++slot)
+      launch_onesweep_slot(slot, keysA, keysB, packed_payload, d_perm, vals_tmp, n, st, S.lb_radix(),
+                           S.next_counter(), S.next_epoch(), s);
+  }
+  launch_radix_finalize(st, packed_payload, d_perm, n, s);
   if (packed && !d_sorted_units) launch_unpack_perm(d_perm, n, s);  // the gather unpacks otherwise
 
   // ---- A4 gather in (code, index) order.  Done BEFORE the fix-up: the order
@@ -256,9 +213,10 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   uint32_t *run_start = S.at<uint32_t>(L.run_start), *run_end = S.at<uint32_t>(L.run_end);
   uint8_t *dirty = S.at<uint8_t>(L.dirty);  // zeroed with the DevState at the start
   if (d_sorted_units) {
+    GroupScope grp(ST_GATHER, s);
     GatherRunsOut ro{run_start, run_end, dirty, S.lb_scan2(), st};
     launch_gather(kc, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),
-                  S.next_counter(), S.next_epoch(), s, nullptr, packed, nullptr, st, &ro);
+                  S.next_counter(), S.next_epoch(), s, nullptr, packed, nullptr, st, &ro, slab);
   }
   debug_check_perm(d_perm, n, "key sort", s);
 
@@ -282,8 +240,9 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   HCHECK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, s));
   HCHECK(cudaStreamSynchronize(s));
   if (husky_status e = cuda_check("sort")) return e;
+  HCHECK(S.err);
   if (hs.violations & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing");
-  if (!use_msd) S.radix_passes = hs.np;
+  S.radix_passes = hs.np;
   debug_check_perm(d_perm, n, "fix-up", s);
 
   // ---- Off-domain input (a unit the coder masks inside a code window: the
@@ -309,8 +268,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
     h_out->n_runs = hs.runs_total;
     h_out->refine_rounds = S.refine_rounds;
     h_out->radix_passes = S.radix_passes;
-    h_out->keys_partitioned = use_msd ? hs.msd_keys_part : (uint64_t)hs.np * n;
-    h_out->keys_local = hs.msd_keys_local;
+    h_out->keys_partitioned = (uint64_t)hs.np * n;
     h_out->exchange = HUSKY_EXCHANGE_NONE;
   }
   return HUSKY_OK;
@@ -431,14 +389,32 @@ static husky_status refine_giants(Sorter &S, const DevState &hs0, void *d_sorted
 using namespace husky;
 
 namespace husky {
-__device__ DevState g_encode_state;
+// husky_encode's violation words: one per concurrent call that reads them
+// back (slots 0..62, claimed per device under a bit mask), slot 63 is the
+// shared sink of calls that do not (written, never read)
+constexpr int kEncodeSlots = 64;
+__device__ uint32_t g_encode_viol[kEncodeSlots];
+static std::atomic<unsigned long long> g_encode_busy[64];
+
+static int claim_encode_slot(int dev) {
+  std::atomic<unsigned long long> &m = g_encode_busy[dev & 63];
+  for (;;) {
+    unsigned long long cur = m.load(std::memory_order_acquire);
+    for (int i = 0; i < kEncodeSlots - 1; ++i)
+      if (!(cur & (1ull << i)) && m.compare_exchange_weak(cur, cur | (1ull << i), std::memory_order_acq_rel))
+        return i;
+    std::this_thread::yield();
+  }
+}
+static void release_encode_slot(int dev, int slot) {
+  g_encode_busy[dev & 63].fetch_and(~(1ull << slot), std::memory_order_acq_rel);
+}
 }
 
 extern "C" {
 
 static const char *kStageNames[ST_COUNT] = {"encode", "hist_scan", "radix_pass", "runs_scan", "runs_classify",
-                                            "fix_small", "fix_medium", "refine", "gather", "multi",
-                                            "msd_hist", "local_sort"};
+                                            "fix_small", "fix_medium", "refine", "gather", "multi"};
 
 void husky_profile_enable(int on) {
   Profiler &P = profiler();
@@ -452,6 +428,20 @@ void husky_profile_reset(void) {
   P.flush();
   std::lock_guard<std::mutex> g(P.mu);
   for (int i = 0; i < ST_COUNT; ++i) { P.ms[i] = 0; P.launches[i] = 0; P.elems[i] = 0; }
+  P.log.clear();
+}
+
+int husky_profile_launches(int *stages, uint64_t *elems, double *ms, int max_records) {
+  Profiler &P = profiler();
+  P.flush();
+  std::lock_guard<std::mutex> g(P.mu);
+  const int k = (int)std::min<size_t>(P.log.size(), (size_t)(max_records > 0 ? max_records : 0));
+  for (int i = 0; i < k; ++i) {
+    if (stages) stages[i] = P.log[i].stage;
+    if (elems) elems[i] = P.log[i].elems;
+    if (ms) ms[i] = P.log[i].ms;
+  }
+  return (int)P.log.size();
 }
 
 int husky_profile_read(double *ms, uint64_t *launches, uint64_t *elems, int max_stages) {
@@ -492,22 +482,30 @@ husky_status husky_encode(int coder, const void *d_units, const int64_t *d_offse
     return HUSKY_OK;
   }
   if (!d_units || !d_offsets || !d_codes) return fail(HUSKY_ERR_INVALID_ARG, "null required pointer");
-  // flags live in a module-scope device word: concurrent husky_encode calls
-  // that request h_perfect on the same device must not overlap (documented).
-  DevState *st = nullptr;
-  HCHECK(cudaGetSymbolAddress((void **)&st, g_encode_state));
-  uint32_t *viol = &st->violations;
-  HCHECK(cudaMemsetAsync(viol, 0, 4, s));
-  launch_encode(coder, false, d_units, d_offsets, n, d_codes, st, device_sm_count(), s);
-  if (husky_status e = cuda_check("encode")) return e;
+  // violation word: a private slot while this call reads it back (concurrent
+  // calls on one device do not share it), the shared sink otherwise
+  uint32_t *words = nullptr;
+  HCHECK(cudaGetSymbolAddress((void **)&words, g_encode_viol));
+  int dev = 0;
+  HCHECK(cudaGetDevice(&dev));
+  const int slot = h_perfect ? claim_encode_slot(dev) : kEncodeSlots - 1;
+  uint32_t *viol = words + slot;
+  husky_status rc = HUSKY_OK;
+  uint32_t v = 0;
+  cudaError_t e = h_perfect ? cudaMemsetAsync(viol, 0, 4, s) : cudaSuccess;
+  if (e == cudaSuccess) {
+    launch_encode(coder, d_units, d_offsets, n, d_codes, viol, device_sm_count(), s);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess && h_perfect) e = cudaMemcpyAsync(&v, viol, 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && h_perfect) e = cudaStreamSynchronize(s);
+  if (h_perfect) release_encode_slot(dev, slot);
+  if (e != cudaSuccess) return fail(HUSKY_ERR_CUDA, "encode: %s", cudaGetErrorString(e));
   if (h_perfect) {
-    uint32_t v = 0;
-    HCHECK(cudaMemcpyAsync(&v, viol, 4, cudaMemcpyDeviceToHost, s));
-    HCHECK(cudaStreamSynchronize(s));
     if (v & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing");
     *h_perfect = !(v & kNotPerfect);
   }
-  return HUSKY_OK;
+  return rc;
 }
 
 husky_status husky_sort_workspace(int coder, uint64_t n, uint64_t total_units, size_t *bytes) {
@@ -594,7 +592,7 @@ static husky_status host_many_pipelined(int coder, int k, const void *const *h_u
                                         const int64_t *const *h_offsets, const uint64_t *n,
                                         uint32_t *const *h_perm, void *const *h_sorted_units,
                                         int64_t *const *h_sorted_offsets, int depth, uint8_t *ws, size_t slice,
-                                        husky_outcome *h_out) {
+                                        uint64_t n_max, uint64_t u_max, husky_outcome *h_out) {
   const size_t w = husky_unit_bytes(coder);
   cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
   std::vector<cudaEvent_t> evH(depth, nullptr), evC(depth, nullptr), evD(depth, nullptr);
@@ -631,11 +629,14 @@ static husky_status host_many_pipelined(int coder, int k, const void *const *h_u
   }
   auto total_of = [&](int b) { return n[b] ? (uint64_t)(h_offsets[b][n[b]] - h_offsets[b][0]) : 0ull; };
   std::vector<bool> used(depth, false);
+  // ONE layout for every batch, sized by the largest: a slot's input regions
+  // never overlap the outputs of the slot's previous batch, which may still be
+  // in flight to the host on sd while the next batch's inputs arrive on sh
+  size_t o_units, o_off, o_perm, o_su, o_so, o_ws;
+  host_layout(coder, n_max, u_max, &o_units, &o_off, &o_perm, &o_su, &o_so, &o_ws);
   auto issue_in = [&](int b) -> cudaError_t {
     const int sl = b % depth;
     uint8_t *base = ws + slice * sl;
-    size_t o_units, o_off, o_perm, o_su, o_so, o_ws;
-    host_layout(coder, n[b], total_of(b), &o_units, &o_off, &o_perm, &o_su, &o_so, &o_ws);
     cudaError_t e = cudaSuccess;
     if (used[sl]) e = cudaStreamWaitEvent(sh, evC[sl], 0);  // the previous sort of this slot has read its inputs
     const int64_t b0 = n[b] ? h_offsets[b][0] : 0;
@@ -656,8 +657,6 @@ static husky_status host_many_pipelined(int coder, int k, const void *const *h_u
       cleanup();
       return st;
     }
-    size_t o_units, o_off, o_perm, o_su, o_so, o_ws;
-    host_layout(coder, n[b], total_of(b), &o_units, &o_off, &o_perm, &o_su, &o_so, &o_ws);
     HM_CHECK(cudaStreamWaitEvent(sc, evH[sl], 0));
     if (used[sl]) HM_CHECK(cudaStreamWaitEvent(sc, evD[sl], 0));  // outputs of this slot copied out
     const int64_t b0 = n[b] ? h_offsets[b][0] : 0;
@@ -717,41 +716,8 @@ husky_status husky_sort_host_many(int coder, int k, const void *const *h_units, 
   size_t a, bb, c, d, e, f;
   const size_t slice = align_up(host_layout(coder, n_max, u_max, &a, &bb, &c, &d, &e, &f), 256);
   if (ws_bytes < slice * depth) return fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, slice * depth);
-  const char *mode = getenv("HUSKY_HOST_MANY");
-  if (!(mode && mode[0] == 't'))
-    return host_many_pipelined(coder, k, h_units, h_offsets, n, h_perm, h_sorted_units, h_sorted_offsets, depth,
-                               (uint8_t *)d_ws, slice, h_out);
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::vector<husky_status> st(depth, HUSKY_OK);
-  std::vector<std::string> err(depth);
-  std::vector<std::thread> workers;
-  for (int w = 0; w < depth && w < k; ++w) {
-    workers.emplace_back([&, w]() {
-      cudaSetDevice(dev);
-      cudaStream_t s;
-      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
-        st[w] = fail(HUSKY_ERR_CUDA, "stream creation failed");
-        err[w] = g_last_error;
-        return;
-      }
-      for (int b = w; b < k && st[w] == HUSKY_OK; b += depth) {
-        st[w] = husky_sort_host(coder, h_units[b], h_offsets[b], n[b], h_perm[b],
-                                h_sorted_units ? h_sorted_units[b] : nullptr,
-                                h_sorted_offsets ? h_sorted_offsets[b] : nullptr, (uint8_t *)d_ws + slice * w, slice,
-                                h_out ? h_out + b : nullptr, s);
-        if (st[w] != HUSKY_OK) err[w] = g_last_error;
-      }
-      cudaStreamDestroy(s);
-    });
-  }
-  for (auto &t : workers) t.join();
-  for (int w = 0; w < depth; ++w)
-    if (st[w] != HUSKY_OK) {
-      g_last_error = err[w];
-      return st[w];
-    }
-  return HUSKY_OK;
+  return host_many_pipelined(coder, k, h_units, h_offsets, n, h_perm, h_sorted_units, h_sorted_offsets, depth,
+                             (uint8_t *)d_ws, slice, n_max, u_max, h_out);
 }
 
 }  // extern "C"

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/husky.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -23,12 +25,14 @@ template <> struct CoderTraits<HUSKY_CODER_ASCII> {
   static constexpr int kUnitBytes = 1, kS = 9, kPL = 9;
   static constexpr int kWin = 7;    // refinement window: 7 units x 8 bits
   static constexpr int kTagCap = 8; // tag value meaning "continues past the window"
+  static constexpr int kSlabMax = 24; // slab record: units [9, 24) after the code's 9
 };
 template <> struct CoderTraits<HUSKY_CODER_UNICODE> {
   using unit_t = uint16_t;
   static constexpr int kUnitBytes = 2, kS = 3, kPL = 3;
   static constexpr int kWin = 3;    // 3 units x 16 bits
   static constexpr int kTagCap = 4;
+  static constexpr int kSlabMax = 10; // slab record: units [3, 10) after the code's 3
 };
 
 // ENGLISH5 / ENGLISH6 (reading R15): byte units; only the
@@ -56,26 +60,14 @@ constexpr uint32_t kNotPerfect = 1u, kDomainBad = 2u, kOffsetsBad = 4u;
 constexpr uint32_t kNotLower = 8u, kNotUpper = 16u;
 
 // ------------------------------------------------------ device-resident state
-// Digit width of the device-planned passes (the main key sort).  9-bit digits
-// cover the 63 bits every husky code uses (9 x 7, 4 x 16 >>> 1,
-// 12 x 5, 10 x 6) in 7 passes instead of 8 (digit 7 is then bit 63 alone), but
-// each 512-bin pass measured ~14% slower, so the sort time came out equal on
-// C2-C4; 8 stays the default.  Host-planned passes (A6 re-key,
-// multi-GPU partition) always use 8-bit digits.  hist / digit_start rows hold
-// kMaxBins entries either way.
-#ifndef HUSKY_SLOT_BITS
-#define HUSKY_SLOT_BITS 8
-#endif
-constexpr int kSlotBits = HUSKY_SLOT_BITS;
-constexpr int kMaxBins = 512;
-static_assert(kSlotBits == 8 || kSlotBits == 9, "slot digits are 8 or 9 bits");
+// LSD digits: 8 bits (9-bit digits -- 7 passes for the 63-bit codes -- measured
+// ~14% slower per pass, so no faster in total: DESIGN.md 6.1).
+constexpr int kDigitBits = 8;
+constexpr int kBins = 1 << kDigitBits;
 // Lives at the start of the caller's workspace; zeroed once per husky_sort.
 struct DevState {
-  // digit histograms of the 64-bit keys: rows of kMaxBins; the device-planned
-  // passes use 9-bit digits (512 bins), the host-planned ones (A6 re-key,
-  // multi-GPU partition) 8-bit digits in the first 256 bins of each row
-  uint32_t hist[8][kMaxBins];
-  uint32_t digit_start[8][kMaxBins];
+  uint32_t hist[8][kBins];        // digit histograms of the 64-bit keys
+  uint32_t digit_start[8][kBins]; // their exclusive scans
   uint32_t trivial_mask;      // bit d: all keys share digit d
   uint32_t violations;        // kNotPerfect | kDomainBad | kOffsetsBad
   uint32_t tile_counter[64];  // dynamic tile ids, one per launch slot
@@ -91,21 +83,29 @@ struct DevState {
   uint32_t np;
   uint32_t hist_done;       // k_hist_slots<true>: CTAs that have added their histograms
   uint32_t pass_digit[8];
-  uint32_t pass_ballot[8];  // rank a pass with per-bit ballots instead of __match_any_sync
-  uint32_t digit_spread[8]; // k_hist_scan: digit d's largest bin holds < 5% of the keys
   unsigned long long sorted_keys;  // uint64_t* of the sorted keys
-  // MSD key sort (msd.cu): OR and NOT-AND of all codes (fused into A1; zero-
-  // initialised), segment-list fill counts and tile counts of the two level
-  // lists, keys moved by partition passes / sorted by the local sort
-  unsigned long long key_or, key_nand;
-  uint32_t msd_count[2], msd_tiles[2];
-  uint32_t msd_all_equal, msd_pad;
-  unsigned long long msd_keys_part, msd_keys_local;
   // general cleanup (NEXT-4): the coder is not monotone on this input, so the
   // refinement / fix-up kernels compare whole strings from unit 0 instead of
   // relying on equal codes (no short rule, no known-equal prefix)
   uint32_t general;
-  uint32_t pad[16];
+  uint32_t pad[15];
+};
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per device and kernel:
+// the attribute belongs to the kernel's function handle in each device's
+// context, so a process that sorts on several GPUs sets it on each of them.
+struct SmemAttr {
+  std::atomic<unsigned long long> done{0};
+  template <typename F>
+  cudaError_t ensure(F *func, int bytes) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+  }
 };
 
 // ----------------------------------------------------------- small helpers
@@ -307,6 +307,12 @@ __device__ __forceinline__ uint64_t load8_unaligned(const uint8_t *p, int need) 
   uint64_t v = lo >> (8 * sh);
   if (sh + need > 8) v |= __ldg(w + 1) << (64 - 8 * sh);
   return v;
+}
+
+// Byte k (1..15) of a slab record held in registers.
+__device__ __forceinline__ uint8_t slab_byte(const uint4 &v, int k) {
+  const uint32_t w = (k >> 2) == 0 ? v.x : ((k >> 2) == 1 ? v.y : ((k >> 2) == 2 ? v.z : v.w));
+  return (uint8_t)(w >> (8 * (k & 3)));
 }
 
 // Compare two unit strings a[0..la), b[0..lb) lexicographically (unsigned units),

@@ -16,11 +16,15 @@ int device_sm_count();  // husky.cu
 constexpr int kEncThreads = 256, kEncBlocksPerSM = HUSKY_ENC_BPS;  // grid (resident: HUSKY_ENC_MINB)
 // packed (nullable, n <= 2^28): also writes the initial radix payload
 // index | min(len, 15) << 28, so the gather knows short strings' lengths
-// without a random offsets read.
+// without a random offsets read.  slab (nullable, ASCII / UNICODE): the
+// 16-byte string records the main gather reads (encode.cu); slab_all: a record
+// for every string, else only for strings longer than PL.  viol: violation
+// bits (OR-ed).
 constexpr uint64_t kPackMaxN = 1ull << 28;
-void launch_encode(int coder, bool hist, const void *units, const int64_t *offsets, uint64_t n,
-                   uint64_t *codes, DevState *st, int num_sms, cudaStream_t s, uint32_t *packed = nullptr);
-// 8 digit histograms (kSlotBits-bit digits) of n keys into DevState::hist (accumulates)
+void launch_encode(int coder, const void *units, const int64_t *offsets, uint64_t n, uint64_t *codes,
+                   uint32_t *viol, int num_sms, cudaStream_t s, uint32_t *packed = nullptr, uint4 *slab = nullptr,
+                   bool slab_all = false);
+// 8 digit histograms (8-bit digits) of n keys into DevState::hist (accumulates)
 void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s);
 // histograms + k_hist_scan + the pass plan fused (the last CTA scans and plans)
 void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *keysA, uint64_t *keysB,
@@ -38,10 +42,6 @@ void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *
 #define HUSKY_RADIX_ITEMS 12
 #endif
 constexpr int kRadixThreads = 512, kRadixItems = HUSKY_RADIX_ITEMS, kRadixTile = kRadixThreads * kRadixItems;
-#ifndef HUSKY_RADIX_MINB
-#define HUSKY_RADIX_MINB 2
-#endif
-constexpr int kRadixMinBlocks = HUSKY_RADIX_MINB;
 // Small inputs (n below kRadixSmallN) use 2048-key tiles (4 keys per thread):
 // a 1e5-string sort has 17 large tiles for 148 SMs.  Measured per C2-like sort
 // (small / large tiles): 1e5 140 / 165 us, 3e5 158 / 174, 1e6 248 / 235,
@@ -57,12 +57,10 @@ inline uint64_t radix_tiles(uint64_t n) {
   return (n + t - 1) / t;
 }
 inline uint64_t radix_tiles_large(uint64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
-// look-back words: one per (tile, digit), tile-major, up to kMaxBins per tile
-inline uint64_t radix_lb_stride(uint64_t n) { return (radix_tiles(n) + 1) & ~1ull; }
-inline uint64_t radix_lb_words(uint64_t n) { return radix_lb_stride(n) * kMaxBins + 2; }
-// exclusive scans of DevState::hist -> digit_start, trivial_mask, digit_spread
-// for the 8-bit digits of the host-planned passes (the pass slots get theirs
-// from launch_hist_plan)
+// look-back words: one per (tile, digit), tile-major
+inline uint64_t radix_lb_words(uint64_t n) { return radix_tiles(n) * kBins + 2; }
+// exclusive scans of DevState::hist -> digit_start, trivial_mask for the
+// host-planned passes (the pass slots get theirs from launch_hist_plan)
 void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s);
 // One stable LSD pass on digit `digit` (bits 8*digit..8*digit+7).  vals_in == NULL
 // synthesises payload = index.  lb: radix_tiles(n)*256 look-back words.
@@ -70,7 +68,7 @@ void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t 
                      uint32_t *vals_out, uint64_t n, int digit, DevState *st,
                      unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
 void launch_iota(uint32_t *perm, uint64_t n, cudaStream_t s);
-// Device-planned passes (kSlotBits-bit digits, no host sync): the last CTA of
+// Device-planned passes (no host sync): the last CTA of
 // launch_hist_plan turns the trivial-digit mask into DevState::np / pass_digit /
 // sorted_keys; slots 0..7 are launched unconditionally and resolve their digit
 // and ping-pong buffers on device (the last planned pass writes vals_final);
@@ -81,40 +79,7 @@ void launch_onesweep_slot(int slot, uint64_t *keysA, uint64_t *keysB, const uint
 void launch_radix_finalize(const DevState *st, const uint32_t *vals_init, uint32_t *vals_final, uint64_t n,
                            cudaStream_t s);
 
-// A2 key sort, MSD variant (msd.cu; opt-in, HUSKY_KEYSORT=msd).  Levels of segmented
-// partition passes on the top varying byte of each segment (onesweep tiles with
-// per-segment look-back), until every bucket has <= kMsdSmall keys; buckets are
-// then sorted in shared memory, several per CTA, by windows of kMsdWin positions.
-constexpr uint32_t kMsdSmall = 2048, kMsdWin = 2048, kMsdLocalCap = kMsdSmall + kMsdWin;
-constexpr uint32_t kSegPart = 1u;  // MsdSeg::flags: partitioned at this level
-struct MsdSeg {
-  uint32_t start, len;  // positions [start, start + len)
-  uint32_t digit;       // byte the segment is partitioned on (its top varying byte)
-  uint32_t tile0;       // first tile of the segment in the level's launch
-  uint32_t buf;         // scratch buffer (0/1) holding the segment's keys and payload
-  uint32_t flags;
-};
-inline uint64_t msd_max_segs(uint64_t n) { return n / (kMsdSmall + 1) + 2; }
-inline uint64_t msd_max_tiles(uint64_t n) { return radix_tiles_large(n) + msd_max_segs(n) + 1; }
-inline uint64_t msd_windows(uint64_t n) { return (n + kMsdWin - 1) / kMsdWin; }
-struct MsdBufs {
-  uint64_t *k[2];            // scratch keys (k[0] holds the codes written by A1)
-  uint32_t *v[2];            // scratch payload
-  uint64_t *kh;              // home: final sorted keys
-  uint32_t *vh;              // home: final payload (the caller's perm)
-  const uint32_t *v_init;    // level-0 payload (NULL: the index)
-  MsdSeg *segs[2];           // segment lists of alternate levels
-  uint32_t *tile_seg[2];     // tile -> segment of each list
-  uint32_t *hist;            // [max_segs][256]: counts, then absolute bucket starts
-  unsigned long long *seg_or, *seg_nand;  // [max_segs]
-  uint32_t *cont;            // [max_segs][8]: bucket continues to the next level
-  uint32_t *win_lo, *win_hi; // [windows]: span of the local-sort buckets starting in a window
-  unsigned long long *lb;    // look-back words [msd_max_tiles][256]
-};
 struct Sorter;
-// Runs the whole MSD key sort: codes in B.k[0] -> sorted keys (DevState::sorted_keys)
-// + payload in B.vh.  One host synchronisation per level after the first.
-husky_status msd_key_sort(Sorter &S, const MsdBufs &B);
 
 // A3 run detection (single-pass scan with decoupled look-back)
 constexpr int kScanThreads = 512, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
@@ -161,7 +126,7 @@ void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, con
                    void *sorted_units, int64_t *sorted_offsets, unsigned long long *lb,
                    uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, const int64_t *base_ptr = nullptr,
                    bool packed = false, const uint64_t *packed_codes = nullptr, const DevState *st = nullptr,
-                   const struct GatherRunsOut *runs_out = nullptr);
+                   const struct GatherRunsOut *runs_out = nullptr, const uint4 *slab = nullptr);
 // A3 fused into the main gather (runs_out != NULL): run starts / ends / dirty
 // flags as k_runs_scan writes them, DevState::n_runs; lb: gather_tiles(n) words
 struct GatherRunsOut {

@@ -37,6 +37,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -317,7 +318,47 @@ struct Comm {
   bool win_failed = false;                // registration failed on some rank: NCCL send/recv
   std::vector<unsigned long long> peer;   // peer base address of the window, per rank
   unsigned long long *d_tmp = nullptr;    // world words (peer addresses, barrier word)
+  bool aborted = false;                   // ncclCommAbort ran: every later call fails fast
 };
+
+// Waits for `s` while watching the communicator: an asynchronous NCCL error
+// (a peer died, a network fault) or no progress within HUSKY_NCCL_TIMEOUT_S
+// seconds (default 600) aborts the communicator and returns HUSKY_ERR_NCCL
+// instead of hanging every rank (failure detection).
+// c == NULL (loopback driver): a plain synchronisation.
+static double nccl_timeout_s() {
+  static const double t = [] {
+    const char *v = getenv("HUSKY_NCCL_TIMEOUT_S");
+    return v ? atof(v) : 600.0;
+  }();
+  return t;
+}
+
+static husky_status comm_sync(Comm *c, cudaStream_t s) {
+  if (!c) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(HUSKY_ERR_CUDA, "cudaStreamSynchronize: %s", cudaGetErrorString(e));
+    return HUSKY_OK;
+  }
+  if (c->aborted) return fail(HUSKY_ERR_NCCL, "communicator was aborted by an earlier failure");
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint64_t it = 0;; ++it) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e == cudaSuccess) return HUSKY_OK;
+    if (e != cudaErrorNotReady) return fail(HUSKY_ERR_CUDA, "stream: %s", cudaGetErrorString(e));
+    ncclResult_t ae = ncclSuccess;
+    ncclCommGetAsyncError(c->nccl, &ae);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((ae != ncclSuccess && ae != ncclInProgress) || el > nccl_timeout_s()) {
+      ncclCommAbort(c->nccl);
+      c->aborted = true;
+      if (ae != ncclSuccess && ae != ncclInProgress)
+        return fail(HUSKY_ERR_NCCL, "NCCL asynchronous error: %s (communicator aborted)", ncclGetErrorString(ae));
+      return fail(HUSKY_ERR_NCCL, "no progress for %.0f s (HUSKY_NCCL_TIMEOUT_S): communicator aborted", el);
+    }
+    if (it > 2000) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
 
 // Where a rank receives: units at 0, lengths and global indices after them.
 // Window offsets are the same on every rank (sized by the largest shard).
@@ -447,7 +488,7 @@ struct Plan {
     init_sorter();
     HCHECK(cudaMemsetAsync(st(), 0, sizeof(DevState), s));
     HCHECK(S.reset_lookback());
-    launch_encode(coder, false, units, offsets, n, at<uint64_t>(M.L.keysA), st(), S.sms, s);
+    launch_encode(coder, units, offsets, n, at<uint64_t>(M.L.keysA), &st()->violations, S.sms, s);
     HUSKY_SCOPE(ST_MULTI, s, 0);
     k_sample<<<1, 256, 0, s>>>(at<uint64_t>(M.L.keysA), n, at<uint64_t>(M.samples) + (size_t)rank * kSampleStride,
                                st());
@@ -462,7 +503,7 @@ struct Plan {
   husky_status choose_splitters() {
     std::vector<uint64_t> all((size_t)world * kSampleStride);
     HCHECK(cudaMemcpyAsync(all.data(), at<uint64_t>(M.samples), all.size() * 8, cudaMemcpyDeviceToHost, s));
-    HCHECK(cudaStreamSynchronize(s));
+    if (husky_status e = comm_sync(comm, s)) return e;
     uint32_t viol = 0;
     std::vector<int> ranks;  // ranks with strings (a rank's samples are all valid or all absent)
     for (int r = 0; r < world; ++r) {
@@ -537,7 +578,7 @@ struct Plan {
     std::vector<uint64_t> c((size_t)world * 2), mat((size_t)world * world * 2);
     HCHECK(cudaMemcpyAsync(c.data(), at<uint64_t>(M.counts), c.size() * 8, cudaMemcpyDeviceToHost, s));
     HCHECK(cudaMemcpyAsync(mat.data(), at<uint64_t>(M.rcounts), mat.size() * 8, cudaMemcpyDeviceToHost, s));
-    HCHECK(cudaStreamSynchronize(s));
+    if (husky_status e = comm_sync(comm, s)) return e;
     send_cnt.assign(world, 0); send_u.assign(world, 0); recv_cnt.assign(world, 0); recv_u.assign(world, 0);
     disp_n.assign(world, 0); disp_u.assign(world, 0);
     n_out = units_out = cap_n = cap_u = 0;
@@ -675,7 +716,7 @@ static husky_status all_ranks_ok(Comm *c, cudaStream_t s, bool mine, bool *all) 
   HCHECK(cudaMemcpyAsync(c->d_tmp + c->world, &v, 8, cudaMemcpyHostToDevice, s));
   NCHECK(ncclAllReduce(c->d_tmp + c->world, c->d_tmp + c->world, 1, ncclUint64, ncclMin, c->nccl, s));
   HCHECK(cudaMemcpyAsync(&v, c->d_tmp + c->world, 8, cudaMemcpyDeviceToHost, s));
-  HCHECK(cudaStreamSynchronize(s));
+  if (husky_status e = comm_sync(c, s)) return e;
   *all = v != 0;
   return HUSKY_OK;
 }
@@ -816,9 +857,20 @@ husky_status husky_comm_create(int rank, int world, const uint8_t id[128], void 
   return HUSKY_OK;
 }
 
+husky_status husky_comm_world(void *comm, int *world) {
+  if (!comm || !world) return fail(HUSKY_ERR_INVALID_ARG, "null pointer");
+  *world = ((Comm *)comm)->world;
+  return HUSKY_OK;
+}
+
 husky_status husky_comm_destroy(void *comm) {
   if (!comm) return HUSKY_OK;
   Comm *c = (Comm *)comm;
+  if (c->aborted) {  // ncclCommAbort already released the NCCL resources
+    if (c->d_tmp) cudaFree(c->d_tmp);
+    delete c;
+    return HUSKY_OK;
+  }
   release_window(c);
   if (c->d_tmp) cudaFree(c->d_tmp);
   ncclResult_t r = ncclCommDestroy(c->nccl);
@@ -843,6 +895,7 @@ husky_status husky_sort_multi_plan(void *comm, int coder, const void *d_units, c
   if (global_base + n_local >= 0xFFFFFFFFull) return fail(HUSKY_ERR_INVALID_ARG, "global index >= 2^32 - 1");
   if ((uintptr_t)d_ws % 256) return fail(HUSKY_ERR_INVALID_ARG, "workspace not 256-byte aligned");
   Comm *c = (Comm *)comm;
+  if (c->aborted) return fail(HUSKY_ERR_NCCL, "communicator was aborted by an earlier failure");
   cudaStream_t s = (cudaStream_t)stream;
   int64_t o[2] = {0, 0};
   if (n_local) {
@@ -944,9 +997,19 @@ husky_status husky_sort_multi_exec(void *plan, uint32_t *d_perm_out, void *d_sor
   if (husky_status e = P->phase4(r_units, r_lens, r_gidx, rws, R, d_perm_out, d_sorted_units_out,
                                  d_sorted_offsets_out, h_out))
     return e;
-  if (h_out) h_out->exchange = P->peer ? HUSKY_EXCHANGE_PEER : HUSKY_EXCHANGE_NCCL;
+  if (h_out) {
+    h_out->exchange = P->peer ? HUSKY_EXCHANGE_PEER : HUSKY_EXCHANGE_NCCL;
+    uint64_t to = 0, from = 0;
+    for (int q = 0; q < P->world; ++q) {
+      if (q == P->rank) continue;
+      to += P->send_u[q] * P->w() + 8 * P->send_cnt[q];
+      from += P->recv_u[q] * P->w() + 8 * P->recv_cnt[q];
+    }
+    h_out->bytes_to_peers = to;
+    h_out->bytes_from_peers = from;
+  }
   pc.mark("local sort");
-  HCHECK(cudaStreamSynchronize(P->s));
+  if (husky_status e = comm_sync(c, P->s)) return e;
   return HUSKY_OK;
 }
 
@@ -982,15 +1045,25 @@ husky_status husky_sort_multi(void *comm, int coder, const void *d_units, const 
   if (h_units_out) *h_units_out = u_out;
   size_t rb = 0;
   husky_sort_multi_recv_workspace(plan, &rb);
-  husky_status e = HUSKY_OK;
-  if (n_out > cap_n || u_out > cap_units) e = fail(HUSKY_ERR_CAPACITY, "shard needs %llu strings / %llu units",
-                                                   (unsigned long long)n_out, (unsigned long long)u_out);
-  // NOTE: every rank must reach the exchange; a capacity failure on one rank
-  // would leave its peers blocked, so callers size outputs from the plan query.
-  else if (ws_bytes < plan_bytes + rb) e = fail(HUSKY_ERR_WORKSPACE, "workspace too small for receive buffers");
-  else e = husky_sort_multi_exec(plan, d_perm_out, d_sorted_units_out, d_sorted_offsets_out,
-                                 (uint8_t *)d_ws + align_up(plan_bytes, 256), ws_bytes - align_up(plan_bytes, 256),
-                                 h_out, stream);
+  // every rank must reach the exchange or none: the capacity / workspace
+  // checks are agreed on across the ranks first (a rank that failed alone
+  // would leave its peers blocked in the exchange)
+  const bool cap_ok = n_out <= cap_n && u_out <= cap_units;
+  const bool ws_ok = ws_bytes >= align_up(plan_bytes, 256) + rb;
+  bool all_cap = true, all_ws = true;
+  husky_status e = all_ranks_ok(c, s, cap_ok, &all_cap);
+  if (!e) e = all_ranks_ok(c, s, ws_ok, &all_ws);
+  if (!e && !all_cap)
+    e = fail(HUSKY_ERR_CAPACITY, cap_ok ? "another rank's shard exceeds its capacity"
+                                        : "shard needs %llu strings / %llu units",
+             (unsigned long long)n_out, (unsigned long long)u_out);
+  else if (!e && !all_ws)
+    e = fail(HUSKY_ERR_WORKSPACE, ws_ok ? "another rank's workspace is too small for its receive buffers"
+                                        : "workspace too small for the receive buffers");
+  else if (!e)
+    e = husky_sort_multi_exec(plan, d_perm_out, d_sorted_units_out, d_sorted_offsets_out,
+                              (uint8_t *)d_ws + align_up(plan_bytes, 256), ws_bytes - align_up(plan_bytes, 256),
+                              h_out, stream);
   husky_plan_destroy(plan);
   return e;
 }
@@ -1152,7 +1225,7 @@ husky_status husky_sort_multi_loopback(int coder, int world, const void *d_units
     agg.max_run = std::max(agg.max_run, o.max_run);
     for (int c = 0; c < 4; ++c) agg.runs_by_class[c] += o.runs_by_class[c];
     agg.refine_rounds += o.refine_rounds; agg.radix_passes += o.radix_passes;
-    agg.keys_partitioned += o.keys_partitioned; agg.keys_local += o.keys_local;
+    agg.keys_partitioned += o.keys_partitioned;
     out_n += dst.n_out; out_u += dst.units_out;
   }
   if (n == 0 && d_sorted_offsets) HCHECK(cudaMemsetAsync(d_sorted_offsets, 0, 8, s));

@@ -18,7 +18,7 @@ namespace husky {
 
 enum Stage : int {
   ST_ENCODE = 0, ST_HIST_SCAN, ST_RADIX, ST_RUNS_SCAN, ST_CLASSIFY, ST_FIX_SMALL, ST_FIX_MEDIUM,
-  ST_REFINE, ST_GATHER, ST_MULTI, ST_MSD_HIST, ST_LOCAL_SORT, ST_COUNT
+  ST_REFINE, ST_GATHER, ST_MULTI, ST_COUNT
 };
 
 struct Profiler {
@@ -31,6 +31,10 @@ struct Profiler {
   uint64_t launches[ST_COUNT] = {};
   uint64_t elems[ST_COUNT] = {};
   uint64_t total_launches = 0;  // always counted
+  // mode 1: every harvested launch in order (stage, elements, ms), bounded
+  struct Rec { int stage; uint64_t elems; double ms; };
+  std::vector<Rec> log;
+  static constexpr size_t kLogMax = 1 << 16;
 
   cudaEvent_t get() {
     if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
@@ -45,6 +49,7 @@ struct Profiler {
       float t = 0.f;
       if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) {
         ms[p.stage] += t;
+        if (on == 1 && log.size() < kLogMax) log.push_back({p.stage, p.elems, (double)t});
       }
       pool.push_back(p.a);
       pool.push_back(p.b);

@@ -122,14 +122,11 @@ void launch_runs_scan(int coder, int mode, const uint64_t *keys, uint64_t n, con
                       uint32_t *tile_counter, uint32_t epoch, cudaStream_t s) {
   if (n == 0) return;
   constexpr int kSmem0 = kScanKP * 8;  // the padded key staging
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_ASCII, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
-    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_ASCII, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
-    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_UNICODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
-    cudaFuncSetAttribute(k_runs_scan<HUSKY_CODER_UNICODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem0);
-    configured = true;
-  }
+  static SmemAttr a0, a1, a2, a3;
+  a0.ensure(k_runs_scan<HUSKY_CODER_ASCII, 0>, kSmem0);
+  a1.ensure(k_runs_scan<HUSKY_CODER_ASCII, 1>, kSmem0);
+  a2.ensure(k_runs_scan<HUSKY_CODER_UNICODE, 0>, kSmem0);
+  a3.ensure(k_runs_scan<HUSKY_CODER_UNICODE, 1>, kSmem0);
   Scope sc_(ST_RUNS_SCAN, s, n);
   dim3 g((unsigned)scan_tiles(n)), b(kScanThreads);
 #define RS_ARGS keys, n, perm, units, offsets, base, run_start, run_end, dirty, st, lb, tile_counter, epoch

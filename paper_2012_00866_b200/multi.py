@@ -30,6 +30,7 @@ _sig("husky_select_splitters", _ST, ctypes.c_int, _P, _P, _U64, ctypes.c_int, _P
 _sig("husky_comm_unique_id", _ST, _P)
 _sig("husky_comm_create", _ST, ctypes.c_int, ctypes.c_int, _P, ctypes.POINTER(_P))
 _sig("husky_comm_destroy", _ST, _P)
+_sig("husky_comm_world", _ST, _P, ctypes.POINTER(ctypes.c_int))
 _sig("husky_sort_multi_workspace", _ST, ctypes.c_int, _U64, _U64, ctypes.c_int, ctypes.POINTER(_SZ))
 _sig("husky_sort_multi_plan", _ST, _P, ctypes.c_int, _P, _P, _U64, _U64, _P, _SZ, ctypes.POINTER(_P),
      ctypes.POINTER(_U64), ctypes.POINTER(_U64), _P)
@@ -144,11 +145,14 @@ def sort_multi(comm, coder, units, offsets, global_base, with_units=True, stream
     return perm[:n_out], (su[:u_out] if with_units else None), so, outc
 
 
-_WORLD = {}
+def husky_comm_world(comm) -> int:
+    w = ctypes.c_int(0)
+    _check(_lib.husky_comm_world(comm, ctypes.byref(w)), "husky_comm_world")
+    return int(w.value)
 
 
 def _world_of(comm):
-    return _WORLD.get(comm.value if hasattr(comm, "value") else comm, 1)
+    return husky_comm_world(comm)
 
 
 def comm_from_process_group(group=None, device=None):
@@ -159,9 +163,7 @@ def comm_from_process_group(group=None, device=None):
     uid = husky_comm_unique_id() if rank == 0 else bytes(128)
     t = torch.tensor(list(uid), dtype=torch.uint8, device=device if device is not None else "cpu")
     dist.broadcast(t, src=0, group=group)
-    comm = husky_comm_create(rank, world, bytes(t.cpu().tolist()))
-    _WORLD[comm.value] = world
-    return comm
+    return husky_comm_create(rank, world, bytes(t.cpu().tolist()))
 
 
 def husky_sort_multi_loopback_workspace(coder, world, n, total_units) -> int:

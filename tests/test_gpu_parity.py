@@ -430,12 +430,10 @@ def test_multi_loopback_peer_edges(torch, h, oracle_mod, monkeypatch, world):
     assert np.array_equal(so.cpu().numpy(), rso) and np.array_equal(su[:tot].cpu().numpy(), rsu)
 
 
-@pytest.mark.parametrize("mode", ["pipe", "threads"])
-def test_sort_host_many_pipelined(torch, h, oracle_mod, monkeypatch, mode):
+def test_sort_host_many_pipelined(torch, h, oracle_mod):
     """The pipelined host API: several batches (different configs and sizes,
     one empty) through 1, 2 and 3 workspace slots, each bit-exact against the
-    oracle -- the three-stream pipeline and the worker-thread scheme."""
-    monkeypatch.setenv("HUSKY_HOST_MANY", mode)
+    oracle (three streams: H2D copies, kernels, D2H copies)."""
     wls = [W.make("C1", 50_000), W.make("C3", 70_000), W.make("C2", 120_000),
            W.from_strings([], ASCII), W.make("C1", 3)]
     for depth in (1, 2, 3):
@@ -458,6 +456,32 @@ def test_sort_host_many_pipelined(torch, h, oracle_mod, monkeypatch, mode):
                 rsu, rso = oracle_mod.gather(w.coder, w.units, w.offsets, ref)
                 assert np.array_equal(b[4], rso)
                 assert np.array_equal(b[3][:rsu.size], rsu)
+
+
+@pytest.mark.parametrize("depth", [1, 2])
+def test_sort_host_many_growing_batches_pinned(torch, h, oracle_mod, depth):
+    """Pinned host buffers and batches that GROW within a slot: a later batch's
+    input copy must not land on an earlier batch's outputs while they are still
+    being copied to the host (the slot layout is sized by the largest batch)."""
+    sizes = [20_000, 60_000, 150_000, 300_000, 40_000, 500_000]
+    wls = [W.make("C1", n) for n in sizes]
+    batches = []
+    for w in wls:
+        tot = int(w.offsets[-1])
+        batches.append((torch.from_numpy(w.units).pin_memory(), torch.from_numpy(w.offsets).pin_memory(),
+                        torch.zeros(w.n, dtype=torch.int32).pin_memory(),
+                        torch.zeros(tot + 8, dtype=torch.uint8).pin_memory(),
+                        torch.zeros(w.n + 1, dtype=torch.int64).pin_memory()))
+    ws = torch.empty(h.husky_sort_host_many_workspace(ASCII, max(sizes), max(int(w.offsets[-1]) for w in wls), depth),
+                     dtype=torch.uint8, device="cuda")
+    h.husky_sort_host_many(ASCII, batches, ws, depth)
+    torch.cuda.synchronize()
+    for w, b in zip(wls, batches):
+        ref = oracle_mod.sort(ASCII, w.units, w.offsets)
+        assert np.array_equal(b[2].numpy().view(np.uint32), ref)
+        rsu, rso = oracle_mod.gather(ASCII, w.units, w.offsets, ref)
+        assert np.array_equal(b[4].numpy(), rso)
+        assert np.array_equal(b[3].numpy()[:rsu.size], rsu)
 
 
 @pytest.mark.parametrize("world", [2, 5])
