@@ -32,7 +32,8 @@ STATUS = {0: "HUSKY_OK", 1: "HUSKY_ERR_INVALID_ARG", 2: "HUSKY_ERR_DOMAIN", 3: "
           4: "HUSKY_ERR_NCCL", 5: "HUSKY_ERR_WORKSPACE", 6: "HUSKY_ERR_CAPACITY"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhusky.so")
+# HUSKY_LIB: load another build of the same sources (lab A/B builds only)
+LIB_PATH = os.environ.get("HUSKY_LIB") or os.path.join(_HERE, "libhusky.so")
 
 
 class HuskyError(RuntimeError):

@@ -38,11 +38,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    """out: another output path (lab A/B builds with HUSKY_NVCC_DEFS)."""
+    if out is not None:
+        return _build_to(out, verbose)
     if not force and not _stale():
         return LIB
+    return _build_to(LIB, verbose)
+
+
+def _build_to(lib_path: str, verbose: bool) -> str:
     inc, libdir = nccl_paths()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build") if lib_path == LIB else lib_path + ".objs"
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", *ARCH, f"-I{inc}",
               "-DNDEBUG", "--expt-relaxed-constexpr"]
@@ -60,14 +67,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for p, cmd in procs:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib_path + f".tmp{os.getpid()}"
     link = [NVCC, "-shared", *ARCH, "-o", tmp, *objs, f"-L{libdir}", "-l:libnccl.so.2",
             f"-Xlinker", f"-rpath={libdir}", "-lcudart"]
     if verbose:
         print(" ".join(link))
     subprocess.check_call(link)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 def build_cub_bar(force: bool = False) -> str:
@@ -83,4 +90,6 @@ def build_cub_bar(force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python _build.py [--force] [--out PATH]   (HUSKY_NVCC_DEFS="-D..." for lab variants)
+    o = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose=True, out=o))

@@ -135,10 +135,20 @@ __global__ void __launch_bounds__(kEncThreads, 4) k_encode(const void *__restric
                                                         const int64_t *__restrict__ offsets, uint64_t n,
                                                         uint64_t *__restrict__ codes, uint32_t *viol_out,
                                                         uint32_t *__restrict__ packed, uint4 *__restrict__ slab,
-                                                        int slab_all) {
+                                                        int slab_all, uint32_t *alpha) {
   constexpr int W = CoderTraits<CODER>::kUnitBytes;
   constexpr bool kSlabCoder = CODER == HUSKY_CODER_ASCII || CODER == HUSKY_CODER_UNICODE;
   uint32_t viol = 0;
+  // ASCII: which 7-bit field values occur in the code windows, as one byte
+  // flag per value in shared memory (plain byte stores of 1: racing writers
+  // agree), OR-ed into DevState::alpha at the end -- cheaper in the loop than
+  // a 128-bit register mask (C5 encode 16.3 ms with the mask)
+  __shared__ uint8_t s_pres[128];
+  const bool want_alpha = CODER == HUSKY_CODER_ASCII && alpha != nullptr;
+  if (want_alpha) {
+    if (threadIdx.x < 128) s_pres[threadIdx.x] = 0;
+    __syncthreads();
+  }
   const uint32_t lane = lane_id();
   const uintptr_t ub = (uintptr_t)units;
   const int64_t ofirst = __ldg(offsets), olast = __ldg(offsets + n);
@@ -190,6 +200,11 @@ __global__ void __launch_bounds__(kEncThreads, 4) k_encode(const void *__restric
       const uint64_t i = base + threadIdx.x + (uint64_t)k * blockDim.x;
       const int64_t L = o1[k] - o0[k];
       const uint64_t c = encode_words<CODER>(w0[k], w1[k], w2[k], sh[k], L, viol);
+      if (want_alpha && i < n) {
+        // the nine 7-bit fields of the code (padding fields are 0: always counted)
+#pragma unroll
+        for (int f = 0; f < 9; ++f) s_pres[(uint32_t)(c >> (7 * (8 - f))) & 0x7Fu] = 1;
+      }
       if (i < n) {
         codes[i] = c;
         // initial radix payload: index | min(len, 15) << 28 (n <= 2^28 only)
@@ -214,10 +229,18 @@ __global__ void __launch_bounds__(kEncThreads, 4) k_encode(const void *__restric
   // reduce violation bits: one atomic per warp that saw any
   viol = __reduce_or_sync(0xFFFFFFFFu, viol);
   if (lane == 0 && viol) atomicOr(viol_out, viol);
+  if (want_alpha) {
+    __syncthreads();
+    if (threadIdx.x < 128) {
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, s_pres[threadIdx.x] != 0);
+      if (lane == 0 && m) atomicOr(alpha + (threadIdx.x >> 5), m);
+    }
+  }
 }
 
 void launch_encode(int coder, const void *units, const int64_t *offsets, uint64_t n, uint64_t *codes,
-                   uint32_t *viol, int num_sms, cudaStream_t s, uint32_t *packed, uint4 *slab, bool slab_all) {
+                   uint32_t *viol, int num_sms, cudaStream_t s, uint32_t *packed, uint4 *slab, bool slab_all,
+                   uint32_t *alpha) {
   if (n == 0) return;
   Scope sc_(ST_ENCODE, s, n);
   uint64_t blocks = (n + kEncThreads * kEncIT - 1) / (kEncThreads * kEncIT);
@@ -227,19 +250,19 @@ void launch_encode(int coder, const void *units, const int64_t *offsets, uint64_
   switch (coder) {
     case HUSKY_CODER_ASCII:
       k_encode<HUSKY_CODER_ASCII><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, viol, packed,
-                                                                           slab, sa);
+                                                                           slab, sa, alpha);
       break;
     case HUSKY_CODER_UNICODE:
       k_encode<HUSKY_CODER_UNICODE><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, viol, packed,
-                                                                             slab, sa);
+                                                                             slab, sa, nullptr);
       break;
     case HUSKY_CODER_ENGLISH5:
       k_encode<HUSKY_CODER_ENGLISH5><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, viol, packed,
-                                                                              nullptr, 0);
+                                                                              nullptr, 0, nullptr);
       break;
     default:
       k_encode<HUSKY_CODER_ENGLISH6><<<(unsigned)blocks, kEncThreads, 0, s>>>(units, offsets, n, codes, viol, packed,
-                                                                              nullptr, 0);
+                                                                              nullptr, 0, nullptr);
       break;
   }
 }

@@ -50,15 +50,25 @@ struct GatherRuns {
   DevState *st;            // n_runs
 };
 
+// look-back words per lane and round trip (32 V predecessors per round);
+// measured on C5 (2^30) gathers: V = 1 42.4 ms, 2 45.1, 4 46.4 -- the walk
+// width is not what bounds the gather (C2: 252 / 262 / 277 us)
+#ifndef HUSKY_GATHER_LBV
+#define HUSKY_GATHER_LBV 1
+#endif
+constexpr int kGatherLbV = HUSKY_GATHER_LBV;
+
 template <int CODER, bool PACKED, bool CHECK, bool PEER>
-// 5 CTAs/SM (48 registers): measured 280 vs 289 us (4/SM) and 298 us (6/SM) on C2
 // L1 prefetch of the long strings' units: 0 = as soon as the offset is loaded
 // (before the block scan), 1 = after the tile's aggregate is published, 2 = none
 #ifndef HUSKY_GATHER_PF
 #define HUSKY_GATHER_PF 1
 #endif
+// resident CTAs per SM: 5 for the packed instantiations (48 registers; C2
+// 280 vs 289 us at 4), 4 for the others (64 registers, no spills: the C5 gather
+// with slab records 50 -> 44 ms)
 #ifndef HUSKY_GATHER_MINB
-#define HUSKY_GATHER_MINB 5
+#define HUSKY_GATHER_MINB (PACKED ? 5 : 4)
 #endif
 __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
     k_gather(uint32_t *__restrict__ perm, uint64_t n, const void *__restrict__ units,
@@ -78,8 +88,24 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   __shared__ uint32_t s_llen[CHECK ? kGatherThreads : 1], s_lidx[CHECK ? kGatherThreads : 1];
   // PEER: the buckets' start positions / units in the partitioned order
   __shared__ unsigned long long s_sn[PEER ? kMaxPeers + 1 : 1], s_su[PEER ? kMaxPeers + 1 : 1];
+  // alphabet-compressed ASCII codes: rank -> unit (the inverse of the re-packing)
+  __shared__ uint8_t s_unrank[64];
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   pdl_wait();  // the main gather is a programmatic dependent of the key sort
+  uint32_t cbits = 0;
+  bool ccomp = false;
+  if (CODER == HUSKY_CODER_ASCII && (PACKED || CHECK) && st && st->ccomp) {
+    ccomp = true;
+    cbits = st->cbits;
+    if (tid < 128) {
+      const uint32_t a[4] = {st->alpha[0], st->alpha[1], st->alpha[2], st->alpha[3]};
+      if (tid == 0 || ((a[tid >> 5] >> (tid & 31)) & 1u)) s_unrank[alpha_rank(a, tid)] = (uint8_t)tid;
+    }
+  }
+  // unit byte b (< S) of a string rebuilt from its sorted code
+  auto decb = [&](uint64_t code, int b) -> uint8_t {
+    return ccomp ? decode_byte_c(code, b, cbits, s_unrank) : decode_byte<CODER>(code, b);
+  };
   if (PEER) {
     for (uint32_t b = tid; b <= peer->world; b += kGatherThreads) {
       s_sn[b] = peer->start_n[b];
@@ -254,13 +280,13 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       const uint64_t lo = d > w0 ? d : w0, hi = d + nb < w1 ? d + nb : w1;
       if (lo < hi) {
         if (PACKED && ((dec >> j) & 1)) {
-          for (uint64_t x = lo; x < hi; ++x) stage[x - w0] = decode_byte<CODER>(sv[j], (int)(x - d));
+          for (uint64_t x = lo; x < hi; ++x) stage[x - w0] = decb(sv[j], (int)(x - d));
         } else if (CHECK && ((slb >> j) & 1)) {
           constexpr int SB = T::kS * W;  // string bytes [0, SB) come from the code
           const uint4 rec = s_slab[j * kGatherThreads + tid];
           for (uint64_t x = lo; x < hi; ++x) {
             const int b = (int)(x - d);
-            stage[x - w0] = b < SB ? decode_byte<CODER>(sv[j], b) : slab_byte(rec, b - SB + 1);
+            stage[x - w0] = b < SB ? decb(sv[j], b) : slab_byte(rec, b - SB + 1);
           }
         } else {
           const uint8_t *sp = ub + sv[j] * W;
@@ -342,14 +368,14 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   }
   if (warp == 0) {
     unsigned long long ex =
-        tile == 0 ? 0ull : ((dbg & 2) ? lookback(lb, tile, 1, epoch) : warp_lookback(lb, tile, epoch));
+        tile == 0 ? 0ull : ((dbg & 2) ? lookback(lb, tile, 1, epoch) : warp_lookback<kGatherLbV>(lb, tile, epoch));
     if (lane == 0) {
       if (tile != 0) st_relaxed_u64(lb + tile, make_flag(kFlagInc, epoch, ex + tile_total));
       s_base = ex;
       if (!PEER && (uint64_t)(tile + 1) * kGatherTile >= n) sorted_offsets[n] = (int64_t)(gbase + ex + tile_total);
     }
   } else if (CHECK && warp == 1) {  // the run-count scan's look-back, next to warp 0's
-    unsigned long long ex = tile == 0 ? 0ull : warp_lookback(runs.lb, tile, epoch);
+    unsigned long long ex = tile == 0 ? 0ull : warp_lookback<kGatherLbV>(runs.lb, tile, epoch);
     if (lane == 0) {
       if (tile != 0) st_relaxed_u64(runs.lb + tile, make_flag(kFlagInc, epoch, ex + tile_runs));
       s_rbase = ex;
@@ -472,9 +498,9 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
           const uint4 r = s_slab[j * kGatherThreads + (warp * 32 + t)];
           constexpr int SB = T::kS * W;
           for (uint64_t b = lane; b < nb; b += 32)
-            ob[d * W + b] = b < SB ? decode_byte<CODER>(s, (int)b) : slab_byte(r, (int)b - SB + 1);
+            ob[d * W + b] = b < SB ? decb(s, (int)b) : slab_byte(r, (int)b - SB + 1);
         } else if (PACKED && ((dt >> j) & 1)) {
-          for (uint64_t b = lane; b < nb; b += 32) ob[d * W + b] = decode_byte<CODER>(s, (int)b);
+          for (uint64_t b = lane; b < nb; b += 32) ob[d * W + b] = decb(s, (int)b);
         } else {
           for (uint64_t b = lane; b < nb; b += 32) ob[d * W + b] = ub[s * W + b];
         }
@@ -503,9 +529,9 @@ void launch_gather(int coder, uint32_t *perm, uint64_t n, const void *units, con
   if (!chk) slab = nullptr;  // slab records are read by the main (CHECK) gather only
 #define G_LAUNCH(C, P, K)                                                                                         \
   do {                                                                                                            \
-    constexpr int kSmem = kGatherStage + 32 + (K ? kGatherTile * 16 : 0);                                         \
+    const int kSmem = kGatherStage + 32 + (K && slab ? kGatherTile * 16 : 0);                                     \
     static SmemAttr attr;                                                                                         \
-    attr.ensure(k_gather<C, P, K, false>, kSmem);                                                                 \
+    attr.ensure(k_gather<C, P, K, false>, kGatherStage + 32 + (K ? kGatherTile * 16 : 0));                        \
     launch_pdl(k_gather<C, P, K, false>, g, b, kSmem, s, perm, n, units, offsets, sorted_units, sorted_offsets, lb, \
                tile_counter, epoch, base_ptr, dbg, packed_codes, st, runs, (const PeerTable *)nullptr, slab);     \
   } while (0)

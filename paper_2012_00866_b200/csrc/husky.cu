@@ -128,6 +128,18 @@ static husky_status cuda_check(const char *where) {
 static husky_status refine_giants(Sorter &S, const DevState &hs0, void *d_sorted_units, int64_t *d_sorted_offsets,
                                   DevState *out, bool general);
 
+// HUSKY_SLAB=1 forces the slab records at any size (tests), 0 disables them
+// (read per sort: a getenv, so tests can switch it within one process)
+static int slab_env() {
+  const char *e = getenv("HUSKY_SLAB");
+  return e ? atoi(e) : -1;
+}
+
+static bool alpha_env() {
+  const char *e = getenv("HUSKY_ALPHA");
+  return !(e && e[0] == '0');
+}
+
 husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
                        uint32_t *d_perm, void *d_sorted_units, int64_t *d_sorted_offsets, void *d_ws,
                        size_t ws_bytes, husky_outcome *h_out, cudaStream_t s) {
@@ -176,18 +188,27 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // the gather rebuilds short strings from ASCII / UNICODE codes only
   const bool packed = n <= kPackMaxN && (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE);
   uint32_t *packed_payload = packed ? S.at<uint32_t>(L.vals2) : nullptr;
-  // slab records (ASCII / UNICODE) when sorted strings are produced: every
-  // string's when n > 2^28 (no packed lengths), else only the long strings'
-  uint4 *slab = (d_sorted_units && (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE))
-                    ? S.at<uint4>(L.slab) : nullptr;
+  // slab records (ASCII / UNICODE) when sorted strings are produced and the
+  // gather's random reads would miss L2: n > kSlabMinN strings (the offsets
+  // alone then span >= 2x the 126 MB L2).  Every string's record when n > 2^28
+  // (no packed lengths), else only the long strings'.  Below the threshold the
+  // random reads mostly hit L2 and the records cost more than they save (C2:
+  // encode 76 -> 119 us, gather 276 -> 332 us with them).  HUSKY_SLAB=1 / 0
+  // forces them on / off (tests).
+  // alphabet compression of the sort's private keys (ASCII; HUSKY_ALPHA=0 off)
+  const bool compress = coder == HUSKY_CODER_ASCII && alpha_env();
+  uint4 *slab = nullptr;
+  if (d_sorted_units && (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE) &&
+      ((n > kSlabMinN && slab_env() != 0) || slab_env() == 1))
+    slab = S.at<uint4>(L.slab);
   uint64_t *keysA = S.keysA(), *keysB = S.keysB();
   uint32_t *vals_tmp = S.at<uint32_t>(L.vals);
   {
     GroupScope grp(ST_ENCODE, s);
     launch_encode(coder, d_units, d_offsets, n, S.keysA(), &st->violations, S.sms, s, packed_payload, slab,
-                  !packed);
+                  !packed, compress ? st->alpha : nullptr);
   }
-  launch_hist_plan(keysA, n, st, keysA, keysB, S.sms, s);
+  launch_hist_plan(keysA, n, st, keysA, keysB, S.sms, s, compress);
 
   // ---- A2 key sort, LSD onesweep: (code, index) -> sorted codes, perm.  The
   // pass plan (which digits are not shared by all keys) is made on device, so

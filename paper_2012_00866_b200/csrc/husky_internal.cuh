@@ -88,8 +88,33 @@ struct DevState {
   // refinement / fix-up kernels compare whole strings from unit 0 instead of
   // relying on equal codes (no short rule, no known-equal prefix)
   uint32_t general;
-  uint32_t pad[15];
+  // alphabet compression of ASCII codes (radix.cu): which 7-bit field values
+  // occur in the code windows (bit v of alpha), and whether the sort's keys
+  // were re-packed with cbits bits per field (ccomp)
+  uint32_t alpha[4];
+  uint32_t ccomp, cbits;
+  uint32_t pad[9];
 };
+
+// Alphabet compression (ASCII): the code's nine 7-bit fields re-packed as
+// their ranks among the field values present (0 -- padding / NUL -- always
+// counted), cbits = ceil(log2(#values)) bits each.  A monotone bijection of
+// each field, so the order of codes, equality of codes, and hence every run is
+// unchanged; with <= 64 values (cbits <= 6) the key fits 56 bits and the LSD
+// sort needs 7 passes instead of 8 (<= 32 values, e.g. one letter case: 6).
+__device__ __forceinline__ uint32_t alpha_bits(const uint32_t a[4]) {
+  const uint32_t cnt = __popc(a[0] | 1u) + __popc(a[1]) + __popc(a[2]) + __popc(a[3]);
+  return cnt <= 1 ? 0u : 32u - __clz(cnt - 1);  // ceil(log2(cnt))
+}
+// rank of field value v (0..127) among the present values
+__device__ __forceinline__ uint32_t alpha_rank(const uint32_t a[4], uint32_t v) {
+  const uint32_t w = v >> 5, below = (1u << (v & 31)) - 1u;
+  uint32_t r = __popc((w == 0 ? (a[0] | 1u) : a[w]) & below);
+  if (w > 0) r += __popc(a[0] | 1u);
+  if (w > 1) r += __popc(a[1]);
+  if (w > 2) r += __popc(a[2]);
+  return r;
+}
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per device and kernel:
 // the attribute belongs to the kernel's function handle in each device's
@@ -216,32 +241,56 @@ __device__ __forceinline__ unsigned long long lookback_window(const unsigned lon
 }
 
 
-// Warp-cooperative look-back (all 32 lanes call it): lane l reads the word of
-// tile (base - l); the nearest inclusive word ends the walk.  Returns the
-// exclusive prefix of `tile` in every lane.
+// Warp-cooperative look-back (all 32 lanes call it): one round trip reads the
+// 32*V nearest unconsumed predecessors (lane l the V words of tiles
+// base - V*l - v, v = 0..V-1); the nearest inclusive word ends the walk.
+// Returns the exclusive prefix of `tile` in every lane.
+// A walk that starts d tiles past the inclusive frontier takes d / (32 V)
+// round trips, so a single-pass scan cannot retire more than 32 V tiles per
+// round trip whatever its concurrency (the gather at 2^30 strings was bound
+// there with V = 1: 21.6 G strings/s = 32 tiles of 1024 per ~1.5 us).
+template <int V = 1>
 __device__ __forceinline__ unsigned long long warp_lookback(const unsigned long long *flags, uint32_t tile,
                                                             uint32_t epoch) {
   const uint32_t lane = threadIdx.x & 31;
   unsigned long long excl = 0;
   int64_t base = (int64_t)tile - 1;
   while (base >= 0) {
-    int64_t j = base - (int64_t)lane;
-    unsigned long long x = j >= 0 ? ld_relaxed_u64(flags + j) : make_flag(kFlagInc, epoch, 0);
-    bool valid = ((uint32_t)(x >> 54) & 0xFF) == epoch && (x & (3ull << 62)) != 0;
-    bool inc = valid && (x & (3ull << 62)) == kFlagInc;
-    uint32_t vmask = __ballot_sync(0xFFFFFFFFu, valid), imask = __ballot_sync(0xFFFFFFFFu, inc);
-    uint32_t take;  // number of leading lanes consumed this round
-    bool stop;
-    uint32_t first_invalid = __ffs(~vmask) - 1;  // 32 if all valid (ffs(0) = 0 -> 0xFFFFFFFF -> wrap)
-    if (vmask == 0xFFFFFFFFu) first_invalid = 32;
-    uint32_t first_inc = imask ? (uint32_t)(__ffs(imask) - 1) : 32u;
-    if (first_inc < first_invalid) { take = first_inc + 1; stop = true; }
-    else { take = first_invalid; stop = false; }
-    unsigned long long v = lane < take ? (x & kValMask) : 0ull;
+    unsigned long long x[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int64_t j = base - (int64_t)(V * lane + v);
+      x[v] = j >= 0 ? ld_relaxed_u64(flags + j) : make_flag(kFlagInc, epoch, 0);
+    }
+    // this lane's consumable prefix of its V words (nearest first): up to the
+    // first unpublished word (exclusive) or the first inclusive word (inclusive)
+    uint32_t k = 0;
+    bool inc = false;
+    unsigned long long part = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (k != (uint32_t)v || inc) break;
+      const bool valid = ((uint32_t)(x[v] >> 54) & 0xFF) == epoch && (x[v] & (3ull << 62)) != 0;
+      if (!valid) break;
+      part += x[v] & kValMask;
+      k = v + 1;
+      inc = (x[v] & (3ull << 62)) == kFlagInc;
+    }
+    const bool full = k == (uint32_t)V && !inc;
+    const uint32_t notfull = __ballot_sync(0xFFFFFFFFu, !full);
+    const uint32_t L = notfull ? (uint32_t)(__ffs(notfull) - 1) : 32u;  // first lane that stopped
+    unsigned long long v = lane <= L ? part : 0ull;  // lanes before L: all V words; lane L: its prefix
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
     excl += v;
+    if (L == 32) {
+      base -= 32 * V;
+      continue;
+    }
+    const uint32_t kL = __shfl_sync(0xFFFFFFFFu, k, L);
+    const bool stop = __shfl_sync(0xFFFFFFFFu, (int)inc, L) != 0;
     if (stop) break;
+    const uint32_t take = L * V + kL;
     base -= take;
     if (take == 0) __nanosleep(64);  // nearest predecessor unpublished: back off
   }
@@ -307,6 +356,12 @@ __device__ __forceinline__ uint64_t load8_unaligned(const uint8_t *p, int need) 
   uint64_t v = lo >> (8 * sh);
   if (sh + need > 8) v |= __ldg(w + 1) << (64 - 8 * sh);
   return v;
+}
+
+// Byte b (0..8) of an ASCII string rebuilt from its alphabet-compressed code:
+// field b holds the rank, unrank[] maps it back to the unit.
+__device__ __forceinline__ uint8_t decode_byte_c(uint64_t code, int b, uint32_t bits, const uint8_t *unrank) {
+  return unrank[(uint32_t)(code >> (bits * (8 - b))) & ((1u << bits) - 1u)];
 }
 
 // Byte k (1..15) of a slab record held in registers.

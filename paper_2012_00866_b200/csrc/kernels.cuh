@@ -21,14 +21,19 @@ constexpr int kEncThreads = 256, kEncBlocksPerSM = HUSKY_ENC_BPS;  // grid (resi
 // for every string, else only for strings longer than PL.  viol: violation
 // bits (OR-ed).
 constexpr uint64_t kPackMaxN = 1ull << 28;
+// slab records only above this many strings (offsets >= 2x the L2)
+constexpr uint64_t kSlabMinN = 1ull << 25;
 void launch_encode(int coder, const void *units, const int64_t *offsets, uint64_t n, uint64_t *codes,
                    uint32_t *viol, int num_sms, cudaStream_t s, uint32_t *packed = nullptr, uint4 *slab = nullptr,
-                   bool slab_all = false);
+                   bool slab_all = false, uint32_t *alpha = nullptr);
 // 8 digit histograms (8-bit digits) of n keys into DevState::hist (accumulates)
 void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_sms, cudaStream_t s);
 // histograms + k_hist_scan + the pass plan fused (the last CTA scans and plans)
+// compress: ASCII codes with DevState::alpha from the encoder -- the keys are
+// re-packed in place (alphabet compression, husky_internal.cuh) when that
+// saves a pass, before the histograms
 void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *keysA, uint64_t *keysB,
-                      int num_sms, cudaStream_t s);
+                      int num_sms, cudaStream_t s, bool compress = false);
 
 // A2 onesweep radix
 // 512 threads x 12 keys = 6144-key tiles, 92 KB smem (keys, payloads, u16

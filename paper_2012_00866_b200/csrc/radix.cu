@@ -53,14 +53,25 @@ void launch_hist_scan(uint64_t n, DevState *st, cudaStream_t s) {
 // histograms (ticket) also does k_hist_scan's scans and the pass plan (which
 // digits to sort, in which order), saving two dependent launches.
 constexpr int kHistBlocksPerSM = 4;  // resident CTAs of 512 threads per SM
+// compress (ASCII, PLAN): alphabet compression first (husky_internal.cuh):
+// every key is re-packed in place from DevState::alpha when that needs at most
+// 56 bits, and the histograms are those of the re-packed keys.
 template <bool PLAN>
-__global__ void __launch_bounds__(512) k_hist_slots(const uint64_t *__restrict__ keys, uint64_t n, DevState *st,
-                                                    uint64_t *keysA, uint64_t *keysB) {
+__global__ void __launch_bounds__(512) k_hist_slots(uint64_t *__restrict__ keys, uint64_t n, DevState *st,
+                                                    uint64_t *keysA, uint64_t *keysB, int compress) {
   constexpr uint32_t M = kBins - 1;
   pdl_wait();  // PLAN: launched as a programmatic dependent of the encoder
   __shared__ uint32_t h[8 * kBins];
   __shared__ uint32_t s_last, s_wt[512 / 32 + 1];
+  __shared__ uint8_t s_rank[128];
   for (int i = threadIdx.x; i < 8 * kBins; i += blockDim.x) h[i] = 0;
+  uint32_t cbits = 7;
+  if (compress) {
+    const uint32_t a[4] = {st->alpha[0], st->alpha[1], st->alpha[2], st->alpha[3]};
+    cbits = alpha_bits(a);
+    if (threadIdx.x < 128) s_rank[threadIdx.x] = (uint8_t)alpha_rank(a, threadIdx.x);
+  }
+  const bool cmp = cbits <= 6;
   __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * 4; base < n; base += stride) {
@@ -68,7 +79,18 @@ __global__ void __launch_bounds__(512) k_hist_slots(const uint64_t *__restrict__
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const uint64_t i = base + threadIdx.x + (uint64_t)r * blockDim.x;
-      k[r] = i < n ? __ldg(keys + i) : 0;
+      k[r] = i < n ? keys[i] : 0;
+    }
+    if (cmp) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint64_t i = base + threadIdx.x + (uint64_t)r * blockDim.x;
+        uint64_t c = 0;
+#pragma unroll
+        for (int f = 0; f < 9; ++f) c |= (uint64_t)s_rank[(uint32_t)(k[r] >> (7 * (8 - f))) & 0x7Fu] << (cbits * (8 - f));
+        k[r] = c;
+        if (i < n) keys[i] = c;
+      }
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -99,6 +121,8 @@ __global__ void __launch_bounds__(512) k_hist_slots(const uint64_t *__restrict__
   }
   if (threadIdx.x == 0) {
     st->trivial_mask = trivial;
+    st->ccomp = cmp ? 1u : 0u;
+    st->cbits = cbits;
     uint32_t np = 0;
     for (int d = 0; d < 8; ++d)
       if (!((trivial >> d) & 1)) st->pass_digit[np++] = d;
@@ -111,18 +135,19 @@ void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_s
   if (n == 0) return;
   Scope sc_(ST_HIST_SCAN, s, n);
   const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * kHistBlocksPerSM);
-  k_hist_slots<false><<<(unsigned)blocks, 512, 0, s>>>(keys, n, st, nullptr, nullptr);
+  k_hist_slots<false><<<(unsigned)blocks, 512, 0, s>>>(const_cast<uint64_t *>(keys), n, st, nullptr, nullptr, 0);
 }
 
 // histograms + scans + pass plan of the device-planned passes in one launch
 // (DevState::hist_done must be 0: DevState is zeroed per sort)
 void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *keysA, uint64_t *keysB,
-                      int num_sms, cudaStream_t s) {
+                      int num_sms, cudaStream_t s, bool compress) {
   if (n == 0) return;
   Scope sc_(ST_HIST_SCAN, s, n);
   GroupScope grp(ST_HIST_SCAN, s);
   const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * kHistBlocksPerSM);
-  launch_pdl(k_hist_slots<true>, dim3((unsigned)blocks), dim3(512), 0, s, keys, n, st, keysA, keysB);
+  launch_pdl(k_hist_slots<true>, dim3((unsigned)blocks), dim3(512), 0, s, const_cast<uint64_t *>(keys), n, st, keysA,
+             keysB, compress ? 1 : 0);
 }
 
 constexpr int kRadixWarps = kRadixThreads / 32;
@@ -165,11 +190,11 @@ struct SlotPtrs {
   uint32_t *v_final, *v_tmp;
 };
 
-// One pass over one tile, decoupled look-back on `lb`.  vals_in == NULL
-// synthesises payload = index.  plan != NULL: this is pass slot `slot` of the
-// device-side plan (buffers, digit resolved here; slots beyond the plan exit at
-// once).  One instantiation per tile size.
-template <int ITEMS>
+// One pass over one tile, decoupled look-back on `lb`.  SYNTH: payload =
+// index (no payload read; the first pass).  plan != NULL: this is pass slot
+// `slot` of the device-side plan (buffers, digit resolved here; slots beyond
+// the plan exit at once).  Two instantiations per tile size (SYNTH or not).
+template <bool SYNTH, int ITEMS>
 __global__ void __launch_bounds__(kRadixThreads, 2)
     k_onesweep(const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint64_t n, int shift,
@@ -285,7 +310,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
 #pragma unroll
   for (int r = 0; r < ITEMS; ++r) {
     const uint64_t idx = tile_base + slot0 + r * 32;
-    v[r] = vals_in == nullptr ? (uint32_t)idx : (idx < n ? __ldg(vals_in + idx) : 0u);
+    v[r] = SYNTH ? (uint32_t)idx : (idx < n ? __ldg(vals_in + idx) : 0u);
   }
 
   // ---- global base of each digit
@@ -341,14 +366,17 @@ static void onesweep_launch(const uint64_t *keys_in, const uint32_t *vals_in, ui
                             uint32_t *tile_counter, uint32_t epoch, const DevState *plan, int slot,
                             const SlotPtrs &sp, cudaStream_t s) {
   constexpr int kX = exchange_bytes<ITEMS>();
-  static SmemAttr attr;
-  attr.ensure(k_onesweep<ITEMS>, kX);
+  static SmemAttr attr_s, attr_v;
+  attr_s.ensure(k_onesweep<true, ITEMS>, kX);
+  attr_v.ensure(k_onesweep<false, ITEMS>, kX);
   const uint64_t t = (uint64_t)kRadixThreads * ITEMS;
   const uint32_t tiles = (uint32_t)((n + t - 1) / t);
+  // the first planned slot synthesises the index when there is no initial payload
+  const bool synth = plan ? (slot == 0 && sp.v_init == nullptr) : vals_in == nullptr;
   // programmatic dependent launch: the pass's CTAs become resident while the
   // previous kernel's last wave drains and start as soon as it completes
-  launch_pdl(k_onesweep<ITEMS>, dim3(tiles), dim3(kRadixThreads), kX, s, keys_in, vals_in, keys_out, vals_out, n,
-             kDigitBits * digit, ds, lb, tile_counter, epoch, plan, slot, sp);
+  launch_pdl(synth ? k_onesweep<true, ITEMS> : k_onesweep<false, ITEMS>, dim3(tiles), dim3(kRadixThreads), kX, s,
+             keys_in, vals_in, keys_out, vals_out, n, kDigitBits * digit, ds, lb, tile_counter, epoch, plan, slot, sp);
 }
 
 void launch_onesweep(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,

@@ -525,3 +525,67 @@ def test_programmatic_launch_off_matches(torch, h, tmp_path):
     r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert np.array_equal(np.load(tmp_path / "p.npy"), p_pdl)
+
+
+# ---------------------------------------------------------------- slab records
+@pytest.mark.parametrize("name,n", [("C1", 70_001), ("C2", 300_000), ("C3", 200_003), ("C4", 50_000),
+                                    ("C5", 300_000)])
+def test_slab_records_forced(torch, h, oracle_mod, monkeypatch, name, n):
+    """The gather's slab path (one 16-B record per string: length + the units
+    after the code window) forced at sizes where it is normally off; bit-exact
+    against the oracle for every config (packed: only strings longer than PL
+    have records)."""
+    monkeypatch.setenv("HUSKY_SLAB", "1")
+    check_against_oracle(torch, h, oracle_mod, W.make(name, n))
+
+
+@pytest.mark.parametrize("coder", [ASCII, UNICODE])
+def test_slab_record_boundaries(torch, h, oracle_mod, monkeypatch, coder):
+    """Lengths around the record's capacity (ASCII 24 / UNICODE 10 units: longer
+    strings fall back to offsets + units), around PL and S, empty strings, NUL
+    and extreme units, shared prefixes (equal codes: the order check compares
+    slab-staged bytes)."""
+    monkeypatch.setenv("HUSKY_SLAB", "1")
+    rng = np.random.default_rng(77 + coder)
+    hi = 0x7F if coder == ASCII else 0xFFFF
+    cap = 24 if coder == ASCII else 10
+    lens = [0, 1, 2, 3, 4, 8, 9, 10, cap - 1, cap, cap + 1, cap + 7, 40]
+    strings = []
+    prefix = rng.integers(1, hi, size=50).tolist()
+    for i in range(60_000):
+        L = int(lens[i % len(lens)])
+        if i % 3 == 0:
+            s = prefix[:L]  # shared prefixes: equal codes, exact compare from unit S
+            if L and i % 6 == 0:
+                s = s[:-1] + [int(rng.integers(0, hi + 1))]
+        else:
+            s = rng.integers(0, hi + 1, size=L).tolist()
+        strings.append(s)
+    w = W.from_strings(strings, coder)
+    check_against_oracle(torch, h, oracle_mod, w)
+
+
+# --------------------------------------------------------- alphabet compression
+@pytest.mark.parametrize("alpha", [1, 2, 26, 31, 32, 33, 62, 63, 64, 100])
+def test_alphabet_compression_sizes(torch, h, oracle_mod, alpha):
+    """ASCII keys re-packed as field ranks (cbits = ceil(log2(#values incl. 0))):
+    alphabet sizes around the 5/6/7-bit boundaries (63 values + padding = 64 is
+    the last one that compresses), NUL among them, lengths 0..14 so padding
+    and truncation occur; bit-exact against the oracle (perm, sorted units --
+    the gather rebuilds units from the compressed codes)."""
+    rng = np.random.default_rng(1000 + alpha)
+    vals = rng.choice(np.arange(0, 128), size=alpha, replace=False)
+    strings = [rng.choice(vals, size=int(rng.integers(0, 15))).tolist() for _ in range(120_000)]
+    w = W.from_strings(strings, ASCII)
+    outc = check_against_oracle(torch, h, oracle_mod, w)
+    if alpha <= 31:  # main key sort: at most 6 passes (refinement passes come on top of radix_passes)
+        assert outc["keys_partitioned"] <= 6 * w.n
+
+
+def test_alphabet_compression_off_matches(torch, h, oracle_mod, monkeypatch):
+    """HUSKY_ALPHA=0 (raw 7-bit fields) sorts C1 identically, with more passes."""
+    w = W.make("C1", 200_000)
+    on = check_against_oracle(torch, h, oracle_mod, w)
+    monkeypatch.setenv("HUSKY_ALPHA", "0")
+    off = check_against_oracle(torch, h, oracle_mod, w)
+    assert on["keys_partitioned"] < off["keys_partitioned"]

@@ -2,7 +2,7 @@
 breakdown (profiler mode 1, one event pair per launch), GPU verifier, and the
 same with HUSKY_KEYSORT=msd if requested.  Not a bench line.
 
-  python tools/c5_probe.py [log2n=30] [reps=3]
+  python tools/c5_probe.py [log2n=30] [reps=3] [config=C5]   (C1-C4: numpy generator, n = 2^log2n)
 """
 import json
 import os
@@ -23,28 +23,38 @@ def main():
     lg = int(sys.argv[1]) if len(sys.argv) > 1 else 30
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     N = 1 << lg
+    cfg = sys.argv[3] if len(sys.argv) > 3 else "C5"
     torch.cuda.set_device(0)
     t0 = time.time()
-    u, o = G.c5_device(N)
+    if cfg == "C5":
+        u, o = G.c5_device(N)
+    else:
+        import numpy as np
+        import workloads as W
+        w = W.make(cfg, N)
+        uu = w.units.view(np.int16) if w.units.dtype == np.uint16 else w.units
+        u = torch.from_numpy(np.concatenate([uu, np.zeros(16, uu.dtype)])).cuda()
+        o = torch.from_numpy(w.offsets).cuda()
+    coder = 1 if cfg == "C3" else 0
     torch.cuda.synchronize()
     gen_s = time.time() - t0
     total = int(o[-1].item())
-    ws = torch.empty(h.husky_sort_workspace(0, N, total), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(h.husky_sort_workspace(coder, N, total), dtype=torch.uint8, device="cuda")
     perm = torch.empty(N, dtype=torch.int32, device="cuda")
-    su = torch.empty(total + 16, dtype=torch.uint8, device="cuda")
+    su = torch.empty(total + 16, dtype=u.dtype, device="cuda")
     so = torch.empty(N + 1, dtype=torch.int64, device="cuda")
-    res = {"n": N, "gen_s": round(gen_s, 2), "ws_gb": round(ws.numel() / 1e9, 2),
+    res = {"lib": os.environ.get("HUSKY_LIB", "default"), "config": cfg, "n": N, "gen_s": round(gen_s, 2), "ws_gb": round(ws.numel() / 1e9, 2),
            "mem_alloc_gb": round(torch.cuda.memory_allocated() / 1e9, 2)}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(2):
-        outc = h.husky_sort(0, u, o, perm, su, so, ws)
+        outc = h.husky_sort(coder, u, o, perm, su, so, ws)
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         flush.fill_(1)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        h.husky_sort(0, u, o, perm, su, so, ws)
+        h.husky_sort(coder, u, o, perm, su, so, ws)
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
@@ -52,13 +62,13 @@ def main():
     h.husky_profile_reset()
     h.husky_profile_enable(1)
     flush.fill_(2)
-    h.husky_sort(0, u, o, perm, su, so, ws)
+    h.husky_sort(coder, u, o, perm, su, so, ws)
     torch.cuda.synchronize()
     h.husky_profile_enable(False)
     res["stages"] = {k: round(v["ms"], 3) for k, v in h.husky_profile_read().items() if v["launches"]}
     res["outcome"] = outc
     t0 = time.time()
-    res["verify"] = checker.verify(u, o, perm, su, so)
+    res["verify"] = checker.verify(u, o, perm, su[:total], so)
     res["verify_s"] = round(time.time() - t0, 2)
     print(json.dumps(res), flush=True)
 
