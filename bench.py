@@ -299,8 +299,12 @@ def measure_single(args, name, n, dev, steps, warmup, flush, want_e2e, h, torch)
 
     # ---- timed region: K steps, an event pair per step; profiler mode 2 adds
     # event pairs around the encoder, histogram, radix-pass group and main gather
+    # (large inputs only: below 2^22 strings the extra records would show in the
+    # step time and they also turn off the library's CUDA-graph replay; the
+    # per-kernel times then come from the breakdown steps)
     h.husky_profile_reset()
-    h.husky_profile_enable(2)
+    group_events = n >= (1 << 22)
+    h.husky_profile_enable(2 if group_events else 0)
     l0 = h.husky_launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     bad = {"pairs": 0, "perm": 0, "content": 0, "offsets": 0}
@@ -320,7 +324,7 @@ def measure_single(args, name, n, dev, steps, warmup, flush, want_e2e, h, torch)
             l0 = h.husky_launch_count()
         torch.cuda.synchronize()
     h.husky_profile_enable(False)
-    groups = h.husky_profile_read()
+    groups = h.husky_profile_read() if group_events else None
     times = [a.elapsed_time(b) for a, b in ev]
     med, mn, mean = statistics.median(times), min(times), statistics.mean(times)
 
@@ -351,7 +355,10 @@ def measure_single(args, name, n, dev, steps, warmup, flush, want_e2e, h, torch)
     peak, peak_src = peaks()
     packed = n <= PACK_MAX_N and coder in (0, 1)
     survey, builder, gstats = byte_models(wl, passes, packed)
-    g = {k: v["ms"] / steps for k, v in groups.items() if v["ms"]}
+    if groups is not None:
+        g = {k: v["ms"] / steps for k, v in groups.items() if v["ms"]}
+    else:  # small inputs: per-kernel times from the breakdown steps
+        g = {k: v["ms_per_step"] for k, v in stages.items()}
     kern = {}
     if passes:
         rp = g.get("radix_pass", 0.0) / passes
@@ -388,8 +395,9 @@ def measure_single(args, name, n, dev, steps, warmup, flush, want_e2e, h, torch)
                      "share_of_step": round(kern[dom]["ms_per_launch"] * (passes if dom == "radix_pass" else 1)
                                             / med, 4),
                      "model": "survey (SURVEY.md 8(d)); model_builder beside it",
-                     "timing": "CUDA events recorded by the library on its launch stream around the kernel "
-                               "group, every timed step (profiler mode 2)",
+                     "timing": ("CUDA events recorded by the library on its launch stream around the kernel "
+                                "group, every timed step (profiler mode 2)") if groups is not None else
+                               "breakdown steps, an event pair per launch (n < 2^22: kept out of the timed steps)",
                      "kernels": kern})
     res = {"name": name, "n": n, "coder": coder, "wl": wl, "times": times, "median": med, "min": mn, "mean": mean,
            "outcome": outc, "validation": bad, "launches": launches // max(steps, 1), "stages": stages,

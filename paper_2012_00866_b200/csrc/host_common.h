@@ -39,9 +39,12 @@ inline bool domain_violation(int c, uint32_t viol) {
 int device_sm_count();
 
 // The single-GPU path (husky_sort) -- also the local phase of the sample sort.
+// allow_graph: replay a cached CUDA graph of the launch sequence when the
+// same call repeats (husky.cu); the sample sort's local sorts pass false
+// (fresh receive buffers every call would only fill the cache).
 husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
                        uint32_t *d_perm, void *d_sorted_units, int64_t *d_sorted_offsets, void *d_ws,
-                       size_t ws_bytes, husky_outcome *h_out, cudaStream_t s);
+                       size_t ws_bytes, husky_outcome *h_out, cudaStream_t s, bool allow_graph = true);
 
 // --------------------------------------------------------------- Sorter
 // One husky_sort invocation: owns the epoch / tile-counter bookkeeping.

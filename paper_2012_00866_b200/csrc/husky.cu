@@ -12,7 +12,9 @@
 // (A6) add one synchronisation per refinement round.
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <atomic>
 #include <thread>
@@ -140,13 +142,203 @@ static bool alpha_env() {
   return !(e && e[0] == '0');
 }
 
+// What one sort enqueues before its single synchronisation (decided on the
+// host from the arguments and the environment; part of the graph cache key).
+struct MainFlags {
+  int coder = 0, kc = 0;
+  bool packed = false, compress = false, slab = false, pdl = true;
+};
+
+// Everything from the DevState reset to the copy of DevState into h_state
+// (pinned when captured into a graph): encode, histograms + plan, the 8 pass
+// slots, the gather with run detection, classification and the small / medium
+// fix-ups.  Enqueued on S.s; no host synchronisation inside.
+static husky_status enqueue_main(Sorter &S, const MainFlags &F, void *d_sorted_units, int64_t *d_sorted_offsets,
+                                 DevState *h_state) {
+  const Layout &L = S.L;
+  DevState *st = S.st;
+  cudaStream_t s = S.s;
+  const uint64_t n = S.n;
+  const int coder = F.coder, kc = F.kc;
+  const void *d_units = S.units;
+  const int64_t *d_offsets = S.offsets;
+  uint32_t *d_perm = S.perm;
+  HCHECK(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+  HCHECK(S.reset_lookback());
+  // the dirty-run flags the main gather sets (cleared here, not between the key
+  // sort and the gather, so the gather stays a programmatic dependent)
+  HCHECK(cudaMemsetAsync(S.at<uint8_t>(L.dirty), 0, L.cap_sm, s));
+
+  // ---- A1 encode (+ flags, alphabet, slab records) and the digit histograms
+  // n <= 2^28: the payload carries min(len, 15) in its top 4 bits, so the
+  // gather rebuilds strings of length <= PL from their code (no random reads)
+  uint32_t *packed_payload = F.packed ? S.at<uint32_t>(L.vals2) : nullptr;
+  uint4 *slab = F.slab ? S.at<uint4>(L.slab) : nullptr;
+  uint64_t *keysA = S.keysA(), *keysB = S.keysB();
+  uint32_t *vals_tmp = S.at<uint32_t>(L.vals);
+  {
+    GroupScope grp(ST_ENCODE, s);
+    launch_encode(coder, d_units, d_offsets, n, S.keysA(), &st->violations, S.sms, s, packed_payload, slab,
+                  !F.packed, F.compress ? st->alpha : nullptr);
+  }
+  launch_hist_plan(keysA, n, st, keysA, keysB, S.sms, s, F.compress);
+
+  // ---- A2 key sort, LSD onesweep: (code, index) -> sorted codes, perm.  The
+  // pass plan (which digits are not shared by all keys) is made on device, so
+  // the host enqueues all 8 pass slots without waiting; slots beyond the plan
+  // exit at once.  Input violations (bad offsets, ASCII domain) make every
+  // later kernel a no-op and are reported at the single synchronisation.
+  {
+    GroupScope grp(ST_RADIX, s);  // profiler mode 2: the 8 pass slots as one timed group
+    for (int slot = 0; slot < 8; ++slot)
+      launch_onesweep_slot(slot, keysA, keysB, packed_payload, d_perm, vals_tmp, n, st, S.lb_radix(),
+                           S.next_counter(), S.next_epoch(), s);
+  }
+  launch_radix_finalize(st, packed_payload, d_perm, n, s);
+  if (F.packed && !d_sorted_units) launch_unpack_perm(d_perm, n, s);  // the gather unpacks otherwise
+
+  // ---- A4 gather in (code, index) order.  Done BEFORE the fix-up: the order
+  // check below then reads every run's strings contiguously instead of through
+  // a second random perm -> offsets -> units walk; only spans the fix-up
+  // reorders are gathered again (rare outside all-colliding inputs).
+  // A3 is fused into this gather: run detection and the order check of every
+  // adjacent equal-code pair on the strings it stages (perm-only mode runs the
+  // separate run scan below instead).
+  uint32_t *run_start = S.at<uint32_t>(L.run_start), *run_end = S.at<uint32_t>(L.run_end);
+  uint8_t *dirty = S.at<uint8_t>(L.dirty);
+  if (d_sorted_units) {
+    GroupScope grp(ST_GATHER, s);
+    GatherRunsOut ro{run_start, run_end, dirty, S.lb_scan2(), st};
+    launch_gather(kc, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),
+                  S.next_counter(), S.next_epoch(), s, nullptr, F.packed, nullptr, st, &ro, slab);
+  }
+  debug_check_perm(d_perm, n, "key sort", s);
+
+  // ---- A3 run detection + order check (keys: DevState::sorted_keys), classification
+  uint2 *list_sm = S.at<uint2>(L.list_sm), *list_g = S.at<uint2>(L.list_g);
+  if (!d_sorted_units)
+    launch_runs_scan(kc, 0, nullptr, n, d_perm, d_units, d_offsets, 0, run_start, run_end, dirty, st,
+                     S.lb_scan(), S.next_counter(), S.next_epoch(), s);
+  launch_runs_classify(run_start, run_end, dirty, st, list_sm, L.cap_sm, list_g, true, S.sms, s);
+
+  // ---- A5 fix-up of small / medium dirty runs (counts read on device), then
+  // A4 again for the spans it reordered.  Enqueued optimistically before the
+  // host knows whether there are giant runs: giant runs are disjoint from the
+  // small/medium ones, so their refinement only appends list entries.
+  launch_fix_small(kc, list_sm, st, d_perm, d_units, d_offsets, S.sms, s);
+  launch_fix_medium(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s);
+  if (d_sorted_units)
+    launch_regather_runs(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, d_sorted_units,
+                         d_sorted_offsets, S.sms, s);
+  HCHECK(cudaMemcpyAsync(h_state, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  return HUSKY_OK;
+}
+
+// ------------------------------------------------------------- CUDA graphs
+// A sort's launch sequence up to its synchronisation depends only on the
+// arguments (buffers, n, coder, flags), so it is captured once into a CUDA
+// graph and replayed when the same call repeats: one cudaGraphLaunch instead
+// of ~15 launches and memsets (small sorts are launch-bound: C1's 1e5 strings
+// move ~26 MB, 4 us at HBM speed).  Captured on a library stream, launched on
+// the caller's; the DevState copy lands in a pinned buffer of the entry.
+// Off while profiling (per-launch events), with HUSKY_DEBUG_SYNC, and with
+// HUSKY_GRAPH=0.  LRU of kGraphCache entries per process.
+struct GraphKey {
+  int dev, coder, packed, compress, slab, pdl;
+  const void *units, *offsets, *perm, *su, *so, *ws;
+  uint64_t n;
+  size_t ws_bytes;
+  bool operator==(const GraphKey &o) const { return memcmp(this, &o, sizeof *this) == 0; }
+};
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec = nullptr;
+  DevState *h_state = nullptr;  // pinned
+  uint32_t epoch = 0, slot = 0;
+  uint64_t launches = 0, last_use = 0;
+};
+constexpr int kGraphCache = 16;
+static std::mutex g_graph_mu;
+static std::vector<GraphEntry> g_graphs;
+static uint64_t g_graph_clock = 0;
+
+static bool graphs_enabled() {
+  const char *e = getenv("HUSKY_GRAPH");
+  return !(e && e[0] == '0');
+}
+
+static cudaStream_t capture_stream(int dev) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  std::lock_guard<std::mutex> g(mu);
+  if (!streams[dev & 63]) cudaStreamCreateWithFlags(&streams[dev & 63], cudaStreamNonBlocking);
+  return streams[dev & 63];
+}
+
+static void free_entry(GraphEntry &e) {
+  if (e.exec) cudaGraphExecDestroy(e.exec);
+  if (e.h_state) cudaFreeHost(e.h_state);
+  e.exec = nullptr;
+  e.h_state = nullptr;
+}
+
+// the cached entry for `key`, captured now if absent (nullptr on failure:
+// the caller falls back to direct launches)
+static GraphEntry *graph_for(const GraphKey &key, Sorter &S, const MainFlags &F, void *su, int64_t *so) {
+  std::lock_guard<std::mutex> g(g_graph_mu);
+  for (auto &e : g_graphs)
+    if (e.key == key) {
+      e.last_use = ++g_graph_clock;
+      return &e;
+    }
+  GraphEntry e;
+  e.key = key;
+  if (cudaMallocHost(&e.h_state, sizeof(DevState)) != cudaSuccess) return nullptr;
+  cudaStream_t cs = capture_stream(key.dev);
+  Sorter C = S;  // capture with a copy: the epoch / slot bookkeeping it ends with is the entry's
+  C.s = cs;
+  Profiler &P = profiler();
+  uint64_t l0;
+  {
+    std::lock_guard<std::mutex> pg(P.mu);
+    l0 = P.total_launches;
+  }
+  cudaGraph_t graph = nullptr;
+  bool ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+  husky_status st = ok ? enqueue_main(C, F, su, so, e.h_state) : HUSKY_ERR_CUDA;
+  const bool ended = ok && cudaStreamEndCapture(cs, &graph) == cudaSuccess;
+  ok = ok && st == HUSKY_OK && ended && graph && C.err == cudaSuccess &&
+       cudaGraphInstantiate(&e.exec, graph, 0) == cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  cudaGetLastError();  // a failed capture leaves no sticky error; clear the last one
+  {
+    std::lock_guard<std::mutex> pg(P.mu);
+    e.launches = P.total_launches - l0;
+    P.total_launches = l0;  // counted again per replay
+  }
+  if (!ok) {
+    free_entry(e);
+    return nullptr;
+  }
+  e.epoch = C.epoch;
+  e.slot = C.slot;
+  e.last_use = ++g_graph_clock;
+  if ((int)g_graphs.size() >= kGraphCache) {
+    auto victim = std::min_element(g_graphs.begin(), g_graphs.end(),
+                                   [](const GraphEntry &a, const GraphEntry &b) { return a.last_use < b.last_use; });
+    free_entry(*victim);
+    *victim = e;
+    return &*victim;
+  }
+  g_graphs.push_back(e);
+  return &g_graphs.back();
+}
+
 husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
                        uint32_t *d_perm, void *d_sorted_units, int64_t *d_sorted_offsets, void *d_ws,
-                       size_t ws_bytes, husky_outcome *h_out, cudaStream_t s) {
+                       size_t ws_bytes, husky_outcome *h_out, cudaStream_t s, bool allow_graph) {
   if (h_out) memset(h_out, 0, sizeof *h_out);
   if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
-  // byte coders share the ASCII instantiation of every kernel but the encoder
-  const int kc = kernel_coder(coder);
   if (n >= 0xFFFFFFFFull) return fail(HUSKY_ERR_INVALID_ARG, "n = %llu >= 2^32 - 1", (unsigned long long)n);
   if ((d_sorted_units == nullptr) != (d_sorted_offsets == nullptr))
     return fail(HUSKY_ERR_INVALID_ARG, "d_sorted_units and d_sorted_offsets must both be set or both NULL");
@@ -164,7 +356,8 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
     return fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, L.total);
 
   Sorter S;
-  S.coder = kc;
+  // byte coders share the ASCII instantiation of every kernel but the encoder
+  S.coder = kernel_coder(coder);
   S.units = d_units;
   S.offsets = d_offsets;
   S.n = n;
@@ -176,18 +369,13 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   S.st = S.at<DevState>(L.state);
   DevState *st = S.st;
 
-  HCHECK(cudaMemsetAsync(st, 0, sizeof(DevState), s));
-  HCHECK(S.reset_lookback());
-  // the dirty-run flags the main gather sets (cleared here, not between the key
-  // sort and the gather, so the gather stays a programmatic dependent)
-  HCHECK(cudaMemsetAsync(S.at<uint8_t>(L.dirty), 0, L.cap_sm, s));
-
-  // ---- A1 encode (+ digit histograms, flags) and the histogram scan
-  // n <= 2^28: the payload carries min(len, 15) in its top 4 bits, so the
-  // gather rebuilds strings of length <= PL from their code (no random reads)
+  MainFlags F;
+  F.coder = coder;
+  F.kc = kernel_coder(coder);
   // the gather rebuilds short strings from ASCII / UNICODE codes only
-  const bool packed = n <= kPackMaxN && (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE);
-  uint32_t *packed_payload = packed ? S.at<uint32_t>(L.vals2) : nullptr;
+  F.packed = n <= kPackMaxN && (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE);
+  // alphabet compression of the sort's private keys (ASCII; HUSKY_ALPHA=0 off)
+  F.compress = coder == HUSKY_CODER_ASCII && alpha_env();
   // slab records (ASCII / UNICODE) when sorted strings are produced and the
   // gather's random reads would miss L2: n > kSlabMinN strings (the offsets
   // alone then span >= 2x the 126 MB L2).  Every string's record when n > 2^28
@@ -195,73 +383,51 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   // random reads mostly hit L2 and the records cost more than they save (C2:
   // encode 76 -> 119 us, gather 276 -> 332 us with them).  HUSKY_SLAB=1 / 0
   // forces them on / off (tests).
-  // alphabet compression of the sort's private keys (ASCII; HUSKY_ALPHA=0 off)
-  const bool compress = coder == HUSKY_CODER_ASCII && alpha_env();
-  uint4 *slab = nullptr;
-  if (d_sorted_units && (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE) &&
-      ((n > kSlabMinN && slab_env() != 0) || slab_env() == 1))
-    slab = S.at<uint4>(L.slab);
-  uint64_t *keysA = S.keysA(), *keysB = S.keysB();
-  uint32_t *vals_tmp = S.at<uint32_t>(L.vals);
-  {
-    GroupScope grp(ST_ENCODE, s);
-    launch_encode(coder, d_units, d_offsets, n, S.keysA(), &st->violations, S.sms, s, packed_payload, slab,
-                  !packed, compress ? st->alpha : nullptr);
+  F.slab = d_sorted_units && (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE) &&
+           ((n > kSlabMinN && slab_env() != 0) || slab_env() == 1);
+  F.pdl = pdl_enabled();
+
+  DevState hs_local;
+  const DevState *hs_src = &hs_local;
+  GraphEntry *ge = nullptr;
+  if (allow_graph && graphs_enabled() && !debug_sync() && profiler().on == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    GraphKey key;
+    memset(&key, 0, sizeof key);
+    key.dev = dev;
+    key.coder = coder;
+    key.packed = F.packed;
+    key.compress = F.compress;
+    key.slab = F.slab;
+    key.pdl = F.pdl;
+    key.units = d_units;
+    key.offsets = d_offsets;
+    key.perm = d_perm;
+    key.su = d_sorted_units;
+    key.so = d_sorted_offsets;
+    key.ws = d_ws;
+    key.n = n;
+    key.ws_bytes = ws_bytes;
+    ge = graph_for(key, S, F, d_sorted_units, d_sorted_offsets);
   }
-  launch_hist_plan(keysA, n, st, keysA, keysB, S.sms, s, compress);
-
-  // ---- A2 key sort, LSD onesweep: (code, index) -> sorted codes, perm.  The
-  // pass plan (which digits are not shared by all keys) is made on device, so
-  // the host enqueues all 8 pass slots without waiting; slots beyond the plan
-  // exit at once.  Input violations (bad offsets, ASCII domain) make every
-  // later kernel a no-op and are reported at the single synchronisation below.
-  {
-    GroupScope grp(ST_RADIX, s);  // profiler mode 2: the 8 pass slots as one timed group
-    for (int slot = 0; slot < 8; ++slot)
-      launch_onesweep_slot(slot, keysA, keysB, packed_payload, d_perm, vals_tmp, n, st, S.lb_radix(),
-                           S.next_counter(), S.next_epoch(), s);
+  if (ge) {
+    HCHECK(cudaGraphLaunch(ge->exec, s));
+    S.epoch = ge->epoch;
+    S.slot = ge->slot;
+    {
+      Profiler &P = profiler();
+      std::lock_guard<std::mutex> pg(P.mu);
+      P.total_launches += ge->launches;
+    }
+    hs_src = ge->h_state;
+  } else {
+    if (husky_status e = enqueue_main(S, F, d_sorted_units, d_sorted_offsets, &hs_local)) return e;
   }
-  launch_radix_finalize(st, packed_payload, d_perm, n, s);
-  if (packed && !d_sorted_units) launch_unpack_perm(d_perm, n, s);  // the gather unpacks otherwise
-
-  // ---- A4 gather in (code, index) order.  Done BEFORE the fix-up: the order
-  // check below then reads every run's strings contiguously instead of through
-  // a second random perm -> offsets -> units walk; only spans the fix-up
-  // reorders are gathered again (rare outside all-colliding inputs).
-  // A3 is fused into this gather: run detection and the order check of every
-  // adjacent equal-code pair on the strings it stages (perm-only mode runs the
-  // separate run scan below instead).
-  uint32_t *run_start = S.at<uint32_t>(L.run_start), *run_end = S.at<uint32_t>(L.run_end);
-  uint8_t *dirty = S.at<uint8_t>(L.dirty);  // zeroed with the DevState at the start
-  if (d_sorted_units) {
-    GroupScope grp(ST_GATHER, s);
-    GatherRunsOut ro{run_start, run_end, dirty, S.lb_scan2(), st};
-    launch_gather(kc, d_perm, n, d_units, d_offsets, d_sorted_units, d_sorted_offsets, S.lb_scan(),
-                  S.next_counter(), S.next_epoch(), s, nullptr, packed, nullptr, st, &ro, slab);
-  }
-  debug_check_perm(d_perm, n, "key sort", s);
-
-  // ---- A3 run detection + order check (keys: DevState::sorted_keys), classification
-  uint2 *list_sm = S.at<uint2>(L.list_sm), *list_g = S.at<uint2>(L.list_g);
-  if (!d_sorted_units)
-    launch_runs_scan(kc, 0, nullptr, n, d_perm, d_units, d_offsets, 0, run_start, run_end, dirty, st,
-                     S.lb_scan(), S.next_counter(), S.next_epoch(), s);
-  launch_runs_classify(run_start, run_end, dirty, st, list_sm, L.cap_sm, list_g, true, S.sms, s);
-
-  // ---- A5 fix-up of small / medium dirty runs (counts read on device), then
-  // A4 again for the spans it reordered.  Enqueued optimistically before the
-  // host knows whether there are giant runs: giant runs are disjoint from the
-  // small/medium ones, so their refinement below only appends list entries.
-  launch_fix_small(kc, list_sm, st, d_perm, d_units, d_offsets, S.sms, s);
-  launch_fix_medium(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s);
-  if (d_sorted_units)
-    launch_regather_runs(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, d_sorted_units,
-                         d_sorted_offsets, S.sms, s);
-  DevState hs;
-  HCHECK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, s));
   HCHECK(cudaStreamSynchronize(s));
   if (husky_status e = cuda_check("sort")) return e;
   HCHECK(S.err);
+  DevState hs = *hs_src;
   if (hs.violations & kOffsetsBad) return fail(HUSKY_ERR_INVALID_ARG, "offsets are not non-decreasing");
   S.radix_passes = hs.np;
   debug_check_perm(d_perm, n, "fix-up", s);

@@ -544,7 +544,7 @@ struct Plan {
     }
     if (husky_status e = sort_impl(coder, at<void>(M.smp_units), at<int64_t>(M.smp_offsets), m,
                                    at<uint32_t>(M.smp_perm), nullptr, nullptr, at<void>(M.smp_ws),
-                                   make_layout(m).total, nullptr, s))
+                                   make_layout(m).total, nullptr, s, false))
       return e;
     HUSKY_SCOPE(ST_MULTI, s, 0);
     k_pick_splitters<<<1, 256, 0, s>>>(recs, rk, m, at<uint32_t>(M.smp_perm), world, split);
@@ -681,7 +681,7 @@ struct Plan {
     }
     husky_status e = sort_impl(coder, r_units, (const int64_t *)(rws + R.offsets), n_out, d_perm_out,
                                d_sorted_units_out, d_sorted_offsets_out, rws + R.sort_ws,
-                               make_layout(n_out).total, h_out, s);
+                               make_layout(n_out).total, h_out, s, false);
     if (e) return e;
     HUSKY_SCOPE(ST_MULTI, s, 0);
     k_remap<<<grid_for(n_out), 256, 0, s>>>(d_perm_out, n_out, r_gidx);

@@ -6,6 +6,7 @@
 // nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/rand_probe2 tools/rand_probe2.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint64_t mix(uint64_t x) {
@@ -77,7 +78,17 @@ __global__ void k_bulk(const uint8_t *buf, uint64_t blocks, uint64_t nblocks_tot
   if (acc == 42) atomicAdd(sink, acc);
 }
 
-int main() {
+int main(int argc, char **argv) {
+  if (argc > 1) {
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(argv[1]));
+    size_t v = 0;
+    cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+    printf("cudaLimitMaxL2FetchGranularity set %s -> %zu\n", cudaGetErrorString(e), v);
+  } else {
+    size_t v = 0;
+    cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+    printf("cudaLimitMaxL2FetchGranularity default %zu\n", v);
+  }
   const uint64_t bytes = 16ull << 30;
   uint8_t *buf;
   cudaMalloc(&buf, bytes);
