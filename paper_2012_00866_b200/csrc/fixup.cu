@@ -5,23 +5,297 @@
 // 433), relying on there being "very few inversions" left.
 // Because every remaining inversion is inside an equal-code run (R6),
 // only dirty runs are re-sorted here, each independently:
-//   small  (<= 32 strings): one warp; every lane owns a string and computes its
-//          rank with the exact comparator against all others (rank sort);
-//   medium (<= 4096): one CTA, bitonic sort of indices in shared memory;
+//   staged (the main pass, sorted strings present, run <= 4096 strings and
+//          <= kFixStageBytes of units): one CTA per run.  The run's strings are
+//          contiguous after the gather, so they are staged into shared memory
+//          with ONE bulk async copy (cp.async.bulk, the TMA engine) completing
+//          on an mbarrier; each string gets a 48-bit big-endian key of its
+//          units after the S that equal codes already fix (+ its 16-bit slot),
+//          and the CTA merge-sorts those items (cub::BlockMergeSort, 512
+//          threads x 8) with a comparator that falls back to a full compare of
+//          the staged units only on equal keys (a bitonic network measured
+//          2.8 ms on 2^23 D1 strings: too many barrier-separated stages).  The sorted run
+//          is written back in place -- perm, sorted offsets and sorted units --
+//          so no re-gather follows.
+//   small  (<= 32 strings, others): one warp; every lane owns a string and
+//          computes its rank with the exact comparator (rank sort);
+//   medium (<= 4096, others): one CTA, bitonic sort of indices in shared memory
+//          with global-memory comparisons (refinement sub-runs, perm-only mode,
+//          runs whose units exceed the stage);
 //   giant  (> 4096): refinement rounds (host loop in husky.cu): the run is
 //          re-keyed from its common prefix (k_seg_prep / k_seg_key2) and sorted
 //          with the onesweep radix; sub-runs that are still ambiguous go round
 //          again or drop into the small/medium lists.
 // All comparisons use the exact comparator (units, length, original index).
+#include <cub/block/block_merge_sort.cuh>
+
 #include "husky_internal.cuh"
 #include "kernels.cuh"
 
 namespace husky {
 
+// A run the staged kernel handled (main pass only: so != NULL): the other
+// fix-up kernels and the re-gather skip it.  Not when every code was equal:
+// the gather then left the sorted offsets inside the one run unwritten (the
+// run is refined and gathered again), so nothing is staged.
+template <int W>
+__device__ __forceinline__ bool staged_run(const DevState *st, const int64_t *so, uint32_t start, uint32_t len) {
+  return so != nullptr && st->trivial_mask != 0xFFu &&
+         (uint64_t)(so[start + len] - so[start]) * W <= (uint64_t)kFixStageBytes;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(a), "r"(phase)
+                 : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+constexpr int kFixThreads = 1024, kFixItems = kMediumMax / kFixThreads;  // 4 strings per thread
+// dynamic shared memory of k_fix_staged: the stage (+16 B of alignment slack +
+// read slack), per string: offset in the stage (n + 1 entries: lengths are
+// differences) and global index; then the output image (the run's bytes in
+// the new order)
+constexpr int kFixArrBytes = ((kMediumMax + 1) * 4 + kMediumMax * 4 + 15) / 16 * 16;
+constexpr int kFixSmem = kFixStageBytes + 32 + kFixArrBytes + kFixStageBytes + 32;
+
+// Order of two sort items of a staged run: item = (top 48 bits of the 8-byte
+// big-endian key of the string's units from byte kstart) << 16 | slot.
+// Equal 48-bit prefixes fall back to the full comparison of the staged units
+// from byte kstart + 6, then the lengths, then the original indices; slot
+// 0xFFFF is padding (after everything).
+struct FixLess {
+  const uint8_t *stage;
+  const uint32_t *soff, *sgid;  // string i: stage bytes [soff[i], soff[i + 1])
+  uint32_t kstart, w;
+  __device__ __forceinline__ bool operator()(const uint64_t &a, const uint64_t &b) const {
+    const uint32_t sa = (uint32_t)(a & 0xFFFFu), sb = (uint32_t)(b & 0xFFFFu);
+    if (sa == 0xFFFFu || sb == 0xFFFFu) return sb == 0xFFFFu && sa != 0xFFFFu;
+    if ((a >> 16) != (b >> 16)) return (a >> 16) < (b >> 16);
+    if (sa == sb) return false;
+    const uint32_t la = soff[sa + 1] - soff[sa], lb = soff[sb + 1] - soff[sb], m = la < lb ? la : lb;
+    for (uint32_t k = kstart + 6; k < m; k += 8) {
+      uint64_t x = stage_load8(stage, soff[sa] + k), y = stage_load8(stage, soff[sb] + k);
+      const uint32_t take = m - k < 8 ? m - k : 8;
+      if (take < 8) {
+        const uint64_t msk = (1ull << (8 * take)) - 1;
+        x &= msk;
+        y &= msk;
+      }
+      const uint64_t d = x ^ y;
+      if (d) {
+        const int sh = ((__ffsll((long long)d) - 1) / (8 * w)) * (8 * w);
+        const uint64_t um = w == 1 ? 0xFFull : 0xFFFFull;
+        return ((x >> sh) & um) < ((y >> sh) & um);
+      }
+    }
+    if (la != lb) return la < lb;
+    return sgid[sa] < sgid[sb];
+  }
+};
+
+#ifdef HUSKY_FIX_TIMING
+// lab builds: per-CTA cycles spent in each phase of k_fix_staged (stage, keys,
+// sort, write-back), summed over its runs
+__device__ unsigned long long g_fix_phase[1024][4];
+#define FT(i) do { if (threadIdx.x == 0) { const long long t_ = clock64(); g_fix_phase[blockIdx.x][i] += t_ - ft_last; ft_last = t_; } } while (0)
+#else
+#define FT(i) do { } while (0)
+#endif
+
+template <int CODER>
+__global__ void __launch_bounds__(kFixThreads, 1)
+    k_fix_staged(const uint2 *__restrict__ list, uint64_t cap, const DevState *st, uint32_t *perm,
+                 uint8_t *__restrict__ su, int64_t *__restrict__ so) {
+  using T = CoderTraits<CODER>;
+  constexpr int W = T::kUnitBytes;
+  using Sort = cub::BlockMergeSort<uint64_t, kFixThreads, kFixItems>;
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint8_t *stage = sm;
+  uint32_t *soff = reinterpret_cast<uint32_t *>(sm + kFixStageBytes + 32);
+  uint32_t *sgid = soff + kMediumMax + 1;
+  __shared__ typename Sort::TempStorage sort_tmp;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t s_wt[kFixThreads / 32 + 1];
+  pdl_wait();
+  if (st->violations & kOffsetsBad) return;
+  if (st->trivial_mask == 0xFFu) return;  // all codes equal: see staged_run
+  const bool general = st->general != 0;
+  // compare from unit S (equal codes fix units [0, S)), or from 0 off-domain
+  const uint32_t kstart = general ? 0u : (uint32_t)(T::kS * W);
+  const uint32_t ns = st->n_small, nm = st->n_medium;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the init, seen by the async proxy
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  const bool bulk_ok = ((uintptr_t)su & 15) == 0;
+  const FixLess less{stage, soff, sgid, kstart, (uint32_t)W};
+#ifdef HUSKY_FIX_TIMING
+  long long ft_last = clock64();
+#endif
+  for (uint32_t e = blockIdx.x; e < ns + nm; e += gridDim.x) {
+    const uint2 ent = e < ns ? list[e] : list[cap - 1 - (e - ns)];
+    const uint32_t start = ent.x, len = ent.y;
+    const int64_t B0u = so[start], B1u = so[start + len];
+    const uint64_t B0 = (uint64_t)B0u * W, B1 = (uint64_t)B1u * W;  // the run's bytes in su
+    if (B1 - B0 > (uint64_t)kFixStageBytes) continue;  // left to k_fix_small / k_fix_medium
+    // ---- stage: bytes [a0, B1) with a0 = B0 rounded down to 16; the aligned
+    // body by one bulk copy (TMA engine, completing on the mbarrier), the
+    // ragged tail by plain loads
+    const uint64_t a0 = bulk_ok ? (B0 & ~15ull) : B0, a1 = bulk_ok ? (B1 & ~15ull) : B0;
+    if (threadIdx.x == 0 && a1 > a0) {
+      // the previous run's generic-proxy accesses to the stage come first
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bar, (uint32_t)(a1 - a0));
+      bulk_g2s(stage, su + a0, (uint32_t)(a1 - a0), &bar);
+    }
+    for (uint64_t x = (a1 > a0 ? a1 : B0) + threadIdx.x; x < B1; x += kFixThreads) stage[x - a0] = su[x];
+    // per string: offset in the stage (n + 1 entries) / global index
+    for (uint32_t i = threadIdx.x; i <= len; i += kFixThreads) {
+      soff[i] = (uint32_t)((uint64_t)so[start + i] * W - a0);
+      if (i < len) sgid[i] = perm[start + i];
+    }
+    if (a1 > a0) mbar_wait(&bar, phase);
+    phase ^= (a1 > a0) ? 1u : 0u;
+    __syncthreads();
+    FT(0);
+    // ---- sort items, blocked: thread t holds strings 8t .. 8t + 7
+    uint64_t item[kFixItems];
+#pragma unroll
+    for (int j = 0; j < kFixItems; ++j) {
+      const uint32_t i = threadIdx.x * kFixItems + j;
+      uint64_t k = ~0ull;
+      if (i < len) {
+        const uint32_t nb = soff[i + 1] - soff[i];
+        uint64_t key = 0;
+        if (nb > kstart) {
+          const uint32_t take = nb - kstart < 8 ? nb - kstart : 8;
+          const uint64_t v = stage_load8(stage, soff[i] + kstart);  // little-endian bytes
+          const uint64_t m = take == 8 ? ~0ull : ((1ull << (8 * take)) - 1);
+          // big-endian by unit: bytes reversed (W = 1) / 16-bit units reversed (W = 2)
+          constexpr uint32_t sel = W == 1 ? 0x0123u : 0x1032u;
+          key = __byte_perm((uint32_t)((v & m) >> 32), 0, sel) |
+                ((uint64_t)__byte_perm((uint32_t)(v & m), 0, sel) << 32);
+        }
+        k = (key & ~0xFFFFull) | i;  // top 48 bits of the key, then the slot
+      }
+      item[j] = k;
+    }
+    FT(1);
+    Sort(sort_tmp).Sort(item, less);
+    __syncthreads();
+    FT(2);
+    // ---- write back in the new order: perm, offsets (scan of the lengths), units
+    uint32_t L[kFixItems], mine = 0;
+#pragma unroll
+    for (int j = 0; j < kFixItems; ++j) {
+      const uint32_t q = (uint32_t)(item[j] & 0xFFFFu);
+      L[j] = q != 0xFFFFu ? (soff[q + 1] - soff[q]) / W : 0u;
+      mine += L[j];
+    }
+    uint32_t tot;
+    uint32_t d = block_exclusive_scan<uint32_t, kFixThreads>(mine, &tot, s_wt);
+    uint32_t dq[kFixItems];  // output unit offset of each of my items
+#pragma unroll
+    for (int j = 0; j < kFixItems; ++j) {
+      const uint32_t r = threadIdx.x * kFixItems + j, q = (uint32_t)(item[j] & 0xFFFFu);
+      if (r < len) {
+        perm[start + r] = sgid[q];
+        so[start + r] = B0u + d;
+      }
+      dq[j] = d;
+      d += L[j];
+    }
+    // the units: the run's bytes in the new order are assembled in shared
+    // memory at the output's 16-byte phase (image byte x <-> su byte a0 + x,
+    // the same phase as the stage), then the aligned body leaves with ONE
+    // bulk async store (cp.async.bulk shared -> global) and the ragged edges
+    // with plain stores
+    uint8_t *image = stage + kFixStageBytes + 32 + kFixArrBytes;  // 16-byte aligned
+    const uint32_t lead = (uint32_t)(B0 - a0);
+#pragma unroll
+    for (int j = 0; j < kFixItems; ++j) {
+      const uint32_t q = (uint32_t)(item[j] & 0xFFFFu);
+      if (q == 0xFFFFu) continue;
+      const uint8_t *src = stage + soff[q];
+      uint8_t *dst = image + lead + dq[j] * W;
+      for (uint32_t b = 0; b < L[j] * W; ++b) dst[b] = src[b];
+    }
+    __syncthreads();
+    const uint64_t c0 = (B0 + 15) & ~15ull;  // first aligned output byte inside the run
+    if (bulk_ok && a1 > c0) {
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the image stores, for the async proxy
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(su + c0),
+                     "r"((uint32_t)__cvta_generic_to_shared(image + (c0 - a0))), "r"((uint32_t)(a1 - c0))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      for (uint64_t x = B0 + threadIdx.x; x < c0; x += kFixThreads) su[x] = image[x - a0];
+      for (uint64_t x = a1 + threadIdx.x; x < B1; x += kFixThreads) su[x] = image[x - a0];
+      // the image (and the stage next to it) may be rewritten only after the
+      // bulk store has read it
+      if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    } else {
+      for (uint64_t x = B0 + threadIdx.x; x < B1; x += kFixThreads) su[x] = image[x - a0];
+    }
+    __syncthreads();  // the stage and the sort storage are reused by the next run
+    FT(3);
+  }
+}
+
+extern "C" int husky_debug_fix_phases(unsigned long long *out) {
+#ifdef HUSKY_FIX_TIMING
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_fix_phase, sizeof(g_fix_phase));
+  return 1024;
+#else
+  (void)out;
+  return 0;
+#endif
+}
+
+void launch_fix_staged(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st, uint32_t *perm,
+                       void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s) {
+  Scope sc_(ST_FIX_MEDIUM, s, 0);
+  static SmemAttr a0, a1;
+  dim3 g(num_sms), b(kFixThreads);
+  if (coder == HUSKY_CODER_ASCII) {
+    a0.ensure(k_fix_staged<HUSKY_CODER_ASCII>, kFixSmem);
+    launch_pdl(k_fix_staged<HUSKY_CODER_ASCII>, g, b, kFixSmem, s, list_sm, cap_sm, st, perm, (uint8_t *)sorted_units,
+               sorted_offsets);
+  } else {
+    a1.ensure(k_fix_staged<HUSKY_CODER_UNICODE>, kFixSmem);
+    launch_pdl(k_fix_staged<HUSKY_CODER_UNICODE>, g, b, kFixSmem, s, list_sm, cap_sm, st, perm,
+               (uint8_t *)sorted_units, sorted_offsets);
+  }
+}
+
 template <int CODER>
 __global__ void __launch_bounds__(256)
     k_fix_small(const uint2 *__restrict__ list, const DevState *st, uint32_t *perm,
-                const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t first) {
+                const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t first,
+                const int64_t *__restrict__ so) {
   using T = CoderTraits<CODER>;
   pdl_wait();
   if (st->violations & kOffsetsBad) return;
@@ -31,6 +305,7 @@ __global__ void __launch_bounds__(256)
   for (uint32_t e = first + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < nsmall; e += warps) {
     uint2 ent = list[e];
     const uint32_t start = ent.x, len = ent.y;
+    if (staged_run<T::kUnitBytes>(st, so, start, len)) continue;
     uint32_t my = lane < len ? perm[start + lane] : 0xFFFFFFFFu;
     uint32_t rank = 0;
     const bool general = st->general != 0;
@@ -50,7 +325,8 @@ __global__ void __launch_bounds__(256)
 template <int CODER>
 __global__ void __launch_bounds__(1024)
     k_fix_medium(const uint2 *__restrict__ list, uint64_t cap, const DevState *st, uint32_t *perm,
-                 const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t first) {
+                 const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t first,
+                 const int64_t *__restrict__ so) {
   using T = CoderTraits<CODER>;
   __shared__ uint32_t s[kMediumMax];
   pdl_wait();
@@ -60,6 +336,7 @@ __global__ void __launch_bounds__(1024)
   for (uint32_t e = first + blockIdx.x; e < nmed; e += gridDim.x) {
     uint2 ent = list[cap - 1 - e];
     const uint32_t start = ent.x, len = ent.y;
+    if (staged_run<T::kUnitBytes>(st, so, start, len)) continue;
 #ifdef HUSKY_TRACE
     if (threadIdx.x == 0) printf("[husky trace] fix_medium entry %u/%u: start %u len %u cap %llu\n", e, nmed, start, len,
                                  (unsigned long long)cap);
@@ -92,24 +369,27 @@ __global__ void __launch_bounds__(1024)
 }
 
 void launch_fix_small(int coder, const uint2 *list_sm, const DevState *st, uint32_t *perm,
-                      const void *units, const int64_t *offsets, int num_sms, cudaStream_t s, uint32_t first) {
+                      const void *units, const int64_t *offsets, int num_sms, cudaStream_t s, uint32_t first,
+                      const int64_t *staged_so) {
   Scope sc_(ST_FIX_SMALL, s, 0);
   dim3 g(num_sms * 4), b(256);
   if (coder == HUSKY_CODER_ASCII)
-    launch_pdl(k_fix_small<HUSKY_CODER_ASCII>, g, b, 0, s, list_sm, st, perm, units, offsets, first);
+    launch_pdl(k_fix_small<HUSKY_CODER_ASCII>, g, b, 0, s, list_sm, st, perm, units, offsets, first, staged_so);
   else
-    launch_pdl(k_fix_small<HUSKY_CODER_UNICODE>, g, b, 0, s, list_sm, st, perm, units, offsets, first);
+    launch_pdl(k_fix_small<HUSKY_CODER_UNICODE>, g, b, 0, s, list_sm, st, perm, units, offsets, first, staged_so);
 }
 
 void launch_fix_medium(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                        uint32_t *perm, const void *units, const int64_t *offsets, int num_sms,
-                       cudaStream_t s, uint32_t first) {
+                       cudaStream_t s, uint32_t first, const int64_t *staged_so) {
   Scope sc_(ST_FIX_MEDIUM, s, 0);
   dim3 g(num_sms), b(1024);
   if (coder == HUSKY_CODER_ASCII)
-    launch_pdl(k_fix_medium<HUSKY_CODER_ASCII>, g, b, 0, s, list_sm, cap_sm, st, perm, units, offsets, first);
+    launch_pdl(k_fix_medium<HUSKY_CODER_ASCII>, g, b, 0, s, list_sm, cap_sm, st, perm, units, offsets, first,
+               staged_so);
   else
-    launch_pdl(k_fix_medium<HUSKY_CODER_UNICODE>, g, b, 0, s, list_sm, cap_sm, st, perm, units, offsets, first);
+    launch_pdl(k_fix_medium<HUSKY_CODER_UNICODE>, g, b, 0, s, list_sm, cap_sm, st, perm, units, offsets, first,
+               staged_so);
 }
 
 // ------------------------------------------------------------------ A6

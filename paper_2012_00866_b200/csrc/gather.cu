@@ -600,7 +600,8 @@ __global__ void __launch_bounds__(256)
     k_regather_runs(const uint2 *__restrict__ list, uint64_t cap, const DevState *st,
                     const uint32_t *__restrict__ perm, const void *__restrict__ units,
                     const int64_t *__restrict__ offsets, void *__restrict__ sorted_units,
-                    int64_t *__restrict__ sorted_offsets, uint32_t first_small, uint32_t first_medium) {
+                    int64_t *__restrict__ sorted_offsets, uint32_t first_small, uint32_t first_medium,
+                    int skip_staged) {
   constexpr int W = CoderTraits<CODER>::kUnitBytes;
   __shared__ unsigned long long s_wt[256 / 32 + 1];
   pdl_wait();
@@ -612,6 +613,10 @@ __global__ void __launch_bounds__(256)
   for (uint32_t e = blockIdx.x; e < ns + nm; e += gridDim.x) {
     uint2 ent = e < ns ? list[first_small + e] : list[cap - 1 - (first_medium + e - ns)];
     const uint32_t start = ent.x, len = ent.y;
+    // runs k_fix_staged sorted and wrote back in place (fixup.cu)
+    if (skip_staged && st->trivial_mask != 0xFFu &&
+        (uint64_t)(sorted_offsets[start + len] - sorted_offsets[start]) * W <= (uint64_t)kFixStageBytes)
+      continue;
     const unsigned long long base = (unsigned long long)sorted_offsets[start];
     unsigned long long running = 0;
     for (uint32_t c = 0; c < len; c += 256) {
@@ -643,15 +648,15 @@ __global__ void __launch_bounds__(256)
 void launch_regather_runs(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                           const uint32_t *perm, const void *units, const int64_t *offsets,
                           void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s,
-                          uint32_t first_small, uint32_t first_medium) {
+                          uint32_t first_small, uint32_t first_medium, bool skip_staged) {
   Scope sc_(ST_FIX_SMALL, s, 0);
   dim3 g(num_sms * 4), b(256);
   if (coder == HUSKY_CODER_ASCII)
     launch_pdl(k_regather_runs<HUSKY_CODER_ASCII>, g, b, 0, s, list_sm, cap_sm, st, (const uint32_t *)perm, units,
-               offsets, sorted_units, sorted_offsets, first_small, first_medium);
+               offsets, sorted_units, sorted_offsets, first_small, first_medium, skip_staged ? 1 : 0);
   else
     launch_pdl(k_regather_runs<HUSKY_CODER_UNICODE>, g, b, 0, s, list_sm, cap_sm, st, (const uint32_t *)perm, units,
-               offsets, sorted_units, sorted_offsets, first_small, first_medium);
+               offsets, sorted_units, sorted_offsets, first_small, first_medium, skip_staged ? 1 : 0);
 }
 
 }  // namespace husky

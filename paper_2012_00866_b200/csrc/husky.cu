@@ -225,11 +225,16 @@ static husky_status enqueue_main(Sorter &S, const MainFlags &F, void *d_sorted_u
   // A4 again for the spans it reordered.  Enqueued optimistically before the
   // host knows whether there are giant runs: giant runs are disjoint from the
   // small/medium ones, so their refinement only appends list entries.
-  launch_fix_small(kc, list_sm, st, d_perm, d_units, d_offsets, S.sms, s);
-  launch_fix_medium(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s);
+  // with sorted strings, runs whose units fit the stage are sorted in shared
+  // memory and written back in place (k_fix_staged); the others (and perm-only
+  // mode) take the global-memory kernels and the re-gather
+  if (d_sorted_units)
+    launch_fix_staged(kc, list_sm, L.cap_sm, st, d_perm, d_sorted_units, d_sorted_offsets, S.sms, s);
+  launch_fix_small(kc, list_sm, st, d_perm, d_units, d_offsets, S.sms, s, 0, d_sorted_offsets);
+  launch_fix_medium(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s, 0, d_sorted_offsets);
   if (d_sorted_units)
     launch_regather_runs(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, d_sorted_units,
-                         d_sorted_offsets, S.sms, s);
+                         d_sorted_offsets, S.sms, s, 0, 0, true);
   HCHECK(cudaMemcpyAsync(h_state, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   return HUSKY_OK;
 }

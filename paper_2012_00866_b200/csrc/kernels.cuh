@@ -104,11 +104,19 @@ void launch_runs_classify(const uint32_t *run_start, const uint32_t *run_end, co
 
 // A5 fix-up of dirty runs (lists filled by classify; counts read on device)
 // entries [first, count) of each list (first > 0: the round after a refinement)
+// staged: the main pass with sorted strings -- every small / medium run whose
+// units fit kFixStageBytes is sorted in shared memory and written back in
+// place (fixup.cu); the other kernels and the re-gather then skip those runs
+// (staged_so = the sorted offsets), else they take every run (staged_so NULL).
+constexpr int kFixStageBytes = 80 * 1024;
+void launch_fix_staged(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st, uint32_t *perm,
+                       void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s);
 void launch_fix_small(int coder, const uint2 *list_sm, const DevState *st, uint32_t *perm,
-                      const void *units, const int64_t *offsets, int num_sms, cudaStream_t s, uint32_t first = 0);
+                      const void *units, const int64_t *offsets, int num_sms, cudaStream_t s, uint32_t first = 0,
+                      const int64_t *staged_so = nullptr);
 void launch_fix_medium(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                        uint32_t *perm, const void *units, const int64_t *offsets, int num_sms,
-                       cudaStream_t s, uint32_t first = 0);
+                       cudaStream_t s, uint32_t first = 0, const int64_t *staged_so = nullptr);
 
 // A6 giant-run refinement
 void launch_seg_prep(int coder, const uint32_t *perm_seg, uint64_t len, const void *units,
@@ -161,7 +169,7 @@ void launch_unpack_perm(uint32_t *perm, uint64_t n, cudaStream_t s);
 void launch_regather_runs(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                           const uint32_t *perm, const void *units, const int64_t *offsets,
                           void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s,
-                          uint32_t first_small = 0, uint32_t first_medium = 0);
+                          uint32_t first_small = 0, uint32_t first_medium = 0, bool skip_staged = false);
 
 // Programmatic dependent launch (PDL): the kernel's CTAs may become resident
 // while the previous kernel in the stream drains; the kernel must execute

@@ -634,3 +634,31 @@ def test_graph_off_matches(torch, h, oracle_mod, monkeypatch):
     monkeypatch.setenv("HUSKY_GRAPH", "0")
     b = run_sort(torch, h, w)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+# ------------------------------------------------ staged fix-up (A5, fixup.cu)
+@pytest.mark.parametrize("coder,gmax,smax", [(ASCII, 4096, 10), (ASCII, 32, 6), (UNICODE, 4096, 8),
+                                             (ASCII, 4096, 40), (UNICODE, 2000, 40)])
+def test_staged_fixup_dirty_runs(torch, h, oracle_mod, coder, gmax, smax):
+    """D1-shaped input: many equal-code runs of 100..gmax strings, all dirty.
+    Runs whose units fit the 96 KB stage are sorted in shared memory from one
+    bulk copy and written back in place; longer ones (suffixes up to 40 units:
+    4096 x 52 B > 96 KB) take the global-memory kernels + re-gather.  Bit-exact
+    against the oracle either way."""
+    w = W.d1(150_000, group_min=min(100, gmax), group_max=gmax, suffix_max=smax, coder=coder)
+    outc = check_against_oracle(torch, h, oracle_mod, w)
+    assert outc["runs_by_class"][0] < outc["n_runs"]  # the runs were dirty
+
+
+def test_staged_fixup_ties_nul_and_prefixes(torch, h, oracle_mod):
+    """Runs whose strings tie on the 8-byte key: shared suffix prefixes, NUL
+    units, proper prefixes, exact duplicates (index tie-break)."""
+    rng = np.random.default_rng(91)
+    strings = []
+    for i in range(60_000):
+        g = i % 37  # 37 runs of ~1600 strings: a distinct 9-unit prefix (code) each
+        tail = [0x61 + g % 3] * int(rng.integers(0, 12)) + rng.integers(0, 3, size=int(rng.integers(0, 4))).tolist()
+        strings.append([0x61 + g // 26, 0x61 + g % 26] + [0x61] * 7 + tail)
+    perm = rng.permutation(len(strings))
+    w = W.from_strings([strings[p] for p in perm], ASCII)
+    check_against_oracle(torch, h, oracle_mod, w)

@@ -89,3 +89,16 @@ def test_c5_blocks_of_one_dataset(base, n):
     o = whole.offsets
     assert np.array_equal(blk.units, whole.units[o[base]:o[base + n]])
     assert np.array_equal(blk.offsets, o[base:base + n + 1] - o[base])
+
+
+def test_d1_groups():
+    """D1: every group is one equal-code run (shared 12-unit prefix), shuffled."""
+    w = W.d1(50_000, group_min=100, group_max=4096)
+    L = _lens(w)
+    assert L.min() >= 13 and L.max() <= 22 and w.n == 50_000
+    pre = {}
+    for i in range(w.n):
+        p = w.units[w.offsets[i]:w.offsets[i] + 12].tobytes()
+        pre[p] = pre.get(p, 0) + 1
+    assert len(pre) == w.meta["groups"]
+    assert all(c <= 4096 for c in pre.values()) and sum(c < 100 for c in pre.values()) <= 1  # the last group is cut

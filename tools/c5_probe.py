@@ -36,6 +36,8 @@ def main():
         u = torch.from_numpy(np.concatenate([uu, np.zeros(16, uu.dtype)])).cuda()
         o = torch.from_numpy(w.offsets).cuda()
     coder = 1 if cfg == "C3" else 0
+    if cfg != "C5":
+        coder = w.coder
     torch.cuda.synchronize()
     gen_s = time.time() - t0
     total = int(o[-1].item())

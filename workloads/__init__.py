@@ -27,7 +27,7 @@ ENGLISH6 = 3
 ALNUM = np.frombuffer(b"0123456789ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz", dtype=np.uint8)
 LOWER = np.frombuffer(b"abcdefghijklmnopqrstuvwxyz", dtype=np.uint8)
 
-FULL_N = {"C1": 100_000, "C2": 10_000_000, "C3": 10_000_000, "C4": 10_000_000, "C5": 1 << 30}
+FULL_N = {"C1": 100_000, "C2": 10_000_000, "C3": 10_000_000, "C4": 10_000_000, "C5": 1 << 30, "D1": 10_000_000}
 
 
 @dataclasses.dataclass
@@ -274,7 +274,39 @@ def c5(n: int = FULL_N["C5"], seed: int = MASTER_SEED + 5, base: int = 0, n_tota
                      "sorted": N // 10})
 
 
-GENERATORS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5}
+def d1(n: int = 10_000_000, seed: int = MASTER_SEED + 6, group_min: int = 100, group_max: int = 4096,
+       suffix_max: int = 10, coder: int = ASCII) -> Workload:
+    """D1 (fix-up workload, not a BASELINE config): n strings in groups of
+    U[group_min, group_max] strings; a group shares a distinct 12-unit prefix
+    (so its husky codes are all equal: one equal-code run) followed by a
+    random suffix of U[1, suffix_max] units; all strings shuffled, so nearly
+    every run is dirty and goes through the segmented fix-up (A5).  Units:
+    a-z (ASCII) or U+4E00..U+9FFF (UNICODE)."""
+    g = _rng(seed)
+    sizes = []
+    while sum(sizes) < n:
+        sizes.append(int(g.integers(group_min, group_max + 1)))
+    sizes[-1] -= sum(sizes) - n
+    ng = len(sizes)
+    lo, hi = (0x61, 0x7B) if coder != UNICODE else (0x4E00, 0xA000)
+    dt = np.uint8 if coder != UNICODE else np.uint16
+    prefixes = g.integers(lo, hi, size=(ng, 12)).astype(dt)
+    grp = np.repeat(np.arange(ng), sizes)
+    g.shuffle(grp)
+    slen = g.integers(1, suffix_max + 1, size=n)
+    lens = 12 + slen
+    off = _offsets(lens)
+    units = np.empty(int(off[-1]), dtype=dt)
+    starts = off[:-1]
+    for k in range(12):
+        units[starts + k] = prefixes[grp, k]
+    rel = np.arange(int(off[-1]), dtype=np.int64) - np.repeat(starts, lens)
+    sfx = rel >= 12
+    units[sfx] = g.integers(lo, hi, size=int(sfx.sum())).astype(dt)
+    return Workload("D1", coder, units, off, {"seed": seed, "n": n, "groups": ng})
+
+
+GENERATORS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5, "D1": d1}
 
 
 def make(name: str, n: int | None = None, seed_offset: int = 0) -> Workload:
