@@ -45,6 +45,8 @@ DESCR = {
     "C4": "C4: 1e7 ASCII strings sharing a 16-char prefix + 8 random [0-9A-Za-z] (all codes collide)",
     "C5": "C5: 2^30 ASCII strings, len U[8,24], [0-9A-Za-z], ~1% exact duplicates, first 10% pre-sorted "
           "(one dataset; block-wise counter generator)",
+    "D1": "D1 (fix-up workload, not a BASELINE config): 1e7 ASCII strings in shuffled groups of U[100,4096] "
+          "sharing a 12-char prefix (one dirty equal-code run per group) + 1..10 random a-z",
 }
 # random reads past ~2 GB are capped at ~36 G accesses/s for 16-64 B blocks
 # (profiles/r02_random_access_probe.txt): the gather's second roofline
@@ -345,7 +347,9 @@ def measure_single(args, name, n, dev, steps, warmup, flush, want_e2e, h, torch)
         e["launches_per_step"] += 1 / n_bd
     for e in stages.values():
         e["ms_per_step"] = round(e["ms_per_step"], 4)
-    passes = int(outc["radix_passes"])
+    # the main key sort's passes (refinement passes of A6 are extra and counted
+    # in outcome.radix_passes; keys_partitioned counts the main sort only)
+    passes = int(outc["keys_partitioned"]) // n if n else 0
     radix_launch_ms = [ms for st_name, el, ms in log if st_name == "radix_pass" and el == n]
     per_step = len(radix_launch_ms) // n_bd if n_bd else 0
     per_pass = [statistics.mean(radix_launch_ms[s * per_step + p] for s in range(n_bd)) for p in range(per_step)]
@@ -360,7 +364,7 @@ def measure_single(args, name, n, dev, steps, warmup, flush, want_e2e, h, torch)
     else:  # small inputs: per-kernel times from the breakdown steps
         g = {k: v["ms_per_step"] for k, v in stages.items()}
     kern = {}
-    if passes:
+    if passes and outc["refine_rounds"] == 0:
         rp = g.get("radix_pass", 0.0) / passes
         kern["radix_pass"] = kernel_entry("k_onesweep (A2 radix pass)", rp, survey["radix_pass"] * n, peak, {
             "passes_per_sort": passes,
@@ -376,7 +380,7 @@ def measure_single(args, name, n, dev, steps, warmup, flush, want_e2e, h, torch)
                               "frac": round(builder["encode"] * n / (g["encode"] * 1e-3) / 1e9 / peak, 4)}})
     if g.get("hist_scan"):
         kern["hist"] = kernel_entry("k_hist_slots (A2 digit histograms + plan)", g["hist_scan"], 8 * n, peak)
-    if g.get("gather"):
+    if g.get("gather") and outc["refine_rounds"] == 0:  # (C4: the main gather only records the one run)
         ra = gstats["random_per_string"] * n / (g["gather"] * 1e-3)
         kern["gather"] = kernel_entry("k_gather (A4 + A3)", g["gather"], survey["gather"] * n, peak, {
             "model_builder": {"bytes_alg_per_launch": int(builder["gather"] * n),
@@ -529,19 +533,38 @@ def run_single(args, h, torch, dev):
     torch.cuda.empty_cache()
     also = {}
     if not args.no_also and name == "C5":
-        r2 = measure_single(args, "C2", W.FULL_N["C2"], dev, args.steps, args.warmup, flush, False, h, torch)
-        r2.pop("perm_dev", None)
-        r2.pop("wl", None)
-        rr = r2["roofline"]
-        also["C2"] = {"workload": DESCR["C2"], "n": r2["n"], "value": round(r2["n"] / (r2["median"] * 1e-3) / 1e6, 4),
-                      "unit": UNIT, "ms_per_step": round(r2["median"], 4), "ms_min": round(r2["min"], 4),
-                      "validation": r2["validation"], "stages": r2["stages"],
-                      "roofline": {k: {"frac": v["frac"], "ms_per_launch": v["ms_per_launch"],
-                                       **({"per_pass": v["per_pass"]} if "per_pass" in v else {}),
-                                       **({"model_builder": v["model_builder"]} if "model_builder" in v else {}),
-                                       **({"random_access": v["random_access"]} if "random_access" in v else {})}
-                                   for k, v in rr.get("kernels", {}).items()},
-                      "outcome": r2["outcome"]}
+        # the other single-GPU configs (parity / structure cases of BASELINE.json)
+        # and D1, a dirty-run workload that exercises the segmented fix-up (A5)
+        for cfg in ("C2", "C3", "C4", "D1"):
+            r2 = measure_single(args, cfg, W.FULL_N[cfg], dev, max(3, args.steps // 2), args.warmup, flush, False, h,
+                                torch)
+            r2.pop("perm_dev", None)
+            wl2 = r2.pop("wl", None)
+            rr = r2["roofline"]
+            entry = {"workload": DESCR[cfg], "n": r2["n"], "value": round(r2["n"] / (r2["median"] * 1e-3) / 1e6, 4),
+                     "unit": UNIT, "ms_per_step": round(r2["median"], 4), "ms_min": round(r2["min"], 4),
+                     "validation": r2["validation"], "stages": r2["stages"],
+                     "roofline": {k: {"frac": v["frac"], "ms_per_launch": v["ms_per_launch"],
+                                      **({"per_pass": v["per_pass"]} if "per_pass" in v else {}),
+                                      **({"model_builder": v["model_builder"]} if "model_builder" in v else {}),
+                                      **({"random_access": v["random_access"]} if "random_access" in v else {})}
+                                  for k, v in rr.get("kernels", {}).items()},
+                     "outcome": r2["outcome"]}
+            fx = r2["stages"].get("fix_medium", {}).get("ms_per_step", 0.0) + \
+                r2["stages"].get("fix_small", {}).get("ms_per_step", 0.0)
+            if cfg == "D1" and fx and wl2 is not None:
+                # sum over strings in runs of (w len + 8) bytes
+                fb = r2["outcome"]["n_in_runs"] * (wl2["ub"] * wl2["stats"]["l_bar"] + 8)
+                peak, _ = peaks()
+                entry["fixup"] = {"kernels": "k_fix_staged (+ k_fix_small / k_fix_medium / k_regather_runs for runs "
+                                             "that do not fit the stage)", "ms": round(fx, 4),
+                                  "bytes_alg": int(fb), "achieved_gbs": round(fb / (fx * 1e-3) / 1e9, 1),
+                                  "frac": round(fb / (fx * 1e-3) / 1e9 / peak, 4),
+                                  "note": "the byte model is a lower bound: sorting a run of ~2000 strings costs "
+                                          "O(n log n) shared-memory comparisons, not a pass over its bytes"}
+            also[cfg] = entry
+            del wl2
+            torch.cuda.empty_cache()
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(name, min(n, args.cpu_sample))

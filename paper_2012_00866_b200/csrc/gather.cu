@@ -484,6 +484,18 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       write_window(g0, w0, w1);
     }
     GT(tile, 5);
+    if (PEER) {
+      // The peer stores (units, lengths, global indices into the destination
+      // ranks' NCCL windows over NVLink) are made visible at system scope
+      // before this CTA retires: the CTA barrier gathers every thread's
+      // stores, the system-scope fence is cumulative over them.  The host
+      // then enqueues a 1-element ncclAllReduce on the same stream, which no
+      // rank completes before every rank's gather kernel has completed, and
+      // only after it do the ranks read their windows (multi.cu: exec) -- the
+      // stores happen-before the reads across ranks.
+      __syncthreads();
+      if (tid == 0) __threadfence_system();
+    }
   } else {
     // debug path: warp-cooperative byte copy, one string at a time per warp
     for (int t = 0; t < 32; ++t) {
