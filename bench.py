@@ -391,6 +391,8 @@ def measure_single(args, name, n, dev, steps, warmup, flush, want_e2e, h, torch)
                               "peak_source": "profiles/r02_random_access_probe.txt (random 16-64 B reads "
                                              "over >= 2 GB, one B200)"},
             "strings": {k: round(v, 4) for k, v in gstats.items()}})
+    for k, v in kern.items():  # DRAM bytes per launch from the committed ncu capture (profiles/traffic.json)
+        v["traffic"] = traffic_of(name, k, n)
     total_ms = sum(v["ms_per_launch"] * (passes if k == "radix_pass" else 1) for k, v in kern.items())
     dom = max(kern, key=lambda k: kern[k]["ms_per_launch"] * (passes if k == "radix_pass" else 1)) if kern else None
     roof = dict(kern[dom]) if dom else {}

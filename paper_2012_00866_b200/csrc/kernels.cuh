@@ -46,7 +46,11 @@ void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *
 #ifndef HUSKY_RADIX_ITEMS
 #define HUSKY_RADIX_ITEMS 12
 #endif
-constexpr int kRadixThreads = 512, kRadixItems = HUSKY_RADIX_ITEMS, kRadixTile = kRadixThreads * kRadixItems;
+#ifndef HUSKY_RADIX_THREADS
+#define HUSKY_RADIX_THREADS 512
+#endif
+constexpr int kRadixThreads = HUSKY_RADIX_THREADS, kRadixItems = HUSKY_RADIX_ITEMS,
+              kRadixTile = kRadixThreads * kRadixItems;
 // Small inputs (n below kRadixSmallN) use 2048-key tiles (4 keys per thread):
 // a 1e5-string sort has 17 large tiles for 148 SMs.  Measured per C2-like sort
 // (small / large tiles): 1e5 140 / 165 us, 3e5 158 / 174, 1e6 248 / 235,

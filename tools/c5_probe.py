@@ -22,7 +22,7 @@ import workloads.gpu as G  # noqa: E402
 def main():
     lg = int(sys.argv[1]) if len(sys.argv) > 1 else 30
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-    N = 1 << lg
+    N = 1 << lg if lg <= 40 else lg  # a log2 size, or an exact n
     cfg = sys.argv[3] if len(sys.argv) > 3 else "C5"
     torch.cuda.set_device(0)
     t0 = time.time()
