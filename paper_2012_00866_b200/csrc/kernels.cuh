@@ -90,6 +90,7 @@ void launch_radix_finalize(const DevState *st, const uint32_t *vals_init, uint32
 
 struct Sorter;
 
+
 // A3 run detection (single-pass scan with decoupled look-back)
 constexpr int kScanThreads = 512, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
 // padded smem staging size of k_runs_scan (one pad u64 every 8)
