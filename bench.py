@@ -464,44 +464,27 @@ def e2e_single(h, torch, wl, steps, warmup, dev):
     d2h = n * 4 + total * ub + (n + 1) * 8
     wl["units"] = wl["offsets"] = None
     torch.cuda.empty_cache()
-    if n <= PACK_MAX_N:
-        # pipelined: the K steps as K batches of husky_sort_host_many (2 device
-        # slots, one stream each for H2D copies, kernels and D2H copies)
-        depth = 2
-        mws = torch.empty(h.husky_sort_host_many_workspace(coder, n, total, depth), dtype=torch.uint8, device=dev)
-        outs = [(torch.empty(n, dtype=torch.int32).pin_memory(), torch.empty(total + 8, dtype=dt).pin_memory(),
-                 torch.empty(n + 1, dtype=torch.int64).pin_memory()) for _ in range(depth)]
-        batches = [(hu, ho, outs[b % depth][0], outs[b % depth][1], outs[b % depth][2]) for b in range(steps)]
-        h.husky_sort_host_many(coder, batches[:depth], mws, depth)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        h.husky_sort_host_many(coder, batches, mws, depth)
-        torch.cuda.synchronize()
-        ms = (time.perf_counter() - t0) * 1e3 / steps
-        api = (f"husky_sort_host_many: {steps} steps as {steps} pipelined batches, {depth} device slots, H2D / "
-               "kernels / D2H on three streams (pinned host buffers), host wall clock around the call")
-        hp = outs[(steps - 1) % depth][0]
-    else:
-        # 2^30 strings: one device slot (inputs + outputs + workspace ~105 GB);
-        # one husky_sort_host call per step, CUDA events around it
-        hws = torch.empty(h.husky_sort_host_workspace(coder, n, total), dtype=torch.uint8, device=dev)
-        hp = torch.empty(n, dtype=torch.int32).pin_memory()
-        hsu = torch.empty(total + 8, dtype=dt).pin_memory()
-        hso = torch.empty(n + 1, dtype=torch.int64).pin_memory()
-        for _ in range(warmup):
-            h.husky_sort_host(coder, hu, ho, hp, hsu, hso, hws)
-        ts = []
-        stream = torch.cuda.current_stream()
-        for i in range(steps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            h.husky_sort_host(coder, hu, ho, hp, hsu, hso, hws)
-            b.record(stream)
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        ms = statistics.median(ts)
-        api = "husky_sort_host, one call per step (pinned host buffers), CUDA events around the call, median"
-        del hws
+    # pipelined: the K steps as K batches of husky_sort_host_many, H2D / kernels
+    # / D2H on three streams.  Up to 2^28 strings: 2 device slots (a batch's
+    # copies overlap another batch's kernels).  Above (C5: inputs + outputs +
+    # workspace ~105 GB): ONE slot -- the next batch's inputs go in over PCIe
+    # while this batch's outputs come out (full duplex), the sort of the next
+    # batch waits for both
+    depth = 2 if n <= PACK_MAX_N else 1
+    mws = torch.empty(h.husky_sort_host_many_workspace(coder, n, total, depth), dtype=torch.uint8, device=dev)
+    outs = [(torch.empty(n, dtype=torch.int32).pin_memory(), torch.empty(total + 8, dtype=dt).pin_memory(),
+             torch.empty(n + 1, dtype=torch.int64).pin_memory()) for _ in range(depth)]
+    batches = [(hu, ho, outs[b % depth][0], outs[b % depth][1], outs[b % depth][2]) for b in range(steps)]
+    h.husky_sort_host_many(coder, batches[:max(depth, warmup)], mws, depth)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h.husky_sort_host_many(coder, batches, mws, depth)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    api = (f"husky_sort_host_many: {steps} steps as {steps} pipelined batches, {depth} device slot(s), H2D / "
+           "kernels / D2H on three streams (pinned host buffers), host wall clock around the call")
+    hp = outs[(steps - 1) % depth][0]
+    del mws
     return {"value": round(n / (ms * 1e-3) / 1e6, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3), "api": api}, hp
 

@@ -281,13 +281,58 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       if (lo < hi) {
         if (PACKED && ((dec >> j) & 1)) {
           for (uint64_t x = lo; x < hi; ++x) stage[x - w0] = decb(sv[j], (int)(x - d));
-        } else if (CHECK && ((slb >> j) & 1)) {
-          constexpr int SB = T::kS * W;  // string bytes [0, SB) come from the code
+        } else if (PACKED && CHECK && ((slb >> j) & 1)) {
+          // (the packed instantiations keep the per-byte loop: the register
+          // image below costs them spills -- C2 / C3 gathers 250 / 224 ->
+          // 264 / 240 us)
+          constexpr int SB = T::kS * W;
           const uint4 rec = s_slab[j * kGatherThreads + tid];
           for (uint64_t x = lo; x < hi; ++x) {
             const int b = (int)(x - d);
             stage[x - w0] = b < SB ? decb(sv[j], b) : slab_byte(rec, b - SB + 1);
           }
+        } else if (!PACKED && CHECK && ((slb >> j) & 1)) {
+          // the string's bytes assembled in three registers first -- units
+          // [0, S) decoded from the code (independent table lookups), the
+          // rest from the slab record -- then stored byte by byte with no
+          // dependency between the stores (a per-byte decode loop measured
+          // 10 us per C5 tile, half of the tile's time)
+          constexpr int SB = T::kS * W;  // string bytes [0, SB) come from the code
+          uint64_t img0 = 0, img1 = 0, img2 = 0;
+#pragma unroll
+          for (int b = 0; b < SB; ++b) {
+            const uint64_t ch = decb(sv[j], b);
+            if (b < 8) img0 |= ch << (8 * b);
+            else img1 |= ch << (8 * (b - 8));
+          }
+          {
+            const uint4 rec = s_slab[j * kGatherThreads + tid];
+            const uint64_t r0 = (uint64_t)rec.x | ((uint64_t)rec.y << 32), r1 = (uint64_t)rec.z | ((uint64_t)rec.w << 32);
+            const uint64_t t0 = (r0 >> 8) | (r1 << 56), t1 = r1 >> 8;  // record bytes 1..15
+            if (SB == 9) {
+              img1 |= t0 << 8;
+              img2 = (t0 >> 56) | (t1 << 8);
+            } else {  // SB == 6
+              img0 |= t0 << 48;
+              img1 = (t0 >> 16) | (t1 << 48);
+              img2 = t1 >> 16;
+            }
+          }
+          // bytes up to a 4-byte boundary of the stage, then whole 32-bit
+          // words (funnel-shifted out of the image), then the tail
+          auto img_byte = [&](uint32_t b) -> uint32_t {
+            const uint64_t wv = b < 8 ? img0 : (b < 16 ? img1 : img2);
+            return (uint32_t)(wv >> (8 * (b & 7))) & 0xFFu;
+          };
+          uint64_t x = lo;
+          for (; x < hi && ((x - w0) & 3); ++x) stage[x - w0] = (uint8_t)img_byte((uint32_t)(x - d));
+          for (; x + 4 <= hi; x += 4) {
+            const uint32_t b = (uint32_t)(x - d), sh = (b & 7) * 8;
+            const uint64_t lo64 = b < 8 ? img0 : (b < 16 ? img1 : img2), hi64 = b < 8 ? img1 : (b < 16 ? img2 : 0ull);
+            const uint64_t v = sh ? ((lo64 >> sh) | (hi64 << (64 - sh))) : lo64;
+            *reinterpret_cast<uint32_t *>(stage + (x - w0)) = (uint32_t)v;
+          }
+          for (; x < hi; ++x) stage[x - w0] = (uint8_t)img_byte((uint32_t)(x - d));
         } else {
           const uint8_t *sp = ub + sv[j] * W;
           for (uint64_t x = lo; x < hi; x += 8) {

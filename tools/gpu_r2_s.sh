@@ -1,0 +1,4 @@
+python -c "import __graft_entry__ as g; g.build()"
+timeout 2400 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for c in "30 3 C5" "23 5 C2" "23 5 C3"; do timeout 300 python tools/c5_probe.py $c 2>&1 | tail -1; done
+timeout 1500 python bench.py > gpurun_out/bench_r2s.json 2> gpurun_out/bench_r2s.err; echo bench rc=$?
