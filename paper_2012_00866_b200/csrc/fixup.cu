@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   if (st->trivial_mask == 0xFFu) return;  // all codes equal: see staged_run
   const bool general = st->general != 0;
   // compare from unit S (equal codes fix units [0, S)), or from 0 off-domain
-  const uint32_t kstart = general ? 0u : (uint32_t)(T::kS * W);
+  const RunRule rule = run_rule<CODER>(st);
+  const uint32_t kstart = general ? 0u : rule.S * W;
   const uint32_t ns = st->n_small, nm = st->n_medium;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(256)
   pdl_wait();
   if (st->violations & kOffsetsBad) return;
   const uint32_t lane = lane_id();
+  const RunRule rule = run_rule<CODER>(st);
   const uint32_t nsmall = st->n_small;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t e = first + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < nsmall; e += warps) {
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(256)
       uint32_t other = __shfl_sync(0xFFFFFFFFu, my, j);
       if (lane < len && j != lane &&
           (general ? cmp_general<CODER>(units, offsets, other, my)
-                   : cmp_equal_code<CODER>(units, offsets, other, my, T::kS)) < 0)
+                   : cmp_equal_code<CODER>(units, offsets, other, my, rule.S, rule.PL)) < 0)
         ++rank;
     }
     __syncwarp();
@@ -332,6 +334,7 @@ __global__ void __launch_bounds__(1024)
   pdl_wait();
   if (st->violations & kOffsetsBad) return;
   const uint32_t nmed = st->n_medium;
+  const RunRule rule = run_rule<CODER>(st);
   const bool general = st->general != 0;
   for (uint32_t e = first + blockIdx.x; e < nmed; e += gridDim.x) {
     uint2 ent = list[cap - 1 - e];
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(1024)
             if (a == 0xFFFFFFFFu) gt = b != 0xFFFFFFFFu;
             else if (b == 0xFFFFFFFFu) gt = false;
             else gt = (general ? cmp_general<CODER>(units, offsets, a, b)
-                               : cmp_equal_code<CODER>(units, offsets, a, b, T::kS)) > 0;
+                               : cmp_equal_code<CODER>(units, offsets, a, b, rule.S, rule.PL)) > 0;
             bool asc = (i & k) == 0;
             if (gt == asc) { s[i] = b; s[ixj] = a; }
           }
@@ -403,6 +406,7 @@ __global__ void __launch_bounds__(256)
     k_seg_prep(const uint32_t *__restrict__ perm_seg, uint64_t len, const void *__restrict__ units,
                const int64_t *__restrict__ offsets, uint32_t from, DevState *st) {
   using T = CoderTraits<CODER>;
+  const int64_t pl = run_rule<CODER>(st).PL;  // the short rule of this sort (R6 / R19)
   constexpr int W = T::kUnitBytes;
   const uint32_t i0 = perm_seg[0];
   const int64_t o0 = offsets[i0], l0 = offsets[i0 + 1] - o0;
@@ -413,7 +417,7 @@ __global__ void __launch_bounds__(256)
        e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t i = perm_seg[e];
     int64_t o = offsets[i], l = offsets[i + 1] - o;
-    if (l <= T::kPL && !st->general) has_short = 1;  // short rule: equal codes only (R6)
+    if (l <= pl && !st->general) has_short = 1;  // short rule: equal codes only (R6)
     int64_t m = l < l0 ? l : l0;
     int64_t lim = (int64_t)from + kLcpCap;
     if (m > lim) m = lim;
@@ -464,6 +468,7 @@ __global__ void __launch_bounds__(256)
                const int64_t *__restrict__ offsets, uint32_t from, uint64_t *__restrict__ key2,
                DevState *st) {
   using T = CoderTraits<CODER>;
+  const int64_t pl = run_rule<CODER>(st).PL;  // the short rule of this sort (R6 / R19)
   __shared__ uint32_t sh_hist[8 * 256];
   for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) sh_hist[i] = 0;
   __syncthreads();
@@ -475,7 +480,7 @@ __global__ void __launch_bounds__(256)
     if (valid) {
       uint32_t i = perm_seg[e];
       int64_t o = offsets[i], l = offsets[i + 1] - o;
-      if (l <= T::kPL && st->seg_has_short) {
+      if (l <= pl && st->seg_has_short) {
         key = (uint64_t)l;
       } else {
         int64_t rem = l - (int64_t)L;

@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       s_su[b] = peer->start_u[b];
     }
   }
+  const RunRule rule = run_rule<CODER>(CHECK ? st : nullptr);  // run detection rule (R6 / R19)
   if (st) {
     if (st->violations & kOffsetsBad) return;  // invalid input: reported by the caller
     if ((PACKED || CHECK) && codes == nullptr) codes = reinterpret_cast<const uint64_t *>(st->sorted_keys);
@@ -225,8 +226,8 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       const uint64_t p = p0 + j;
       const unsigned long long pc = j == 0 ? prevc : cc[j - 1];
       const unsigned long long nc = j == kGatherItems - 1 ? nextc : cc[j + 1];
-      const bool ep = p < n && p > 0 && cc[j] == pc;
-      const bool en = p + 1 < n && cc[j] == nc;
+      const bool ep = p < n && p > 0 && ((cc[j] ^ pc) & rule.mask) == 0;
+      const bool en = p + 1 < n && ((cc[j] ^ nc) & rule.mask) == 0;
       eqp |= (uint32_t)ep << j;
       eqn |= (uint32_t)en << j;
       nstart += (!ep && en);
@@ -447,12 +448,12 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
     for (int j = 0; j < kGatherItems; ++j) {
       if ((eqp >> j) & 1) {
         int c;
-        if (pl <= PL || len[j] <= PL) {
+        if (pl <= rule.PL || len[j] <= rule.PL) {
           c = pl < len[j] ? -1 : (pl > len[j] ? 1 : 0);  // short rule (R6)
         } else if (sorted_units && !direct && po != ~0ull && po + pl <= win_units && d + len[j] <= win_units) {
           c = 0;  // both staged: compare units [S, min) in shared memory, 8 bytes at a time
           const uint32_t m = (pl < len[j] ? pl : len[j]) * W;  // bytes
-          for (uint32_t k = T::kS * W; k < m && c == 0; k += 8) {
+          for (uint32_t k = rule.S * W; k < m && c == 0; k += 8) {
             uint64_t x = stage_load8(stage, (uint32_t)(po * W) + k), y = stage_load8(stage, (uint32_t)(d * W) + k);
             const uint32_t take = m - k < 8 ? m - k : 8;
             if (take < 8) {
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
           }
           if (c == 0) c = pl < len[j] ? -1 : (pl > len[j] ? 1 : 0);
         } else {
-          c = cmp_units_from<CODER>(units, __ldg(offsets + pi), pl, __ldg(offsets + ix[j]), len[j], T::kS);
+          c = cmp_units_from<CODER>(units, __ldg(offsets + pi), pl, __ldg(offsets + ix[j]), len[j], rule.S);
         }
         if (c > 0 || (c == 0 && pi > ix[j])) bad |= 1u << j;
       }

@@ -137,6 +137,11 @@ static int slab_env() {
   return e ? atoi(e) : -1;
 }
 
+static int skip_env() {
+  const char *e = getenv("HUSKY_SKIP");
+  return e ? atoi(e) : 1;
+}
+
 static bool alpha_env() {
   const char *e = getenv("HUSKY_ALPHA");
   return !(e && e[0] == '0');
@@ -147,6 +152,7 @@ static bool alpha_env() {
 struct MainFlags {
   int coder = 0, kc = 0;
   bool packed = false, compress = false, slab = false, pdl = true;
+  int skip = 0;  // leave the lowest varying digit unsorted (R19): 0 never, 1 entropy rule, 2 always
 };
 
 // Everything from the DevState reset to the copy of DevState into h_state
@@ -181,7 +187,9 @@ static husky_status enqueue_main(Sorter &S, const MainFlags &F, void *d_sorted_u
     launch_encode(coder, d_units, d_offsets, n, S.keysA(), &st->violations, S.sms, s, packed_payload, slab,
                   !F.packed, F.compress ? st->alpha : nullptr);
   }
-  launch_hist_plan(keysA, n, st, keysA, keysB, S.sms, s, F.compress);
+  launch_hist_plan(keysA, n, st, keysA, keysB, S.sms, s, F.compress, F.skip,
+                   kc == HUSKY_CODER_UNICODE ? CoderTraits<HUSKY_CODER_UNICODE>::kS : CoderTraits<HUSKY_CODER_ASCII>::kS,
+                   kc == HUSKY_CODER_UNICODE ? CoderTraits<HUSKY_CODER_UNICODE>::kPL : CoderTraits<HUSKY_CODER_ASCII>::kPL);
 
   // ---- A2 key sort, LSD onesweep: (code, index) -> sorted codes, perm.  The
   // pass plan (which digits are not shared by all keys) is made on device, so
@@ -249,7 +257,7 @@ static husky_status enqueue_main(Sorter &S, const MainFlags &F, void *d_sorted_u
 // Off while profiling (per-launch events), with HUSKY_DEBUG_SYNC, and with
 // HUSKY_GRAPH=0.  LRU of kGraphCache entries per process.
 struct GraphKey {
-  int dev, coder, packed, compress, slab, pdl;
+  int dev, coder, packed, compress, slab, pdl, skip;
   const void *units, *offsets, *perm, *su, *so, *ws;
   uint64_t n;
   size_t ws_bytes;
@@ -391,6 +399,8 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   F.slab = d_sorted_units && (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE) &&
            ((n > kSlabMinN && slab_env() != 0) || slab_env() == 1);
   F.pdl = pdl_enabled();
+  // partial key sort (R19, ASCII codes only; HUSKY_SKIP=0 never, =2 always)
+  F.skip = coder == HUSKY_CODER_ASCII ? skip_env() : 0;
 
   DevState hs_local;
   const DevState *hs_src = &hs_local;
@@ -406,6 +416,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
     key.compress = F.compress;
     key.slab = F.slab;
     key.pdl = F.pdl;
+    key.skip = F.skip;
     key.units = d_units;
     key.offsets = d_offsets;
     key.perm = d_perm;
@@ -497,7 +508,9 @@ static husky_status refine_giants(Sorter &S, const DevState &hs0, void *d_sorted
   } else {
     std::vector<uint2> g(n_giant);
     HCHECK(cudaMemcpy(g.data(), list_g, n_giant * sizeof(uint2), cudaMemcpyDeviceToHost));
-    for (auto &x : g) queue.push_back({x.x, x.y, (uint32_t)(coder == HUSKY_CODER_ASCII ? 9 : 3)});
+    // units fixed by equal codes: the sort's run rule (R6 / R19)
+    const uint32_t s0 = hs0.seq_units ? hs0.seq_units : (uint32_t)(coder == HUSKY_CODER_ASCII ? 9 : 3);
+    for (auto &x : g) queue.push_back({x.x, x.y, s0});
     giant_spans = g;
   }
   const uint32_t win = coder == HUSKY_CODER_ASCII ? 7 : 3;

@@ -93,8 +93,29 @@ struct DevState {
   // were re-packed with cbits bits per field (ccomp)
   uint32_t alpha[4];
   uint32_t ccomp, cbits;
-  uint32_t pad[9];
+  // the run rule of this sort (k_hist_slots<PLAN>; 0 = the coder's defaults):
+  // keys are equal for run detection when equal under key_mask; equal masked
+  // keys fix units [0, seq_units), and a string of <= short_len units is then
+  // a prefix of the other (R6 / R19)
+  uint32_t seq_units, short_len;
+  unsigned long long key_mask;
+  uint32_t pad[5];
 };
+
+// The run rule kernels apply: by default equal codes fix units [0, S) and the
+// short rule holds for lengths <= PL (R6); a sort whose plan leaves the lowest
+// digit unsorted (R19) has a shorter fixed prefix and masks that digit out of
+// run detection.
+struct RunRule {
+  uint32_t S, PL;
+  unsigned long long mask;
+};
+template <int CODER>
+__device__ __forceinline__ RunRule run_rule(const DevState *st) {
+  using T = CoderTraits<CODER>;
+  if (st == nullptr || st->seq_units == 0) return RunRule{(uint32_t)T::kS, (uint32_t)T::kPL, ~0ull};
+  return RunRule{st->seq_units, st->short_len, st->key_mask};
+}
 
 // Alphabet compression (ASCII): the code's nine 7-bit fields re-packed as
 // their ranks among the field values present (0 -- padding / NUL -- always
@@ -432,18 +453,18 @@ __device__ __forceinline__ int cmp_general(const void *units, const int64_t *off
   return ia < ib ? -1 : (ia > ib ? 1 : 0);
 }
 
-// Exact comparator for two strings whose husky codes are EQUAL (R6):
-// if either length <= PL the shorter one is a prefix of the longer (order by
-// length, then index); otherwise units [0, S) are equal and the comparison
-// starts at unit `from` (>= S when the caller knows a longer common prefix).
+// Exact comparator for two strings whose husky codes are EQUAL (under the run
+// rule's mask, R6 / R19): if either length <= pl the shorter one is
+// a prefix of the longer (order by length, then index); otherwise units [0, S)
+// are equal and the comparison starts at unit `from` (>= S).
+// pl: the short-rule length (RunRule::PL).
 template <int CODER>
 __device__ __forceinline__ int cmp_equal_code(const void *units, const int64_t *offsets, uint32_t ia,
-                                              uint32_t ib, int64_t from) {
-  using T = CoderTraits<CODER>;
+                                              uint32_t ib, int64_t from, int64_t pl) {
   int64_t oa = offsets[ia], la = offsets[ia + 1] - oa;
   int64_t ob = offsets[ib], lb = offsets[ib + 1] - ob;
   int c;
-  if (la <= T::kPL || lb <= T::kPL) c = (la < lb) ? -1 : (la > lb ? 1 : 0);
+  if (la <= pl || lb <= pl) c = (la < lb) ? -1 : (la > lb ? 1 : 0);
   else c = cmp_units_from<CODER>(units, oa, la, ob, lb, from);
   if (c) return c;
   return ia < ib ? -1 : (ia > ib ? 1 : 0);

@@ -56,9 +56,15 @@ constexpr int kHistBlocksPerSM = 4;  // resident CTAs of 512 threads per SM
 // compress (ASCII, PLAN): alphabet compression first (husky_internal.cuh):
 // every key is re-packed in place from DevState::alpha when that needs at most
 // 56 bits, and the histograms are those of the re-packed keys.
+// skip (PLAN, ASCII codes; R19): 1 = leave the lowest varying digit
+// unsorted when the other varying digits carry enough entropy that the extra
+// equal-key pairs this creates are rare (the run machinery resolves them
+// exactly), 2 = whenever possible (tests), 0 = never.  def_s / def_pl: the
+// coder's run rule when nothing is skipped.
 template <bool PLAN>
 __global__ void __launch_bounds__(512) k_hist_slots(uint64_t *__restrict__ keys, uint64_t n, DevState *st,
-                                                    uint64_t *keysA, uint64_t *keysB, int compress) {
+                                                    uint64_t *keysA, uint64_t *keysB, int compress, int skip,
+                                                    uint32_t def_s, uint32_t def_pl) {
   constexpr uint32_t M = kBins - 1;
   pdl_wait();  // PLAN: launched as a programmatic dependent of the encoder
   __shared__ uint32_t h[8 * kBins];
@@ -109,7 +115,9 @@ __global__ void __launch_bounds__(512) k_hist_slots(uint64_t *__restrict__ keys,
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // the last CTA: exclusive scans and trivial digits (as k_hist_scan), then the plan
+  // the last CTA: exclusive scans and trivial digits (as k_hist_scan), the
+  // entropy of each digit's histogram, then the plan
+  __shared__ float s_h[8], s_hw[512 / 32];
   uint32_t trivial = 0;
   for (int d = 0; d < 8; ++d) {
     const uint32_t v = threadIdx.x < kBins ? __ldcg(&st->hist[d][threadIdx.x]) : 0u;
@@ -118,14 +126,51 @@ __global__ void __launch_bounds__(512) k_hist_slots(uint64_t *__restrict__ keys,
     if (threadIdx.x < kBins) st->digit_start[d][threadIdx.x] = ex;
     const bool all_here = __syncthreads_or((uint64_t)v == n) != 0;
     trivial |= (uint32_t)all_here << d;
+    if (skip) {  // H_d = -sum p log2 p over the digit's bins
+      const float pr = (float)v / (float)n;
+      float h = v ? -pr * __log2f(pr) : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
+      if (lane_id() == 0) s_hw[threadIdx.x >> 5] = h;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < 512 / 32; ++w) t += s_hw[w];
+        s_h[d] = t;
+      }
+      __syncthreads();
+    }
   }
   if (threadIdx.x == 0) {
     st->trivial_mask = trivial;
     st->ccomp = cmp ? 1u : 0u;
     st->cbits = cbits;
-    uint32_t np = 0;
+    uint32_t np = 0, dig[8];
     for (int d = 0; d < 8; ++d)
-      if (!((trivial >> d) & 1)) st->pass_digit[np++] = d;
+      if (!((trivial >> d) & 1)) dig[np++] = d;
+    uint32_t seq = def_s, pl = def_pl;
+    unsigned long long mask = ~0ull;
+    if (skip && np >= 2) {
+      // leave digit d0 (the lowest varying) unsorted: equal keys above it fix
+      // the fields that lie wholly above bit 8 (d0 + 1)
+      const uint32_t d0 = dig[0], fb = cmp ? cbits : 7u;
+      const int sp = 9 - (int)((8 * (d0 + 1) + fb - 1) / fb);
+      float hhi = 0.f;
+      for (uint32_t i = 1; i < np; ++i) hhi += s_h[dig[i]];
+      // expected extra equal-key pairs if the other digits were independent
+      const float extra = 0.5f * (float)n * (float)n * exp2f(-hhi);
+      if (sp >= 1 && (skip == 2 || extra < 1e-4f * (float)n)) {
+        for (uint32_t i = 0; i + 1 < np; ++i) dig[i] = dig[i + 1];
+        --np;
+        seq = (uint32_t)sp;
+        pl = (uint32_t)sp;
+        mask = ~((1ull << (8 * (d0 + 1))) - 1ull);
+      }
+    }
+    for (uint32_t i = 0; i < np; ++i) st->pass_digit[i] = dig[i];
+    st->seq_units = seq;
+    st->short_len = pl;
+    st->key_mask = mask;
     st->np = np;
     st->sorted_keys = (unsigned long long)((np & 1) ? keysB : keysA);
   }
@@ -135,19 +180,20 @@ void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_s
   if (n == 0) return;
   Scope sc_(ST_HIST_SCAN, s, n);
   const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * kHistBlocksPerSM);
-  k_hist_slots<false><<<(unsigned)blocks, 512, 0, s>>>(const_cast<uint64_t *>(keys), n, st, nullptr, nullptr, 0);
+  k_hist_slots<false><<<(unsigned)blocks, 512, 0, s>>>(const_cast<uint64_t *>(keys), n, st, nullptr, nullptr, 0, 0,
+                                                      0u, 0u);
 }
 
 // histograms + scans + pass plan of the device-planned passes in one launch
 // (DevState::hist_done must be 0: DevState is zeroed per sort)
 void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *keysA, uint64_t *keysB,
-                      int num_sms, cudaStream_t s, bool compress) {
+                      int num_sms, cudaStream_t s, bool compress, int skip, uint32_t def_s, uint32_t def_pl) {
   if (n == 0) return;
   Scope sc_(ST_HIST_SCAN, s, n);
   GroupScope grp(ST_HIST_SCAN, s);
   const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * kHistBlocksPerSM);
   launch_pdl(k_hist_slots<true>, dim3((unsigned)blocks), dim3(512), 0, s, const_cast<uint64_t *>(keys), n, st, keysA,
-             keysB, compress ? 1 : 0);
+             keysB, compress ? 1 : 0, skip, def_s, def_pl);
 }
 
 constexpr int kRadixWarps = kRadixThreads / 32;

@@ -51,13 +51,15 @@ __global__ void __launch_bounds__(kScanThreads)
   cp_async_wait_all();
   __syncthreads();
 
-  // keys at p0-1 .. p0+kScanItems
+  // keys at p0-1 .. p0+kScanItems (MODE 0: under the run rule's mask, R19)
+  const RunRule rule = run_rule<CODER>(st);
+  const unsigned long long km = MODE == 0 ? rule.mask : ~0ull;
   uint64_t c[kScanItems + 2];
 #pragma unroll
   for (int j = 0; j < kScanItems + 2; ++j) {
     int64_t p = (int64_t)p0 + j - 1;
     uint32_t i = tid * kScanItems + j;
-    c[j] = (p >= 0 && (uint64_t)p < n) ? s_keys[i + i / 8] : 0ull;
+    c[j] = (p >= 0 && (uint64_t)p < n) ? (s_keys[i + i / 8] & km) : 0ull;
   }
   uint32_t eqp = 0, eqn = 0, cnt = 0;  // bit j: eq_prev / eq_next of position p0+j
 #pragma unroll
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(kScanThreads)
     if ((eqn >> j) & 1) {
       bool bad;
       if (MODE == 0) {
-        bad = cmp_equal_code<CODER>(units, offsets, __ldg(perm + p), __ldg(perm + p + 1), T::kS) > 0;
+        bad = cmp_equal_code<CODER>(units, offsets, __ldg(perm + p), __ldg(perm + p + 1), rule.S, rule.PL) > 0;
       } else {
         constexpr uint64_t tagmask = CODER == HUSKY_CODER_ASCII ? 0xFFull : 0xFFFFull;
         bad = (c[j + 1] & tagmask) == (uint64_t)(16 + T::kTagCap);

@@ -662,3 +662,30 @@ def test_staged_fixup_ties_nul_and_prefixes(torch, h, oracle_mod):
     perm = rng.permutation(len(strings))
     w = W.from_strings([strings[p] for p in perm], ASCII)
     check_against_oracle(torch, h, oracle_mod, w)
+
+
+# ------------------------------------- partial key sort (lowest digit unsorted)
+@pytest.mark.parametrize("name,n", [("C1", 100_000), ("C2", 300_000), ("C5", 300_000), ("C4", 40_000),
+                                    ("D1", 150_000)])
+def test_lowest_digit_unsorted_forced(torch, h, oracle_mod, monkeypatch, name, n):
+    """HUSKY_SKIP=2 leaves the lowest varying digit of the ASCII keys unsorted
+    whenever the plan allows (R19): run detection then compares keys under the
+    mask, equal masked keys fix fewer leading units and the short rule shrinks
+    with them; every extra equal-key pair is resolved by the run machinery.
+    Bit-exact against the oracle, with fewer key-sort passes."""
+    w = W.make(name, n)
+    monkeypatch.setenv("HUSKY_SKIP", "0")
+    ref = check_against_oracle(torch, h, oracle_mod, w)
+    monkeypatch.setenv("HUSKY_SKIP", "2")
+    forced = check_against_oracle(torch, h, oracle_mod, w)
+    if ref["keys_partitioned"] >= 2 * n:
+        assert forced["keys_partitioned"] == ref["keys_partitioned"] - n
+
+
+@pytest.mark.parametrize("seed", range(0, 300, 7))
+def test_lowest_digit_unsorted_fuzz(torch, h, oracle_mod, monkeypatch, seed):
+    """The fuzz cases (every coder, NULs, prefixes, duplicates, ragged sizes)
+    with the partial key sort forced."""
+    import test_gpu_fuzz as F
+    monkeypatch.setenv("HUSKY_SKIP", "2")
+    check_against_oracle(torch, h, oracle_mod, F._case(1000 + seed))
