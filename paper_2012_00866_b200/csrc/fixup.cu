@@ -5,8 +5,8 @@
 // 433), relying on there being "very few inversions" left.
 // Because every remaining inversion is inside an equal-code run (R6),
 // only dirty runs are re-sorted here, each independently:
-//   staged (the main pass, sorted strings present, run <= 4096 strings and
-//          <= kFixStageBytes of units): one CTA per run.  The run's strings are
+//   staged (the main pass, sorted strings present, 32 < run <= 4096 strings
+//          and <= kFixStageBytes of units): one CTA per run.  The run's strings are
 //          contiguous after the gather, so they are staged into shared memory
 //          with ONE bulk async copy (cp.async.bulk, the TMA engine) completing
 //          on an mbarrier; each string gets a 48-bit big-endian key of its
@@ -17,8 +17,8 @@
 //          2.8 ms on 2^23 D1 strings: too many barrier-separated stages).  The sorted run
 //          is written back in place -- perm, sorted offsets and sorted units --
 //          so no re-gather follows.
-//   small  (<= 32 strings, others): one warp; every lane owns a string and
-//          computes its rank with the exact comparator (rank sort);
+//   small  (<= 32 strings): one warp; every lane owns a string and computes
+//          its rank with the exact comparator (rank sort);
 //   medium (<= 4096, others): one CTA, bitonic sort of indices in shared memory
 //          with global-memory comparisons (refinement sub-runs, perm-only mode,
 //          runs whose units exceed the stage);
@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   // compare from unit S (equal codes fix units [0, S)), or from 0 off-domain
   const RunRule rule = run_rule<CODER>(st);
   const uint32_t kstart = general ? 0u : rule.S * W;
-  const uint32_t ns = st->n_small, nm = st->n_medium;
+  // medium runs only: runs of <= 32 strings go to k_fix_small (a warp each;
+  // a CTA-wide staged sort per 2-string run measured 0.8 ms for the ~10K
+  // extra pairs of a partial key sort at 2^30)
+  const uint32_t nm = st->n_medium;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the init, seen by the async proxy
@@ -154,8 +157,8 @@ __global__ void __launch_bounds__(kFixThreads, 1)
 #ifdef HUSKY_FIX_TIMING
   long long ft_last = clock64();
 #endif
-  for (uint32_t e = blockIdx.x; e < ns + nm; e += gridDim.x) {
-    const uint2 ent = e < ns ? list[e] : list[cap - 1 - (e - ns)];
+  for (uint32_t e = blockIdx.x; e < nm; e += gridDim.x) {
+    const uint2 ent = list[cap - 1 - e];
     const uint32_t start = ent.x, len = ent.y;
     const int64_t B0u = so[start], B1u = so[start + len];
     const uint64_t B0 = (uint64_t)B0u * W, B1 = (uint64_t)B1u * W;  // the run's bytes in su
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(256)
   for (uint32_t e = first + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < nsmall; e += warps) {
     uint2 ent = list[e];
     const uint32_t start = ent.x, len = ent.y;
-    if (staged_run<T::kUnitBytes>(st, so, start, len)) continue;
+    (void)so;  // small runs are never staged
     uint32_t my = lane < len ? perm[start + lane] : 0xFFFFFFFFu;
     uint32_t rank = 0;
     const bool general = st->general != 0;

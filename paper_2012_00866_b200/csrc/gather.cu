@@ -671,8 +671,8 @@ __global__ void __launch_bounds__(256)
   for (uint32_t e = blockIdx.x; e < ns + nm; e += gridDim.x) {
     uint2 ent = e < ns ? list[first_small + e] : list[cap - 1 - (first_medium + e - ns)];
     const uint32_t start = ent.x, len = ent.y;
-    // runs k_fix_staged sorted and wrote back in place (fixup.cu)
-    if (skip_staged && st->trivial_mask != 0xFFu &&
+    // medium runs k_fix_staged sorted and wrote back in place (fixup.cu)
+    if (skip_staged && e >= ns && st->trivial_mask != 0xFFu &&
         (uint64_t)(sorted_offsets[start + len] - sorted_offsets[start]) * W <= (uint64_t)kFixStageBytes)
       continue;
     const unsigned long long base = (unsigned long long)sorted_offsets[start];

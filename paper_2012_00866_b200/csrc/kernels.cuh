@@ -113,10 +113,11 @@ void launch_runs_classify(const uint32_t *run_start, const uint32_t *run_end, co
 
 // A5 fix-up of dirty runs (lists filled by classify; counts read on device)
 // entries [first, count) of each list (first > 0: the round after a refinement)
-// staged: the main pass with sorted strings -- every small / medium run whose
-// units fit kFixStageBytes is sorted in shared memory and written back in
-// place (fixup.cu); the other kernels and the re-gather then skip those runs
-// (staged_so = the sorted offsets), else they take every run (staged_so NULL).
+// staged: the main pass with sorted strings -- every medium run whose units
+// fit kFixStageBytes is sorted in shared memory and written back in place
+// (fixup.cu); k_fix_medium and the re-gather then skip those runs (staged_so =
+// the sorted offsets), else they take every run (staged_so NULL).  Small runs
+// always take k_fix_small.
 constexpr int kFixStageBytes = 80 * 1024;
 void launch_fix_staged(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st, uint32_t *perm,
                        void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s);
