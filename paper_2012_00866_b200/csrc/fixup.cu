@@ -295,35 +295,83 @@ void launch_fix_staged(int coder, const uint2 *list_sm, uint64_t cap_sm, const D
   }
 }
 
+// A tiny dirty run (<= kTinyMax strings) by ONE thread: the strings' offsets
+// are loaded once, every pair is compared independently (their loads overlap)
+// and each string goes to its rank.  A partial key sort (R19) leaves ~10^6
+// two-string runs at 2^30 strings; a warp each left most lanes idle.
+template <int CODER>
+__device__ __forceinline__ void fix_tiny(uint32_t start, uint32_t len, uint32_t *perm, const void *units,
+                                         const int64_t *offsets, const RunRule &rule, bool general) {
+  uint32_t id[kTinyMax], rank[kTinyMax];
+  int64_t o[kTinyMax], l[kTinyMax];
+#pragma unroll
+  for (uint32_t i = 0; i < kTinyMax; ++i) {
+    id[i] = i < len ? perm[start + i] : 0u;
+    rank[i] = 0;
+  }
+#pragma unroll
+  for (uint32_t i = 0; i < kTinyMax; ++i) {
+    o[i] = i < len ? offsets[id[i]] : 0;
+    l[i] = i < len ? offsets[id[i] + 1] - o[i] : 0;
+  }
+#pragma unroll
+  for (uint32_t i = 1; i < kTinyMax; ++i) {
+#pragma unroll
+    for (uint32_t j = 0; j < i; ++j) {
+      if (i >= len) continue;
+      int c;  // string j against string i
+      if (general) c = cmp_units_from<CODER>(units, o[j], l[j], o[i], l[i], 0);
+      else if (l[j] <= rule.PL || l[i] <= rule.PL) c = l[j] < l[i] ? -1 : (l[j] > l[i] ? 1 : 0);
+      else c = cmp_units_from<CODER>(units, o[j], l[j], o[i], l[i], rule.S);
+      if (c == 0) c = id[j] < id[i] ? -1 : 1;
+      if (c < 0) ++rank[i];
+      else ++rank[j];
+    }
+  }
+#pragma unroll
+  for (uint32_t i = 0; i < kTinyMax; ++i)
+    if (i < len) perm[start + rank[i]] = id[i];
+}
+
+// Small dirty runs (<= kSmallMax strings): each lane takes one list entry;
+// runs of <= kTinyMax strings are fixed by that lane alone, larger ones by the
+// whole warp, one after another (every lane ranks one string with the exact
+// comparator).
 template <int CODER>
 __global__ void __launch_bounds__(256)
     k_fix_small(const uint2 *__restrict__ list, const DevState *st, uint32_t *perm,
                 const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t first,
                 const int64_t *__restrict__ so) {
-  using T = CoderTraits<CODER>;
   pdl_wait();
   if (st->violations & kOffsetsBad) return;
+  (void)so;  // small runs are never staged
   const uint32_t lane = lane_id();
   const RunRule rule = run_rule<CODER>(st);
   const uint32_t nsmall = st->n_small;
+  const bool general = st->general != 0;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t e = first + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < nsmall; e += warps) {
-    uint2 ent = list[e];
-    const uint32_t start = ent.x, len = ent.y;
-    (void)so;  // small runs are never staged
-    uint32_t my = lane < len ? perm[start + lane] : 0xFFFFFFFFu;
-    uint32_t rank = 0;
-    const bool general = st->general != 0;
-    for (uint32_t j = 0; j < len; ++j) {
-      uint32_t other = __shfl_sync(0xFFFFFFFFu, my, j);
-      if (lane < len && j != lane &&
-          (general ? cmp_general<CODER>(units, offsets, other, my)
-                   : cmp_equal_code<CODER>(units, offsets, other, my, rule.S, rule.PL)) < 0)
-        ++rank;
+  for (uint32_t b = first + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; b < nsmall; b += warps * 32) {
+    const uint32_t e = b + lane;
+    const uint2 mine = e < nsmall ? list[e] : make_uint2(0, 0);
+    if (mine.y >= 2 && mine.y <= kTinyMax) fix_tiny<CODER>(mine.x, mine.y, perm, units, offsets, rule, general);
+    uint32_t big = __ballot_sync(0xFFFFFFFFu, mine.y > kTinyMax);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const uint32_t start = __shfl_sync(0xFFFFFFFFu, mine.x, src), len = __shfl_sync(0xFFFFFFFFu, mine.y, src);
+      uint32_t my = lane < len ? perm[start + lane] : 0xFFFFFFFFu;
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < len; ++j) {
+        uint32_t other = __shfl_sync(0xFFFFFFFFu, my, j);
+        if (lane < len && j != lane &&
+            (general ? cmp_general<CODER>(units, offsets, other, my)
+                     : cmp_equal_code<CODER>(units, offsets, other, my, rule.S, rule.PL)) < 0)
+          ++rank;
+      }
+      __syncwarp();
+      if (lane < len) perm[start + rank] = my;
+      __syncwarp();
     }
-    __syncwarp();
-    if (lane < len) perm[start + rank] = my;
-    __syncwarp();
   }
 }
 

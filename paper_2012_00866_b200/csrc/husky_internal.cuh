@@ -51,6 +51,7 @@ template <> struct CoderTraits<HUSKY_CODER_ENGLISH6> {
 };
 
 constexpr int kSmallMax = 32;    // dirty runs up to this many strings: one warp
+constexpr uint32_t kTinyMax = 4; // ... and up to this many: one thread
 constexpr int kMediumMax = 4096; // ... up to this many: one CTA (bitonic in smem)
 
 // violation bits (OR-reduced; zero-initialised state)

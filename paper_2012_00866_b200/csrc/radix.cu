@@ -56,11 +56,16 @@ constexpr int kHistBlocksPerSM = 4;  // resident CTAs of 512 threads per SM
 // compress (ASCII, PLAN): alphabet compression first (husky_internal.cuh):
 // every key is re-packed in place from DevState::alpha when that needs at most
 // 56 bits, and the histograms are those of the re-packed keys.
-// skip (PLAN, ASCII codes; R19): 1 = leave the lowest varying digit
-// unsorted when the other varying digits carry enough entropy that the extra
-// equal-key pairs this creates are rare (the run machinery resolves them
-// exactly), 2 = whenever possible (tests), 0 = never.  def_s / def_pl: the
+// skip (PLAN, ASCII codes; R19): 1 = leave the lowest one or two
+// varying digits unsorted when the other varying digits carry enough entropy
+// that the extra equal-key pairs this creates are rare (the run machinery
+// resolves them exactly), 2 / 3 = one / two digits whenever possible (tests),
+// 0 = never.  def_s / def_pl: the
 // coder's run rule when nothing is skipped.
+#ifndef HUSKY_SKIP2_BAR
+#define HUSKY_SKIP2_BAR 4e-3f
+#endif
+constexpr float kSkip2Bar = HUSKY_SKIP2_BAR;
 template <bool PLAN>
 __global__ void __launch_bounds__(512) k_hist_slots(uint64_t *__restrict__ keys, uint64_t n, DevState *st,
                                                     uint64_t *keysA, uint64_t *keysB, int compress, int skip,
@@ -151,20 +156,28 @@ __global__ void __launch_bounds__(512) k_hist_slots(uint64_t *__restrict__ keys,
     uint32_t seq = def_s, pl = def_pl;
     unsigned long long mask = ~0ull;
     if (skip && np >= 2) {
-      // leave digit d0 (the lowest varying) unsorted: equal keys above it fix
-      // the fields that lie wholly above bit 8 (d0 + 1)
-      const uint32_t d0 = dig[0], fb = cmp ? cbits : 7u;
-      const int sp = 9 - (int)((8 * (d0 + 1) + fb - 1) / fb);
-      float hhi = 0.f;
-      for (uint32_t i = 1; i < np; ++i) hhi += s_h[dig[i]];
-      // expected extra equal-key pairs if the other digits were independent
-      const float extra = 0.5f * (float)n * (float)n * exp2f(-hhi);
-      if (sp >= 1 && (skip == 2 || extra < 1e-4f * (float)n)) {
-        for (uint32_t i = 0; i + 1 < np; ++i) dig[i] = dig[i + 1];
-        --np;
-        seq = (uint32_t)sp;
-        pl = (uint32_t)sp;
-        mask = ~((1ull << (8 * (d0 + 1))) - 1ull);
+      // leave the k lowest varying digits unsorted (k = 2 then 1): equal keys
+      // above them fix the fields that lie wholly above bit 8 (dig[k-1] + 1)
+      const uint32_t fb = cmp ? cbits : 7u;
+      for (uint32_t k = 2; k >= 1; --k) {
+        if (np < k + 1 || (skip == 2 && k != 1) || (skip == 3 && k != 2)) continue;
+        const uint32_t dtop = dig[k - 1];
+        const int sp = 9 - (int)((8 * (dtop + 1) + fb - 1) / fb);
+        float hhi = 0.f;
+        for (uint32_t i = k; i < np; ++i) hhi += s_h[dig[i]];
+        // expected extra equal-key pairs if the other digits were independent;
+        // one more pass costs ~24 B per key, one extra pair a check and at
+        // worst a two-string fix-up, so the bar is a small fraction of n
+        const float extra = 0.5f * (float)n * (float)n * exp2f(-hhi);
+        const float bar = (k == 1 ? 1e-4f : kSkip2Bar) * (float)n;
+        if (sp >= 1 && (skip >= 2 || extra < bar)) {
+          for (uint32_t i = 0; i + k < np; ++i) dig[i] = dig[i + k];
+          np -= k;
+          seq = (uint32_t)sp;
+          pl = (uint32_t)sp;
+          mask = ~((1ull << (8 * (dtop + 1))) - 1ull);
+          break;
+        }
       }
     }
     for (uint32_t i = 0; i < np; ++i) st->pass_digit[i] = dig[i];

@@ -24,8 +24,9 @@ def test_c5_above_2p28(oracle_mod):
     total = int(o[-1].item())
     perm, su, so, outc = h.sort(0, u, o)
     torch.cuda.synchronize()
-    # alphabet-compressed 54-bit keys: 7 passes, 6 with the lowest digit left unsorted (R19)
-    assert outc["keys_partitioned"] in (6 * n, 7 * n)
+    # alphabet-compressed 54-bit keys: 7 passes, 5 or 6 with the lowest one or two
+    # digits left unsorted (R19)
+    assert outc["keys_partitioned"] in (5 * n, 6 * n, 7 * n)
     r = checker.verify(u, o, perm, su, so)
     assert r == {"pairs": 0, "perm": 0, "content": 0, "offsets": 0}
     # independent host check (CPU oracle's verifier on the whole result)

@@ -680,12 +680,39 @@ def test_lowest_digit_unsorted_forced(torch, h, oracle_mod, monkeypatch, name, n
     forced = check_against_oracle(torch, h, oracle_mod, w)
     if ref["keys_partitioned"] >= 2 * n:
         assert forced["keys_partitioned"] == ref["keys_partitioned"] - n
+    # two digits (HUSKY_SKIP=3): many more equal masked keys, fewer fixed units;
+    # the extra pairs are tiny dirty runs (a thread each, fixup.cu fix_tiny)
+    monkeypatch.setenv("HUSKY_SKIP", "3")
+    forced2 = check_against_oracle(torch, h, oracle_mod, w)
+    if ref["keys_partitioned"] >= 3 * n:
+        assert forced2["keys_partitioned"] == ref["keys_partitioned"] - 2 * n
 
 
 @pytest.mark.parametrize("seed", range(0, 300, 7))
-def test_lowest_digit_unsorted_fuzz(torch, h, oracle_mod, monkeypatch, seed):
+@pytest.mark.parametrize("skip", ["2", "3"])
+def test_lowest_digit_unsorted_fuzz(torch, h, oracle_mod, monkeypatch, seed, skip):
     """The fuzz cases (every coder, NULs, prefixes, duplicates, ragged sizes)
-    with the partial key sort forced."""
+    with the partial key sort forced (one / two digits)."""
     import test_gpu_fuzz as F
-    monkeypatch.setenv("HUSKY_SKIP", "2")
+    monkeypatch.setenv("HUSKY_SKIP", skip)
     check_against_oracle(torch, h, oracle_mod, F._case(1000 + seed))
+
+
+@pytest.mark.parametrize("n", [5_000, 70_001])
+def test_tiny_runs_lane_fixup(torch, h, oracle_mod, n):
+    """Dirty runs of 2, 3 and 4 strings (a thread each: fix_tiny and the
+    lane re-gather) beside runs of 5..32 (a warp each), all sharing their
+    9-unit prefix (equal codes) and differing later, in shuffled order."""
+    rng = np.random.default_rng(n)
+    strings = []
+    while len(strings) < n:
+        size = int(rng.choice([2, 3, 4, 5, 9, 32]))
+        head = rng.integers(0x61, 0x7B, size=9).tolist()
+        for _ in range(size):
+            strings.append(head + rng.integers(0x61, 0x64, size=int(rng.integers(0, 6))).tolist())
+    strings = strings[:n]
+    perm = rng.permutation(len(strings))
+    w = W.from_strings([strings[p] for p in perm], ASCII)
+    out = check_against_oracle(torch, h, oracle_mod, w)
+    assert out["runs_by_class"][1] > 0
+    check_against_oracle(torch, h, oracle_mod, w, with_units=False)  # perm-only mode

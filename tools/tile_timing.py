@@ -6,14 +6,21 @@ sys.path.insert(0, ".")
 import paper_2012_00866_b200 as h
 import workloads as W
 
-w = W.make(sys.argv[1] if len(sys.argv) > 1 else "C2")
-u = torch.from_numpy(w.units.view(np.int16) if w.units.dtype == np.uint16 else w.units).cuda()
-o = torch.from_numpy(w.offsets).cuda()
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+if cfg == "C5":  # python tools/tile_timing.py C5 <log2n>: device generator
+    import workloads.gpu as G
+    u, o = G.c5_device(1 << int(sys.argv[2]))
+    coder, n = 0, int(o.numel() - 1)
+else:
+    w = W.make(cfg)
+    u = torch.from_numpy(w.units.view(np.int16) if w.units.dtype == np.uint16 else w.units).cuda()
+    o = torch.from_numpy(w.offsets).cuda()
+    coder, n = w.coder, w.n
 for _ in range(3):
-    h.sort(w.coder, u, o)
+    h.sort(coder, u, o)
 lib = h.lib()
 lib.husky_debug_tile_times.restype = ctypes.c_int
-import os; TS = int(os.environ.get("TILE", "6144")); ntiles = (w.n + TS - 1) // TS
+import os; TS = int(os.environ.get("TILE", "6144")); ntiles = (n + TS - 1) // TS
 buf = np.zeros((8192, 8), dtype=np.uint64)
 k = lib.husky_debug_tile_times(buf.ctypes.data_as(ctypes.c_void_p), 8192)
 t = buf[:min(ntiles, k)].astype(np.int64)
