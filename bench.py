@@ -405,11 +405,32 @@ def measure_single(args, name, n, dev, steps, warmup, flush, want_e2e, h, torch)
                                 "group, every timed step (profiler mode 2)") if groups is not None else
                                "breakdown steps, an event pair per launch (n < 2^22: kept out of the timed steps)",
                      "kernels": kern})
+    # ---- perm-only mode (no sorted strings: the run scan replaces the gather;
+    # SURVEY.md 8(d) reports it separately); its perm must equal the full sort's
+    del su, so
+    po = torch.empty_like(perm)
+    for _ in range(2):
+        h.husky_sort(coder, u, o, po, None, None, ws)
+    tpo = []
+    for i in range(min(steps, 5)):
+        flush.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        h.husky_sort(coder, u, o, po, None, None, ws)
+        b.record(stream)
+        torch.cuda.synchronize()
+        tpo.append(a.elapsed_time(b))
+    mpo = statistics.median(tpo)
+    perm_only = {"value": round(n / (mpo * 1e-3) / 1e6, 4), "unit": UNIT, "ms_per_step": round(mpo, 4),
+                 "ms_min": round(min(tpo), 4), "steps": len(tpo),
+                 "matches_full_sort_perm": bool(torch.equal(po, perm))}
+    del po
     res = {"name": name, "n": n, "coder": coder, "wl": wl, "times": times, "median": med, "min": mn, "mean": mean,
            "outcome": outc, "validation": bad, "launches": launches // max(steps, 1), "stages": stages,
-           "roofline": roof, "clocks": clk.summary(), "kernels_ms_sum": total_ms, "packed": packed}
+           "roofline": roof, "clocks": clk.summary(), "kernels_ms_sum": total_ms, "packed": packed,
+           "perm_only": perm_only}
     # keep what the e2e / library legs need, drop the rest
-    del ws, su, so
+    del ws
     res["perm_dev"] = perm
     return res
 
@@ -534,7 +555,7 @@ def run_single(args, h, torch, dev):
                                       **({"model_builder": v["model_builder"]} if "model_builder" in v else {}),
                                       **({"random_access": v["random_access"]} if "random_access" in v else {})}
                                   for k, v in rr.get("kernels", {}).items()},
-                     "outcome": r2["outcome"]}
+                     "outcome": r2["outcome"], "perm_only": r2["perm_only"]}
             fx = r2["stages"].get("fix_medium", {}).get("ms_per_step", 0.0) + \
                 r2["stages"].get("fix_small", {}).get("ms_per_step", 0.0)
             if cfg == "D1" and fx and wl2 is not None:
@@ -567,7 +588,7 @@ def run_single(args, h, torch, dev):
             "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": r["launches"],
             "clocks": r["clocks"], "stages": r["stages"], "validation": dict(r["validation"], steps=args.steps,
                                                                              verifier="checker/verify.cu"),
-            "library_bar": bar, "outcome": r["outcome"], "also": also or None}
+            "library_bar": bar, "outcome": r["outcome"], "perm_only": r["perm_only"], "also": also or None}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -766,7 +787,9 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="strings in the dataset (default: the config's full size)")
     ap.add_argument("--cpu-sample", type=int, default=1 << 21)
     ap.add_argument("--ref-sample", type=int, default=1 << 21)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    # e2e batches per timed call: the pipeline's first H2D and last D2H are not
+    # overlapped, so a few more batches than 3 show the steady state
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-also", action="store_true")
