@@ -301,7 +301,8 @@ void launch_fix_staged(int coder, const uint2 *list_sm, uint64_t cap_sm, const D
 // two-string runs at 2^30 strings; a warp each left most lanes idle.
 template <int CODER>
 __device__ __forceinline__ void fix_tiny(uint32_t start, uint32_t len, uint32_t *perm, const void *units,
-                                         const int64_t *offsets, const RunRule &rule, bool general) {
+                                         const int64_t *offsets, const RunRule &rule, bool general,
+                                         void *sorted_units, int64_t *sorted_offsets) {
   uint32_t id[kTinyMax], rank[kTinyMax];
   int64_t o[kTinyMax], l[kTinyMax];
 #pragma unroll
@@ -331,6 +332,22 @@ __device__ __forceinline__ void fix_tiny(uint32_t start, uint32_t len, uint32_t 
 #pragma unroll
   for (uint32_t i = 0; i < kTinyMax; ++i)
     if (i < len) perm[start + rank[i]] = id[i];
+  if (sorted_units) {
+    // the main pass: the run's span in the sorted strings (its base and total
+    // length are unchanged), rewritten in the new order -- no re-gather needed
+    constexpr int W = CoderTraits<CODER>::kUnitBytes;
+    const uint64_t base = (uint64_t)sorted_offsets[start];
+#pragma unroll
+    for (uint32_t i = 0; i < kTinyMax; ++i) {
+      if (i >= len) continue;
+      uint64_t d = base;
+#pragma unroll
+      for (uint32_t k = 0; k < kTinyMax; ++k)
+        if (k < len && rank[k] < rank[i]) d += (uint64_t)l[k];
+      sorted_offsets[start + rank[i]] = (int64_t)d;
+      copy_units<W>((const uint8_t *)units, o[i], (uint8_t *)sorted_units, d, (uint64_t)l[i]);
+    }
+  }
 }
 
 // Small dirty runs (<= kSmallMax strings): each lane takes one list entry;
@@ -341,10 +358,9 @@ template <int CODER>
 __global__ void __launch_bounds__(256)
     k_fix_small(const uint2 *__restrict__ list, const DevState *st, uint32_t *perm,
                 const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t first,
-                const int64_t *__restrict__ so) {
+                void *sorted_units, int64_t *sorted_offsets) {
   pdl_wait();
   if (st->violations & kOffsetsBad) return;
-  (void)so;  // small runs are never staged
   const uint32_t lane = lane_id();
   const RunRule rule = run_rule<CODER>(st);
   const uint32_t nsmall = st->n_small;
@@ -353,7 +369,8 @@ __global__ void __launch_bounds__(256)
   for (uint32_t b = first + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; b < nsmall; b += warps * 32) {
     const uint32_t e = b + lane;
     const uint2 mine = e < nsmall ? list[e] : make_uint2(0, 0);
-    if (mine.y >= 2 && mine.y <= kTinyMax) fix_tiny<CODER>(mine.x, mine.y, perm, units, offsets, rule, general);
+    if (mine.y >= 2 && mine.y <= kTinyMax)
+      fix_tiny<CODER>(mine.x, mine.y, perm, units, offsets, rule, general, sorted_units, sorted_offsets);
     uint32_t big = __ballot_sync(0xFFFFFFFFu, mine.y > kTinyMax);
     while (big) {
       const int src = __ffs(big) - 1;
@@ -424,13 +441,15 @@ __global__ void __launch_bounds__(1024)
 
 void launch_fix_small(int coder, const uint2 *list_sm, const DevState *st, uint32_t *perm,
                       const void *units, const int64_t *offsets, int num_sms, cudaStream_t s, uint32_t first,
-                      const int64_t *staged_so) {
+                      void *sorted_units, int64_t *sorted_offsets) {
   Scope sc_(ST_FIX_SMALL, s, 0);
   dim3 g(num_sms * 4), b(256);
   if (coder == HUSKY_CODER_ASCII)
-    launch_pdl(k_fix_small<HUSKY_CODER_ASCII>, g, b, 0, s, list_sm, st, perm, units, offsets, first, staged_so);
+    launch_pdl(k_fix_small<HUSKY_CODER_ASCII>, g, b, 0, s, list_sm, st, perm, units, offsets, first, sorted_units,
+               sorted_offsets);
   else
-    launch_pdl(k_fix_small<HUSKY_CODER_UNICODE>, g, b, 0, s, list_sm, st, perm, units, offsets, first, staged_so);
+    launch_pdl(k_fix_small<HUSKY_CODER_UNICODE>, g, b, 0, s, list_sm, st, perm, units, offsets, first,
+               sorted_units, sorted_offsets);
 }
 
 void launch_fix_medium(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,

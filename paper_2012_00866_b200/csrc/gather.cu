@@ -655,18 +655,9 @@ void launch_unpack_perm(uint32_t *perm, uint64_t n, cudaStream_t s) {
 // are unchanged; only the order inside moves).  Small runs: a lane each when
 // they hold <= kTinyMax strings, else a warp (lane per string); medium runs:
 // a CTA each.  (One CTA per two-string run left 255 of 256 threads idle: 7.3 ms
-// for the ~10^6 such runs of a 2^30 partial key sort.)
-template <int W>
-__device__ __forceinline__ void copy_units(const uint8_t *ub, int64_t o, uint8_t *ob, uint64_t d, uint64_t L) {
-  const uint64_t nb = L * W;
-  const uint8_t *sp = ub + o * W;
-  uint8_t *dp = ob + d * W;
-  for (uint64_t q = 0; q < nb; q += 8) {
-    int take = (int)(nb - q < 8 ? nb - q : 8);
-    uint64_t v = load8_unaligned(sp + q, take);
-    for (int b = 0; b < take; ++b) dp[q + b] = (uint8_t)(v >> (8 * b));
-  }
-}
+// for the ~10^6 such runs of a 2^30 partial key sort.)  skip_staged (the main
+// pass): runs fix_tiny already wrote back and medium runs k_fix_staged sorted
+// in place are skipped.
 
 template <int CODER>
 __global__ void __launch_bounds__(256)
@@ -687,7 +678,7 @@ __global__ void __launch_bounds__(256)
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
   for (uint32_t b = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; b < ns; b += nw * 32) {
     const uint2 mine = b + lane < ns ? list[first_small + b + lane] : make_uint2(0, 0);
-    if (mine.y <= kTinyMax) {
+    if (mine.y <= kTinyMax && !skip_staged) {  // (main pass: fix_tiny wrote them)
       uint64_t d = mine.y ? (uint64_t)sorted_offsets[mine.x] : 0;
       for (uint32_t k = 0; k < mine.y; ++k) {
         const uint32_t i = perm[mine.x + k];

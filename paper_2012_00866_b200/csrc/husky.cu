@@ -238,7 +238,7 @@ static husky_status enqueue_main(Sorter &S, const MainFlags &F, void *d_sorted_u
   // mode) take the global-memory kernels and the re-gather
   if (d_sorted_units)
     launch_fix_staged(kc, list_sm, L.cap_sm, st, d_perm, d_sorted_units, d_sorted_offsets, S.sms, s);
-  launch_fix_small(kc, list_sm, st, d_perm, d_units, d_offsets, S.sms, s, 0, d_sorted_offsets);
+  launch_fix_small(kc, list_sm, st, d_perm, d_units, d_offsets, S.sms, s, 0, d_sorted_units, d_sorted_offsets);
   launch_fix_medium(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s, 0, d_sorted_offsets);
   if (d_sorted_units)
     launch_regather_runs(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, d_sorted_units,

@@ -443,6 +443,20 @@ __device__ __forceinline__ uint64_t stage_load8(const uint8_t *stage, uint32_t o
   return (uint64_t)__funnelshift_r(x0, x1, sh) | ((uint64_t)__funnelshift_r(x1, x2, sh) << 32);
 }
 
+// Copy one string's units (L units of W bytes) from ub + o*W to ob + d*W:
+// unaligned 8-byte loads, byte stores.
+template <int W>
+__device__ __forceinline__ void copy_units(const uint8_t *ub, int64_t o, uint8_t *ob, uint64_t d, uint64_t L) {
+  const uint64_t nb = L * W;
+  const uint8_t *sp = ub + o * W;
+  uint8_t *dp = ob + d * W;
+  for (uint64_t q = 0; q < nb; q += 8) {
+    int take = (int)(nb - q < 8 ? nb - q : 8);
+    uint64_t v = load8_unaligned(sp + q, take);
+    for (int b = 0; b < take; ++b) dp[q + b] = (uint8_t)(v >> (8 * b));
+  }
+}
+
 // Exact comparator with no assumption on the codes (general cleanup, NEXT-4):
 // units from 0, a proper prefix first, then the index.
 template <int CODER>

@@ -121,9 +121,12 @@ void launch_runs_classify(const uint32_t *run_start, const uint32_t *run_end, co
 constexpr int kFixStageBytes = 80 * 1024;
 void launch_fix_staged(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st, uint32_t *perm,
                        void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s);
+// sorted_units / sorted_offsets (the main pass with sorted strings): runs of
+// <= kTinyMax strings are also written back into the sorted strings (the
+// re-gather then skips them); NULL in perm-only mode and after a refinement
 void launch_fix_small(int coder, const uint2 *list_sm, const DevState *st, uint32_t *perm,
                       const void *units, const int64_t *offsets, int num_sms, cudaStream_t s, uint32_t first = 0,
-                      const int64_t *staged_so = nullptr);
+                      void *sorted_units = nullptr, int64_t *sorted_offsets = nullptr);
 void launch_fix_medium(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st,
                        uint32_t *perm, const void *units, const int64_t *offsets, int num_sms,
                        cudaStream_t s, uint32_t first = 0, const int64_t *staged_so = nullptr);
