@@ -618,15 +618,18 @@ def run_sharded(args, h, torch, dev, rank, world):
         times, bad_pairs, hash_ok = [], 0, True
         dist.barrier() if world > 1 else None
         torch.cuda.synchronize()
+        launches = 0
         with ClockSampler(dev.index or 0) as clk:
             for i in range(steps):
                 flush.fill_(i & 0xFF)
                 if world > 1:
                     dist.barrier()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                l0 = h.husky_launch_count()
                 a.record(stream)
                 outs = h.sort_multi(comm, coder, u, o, base)
                 b.record(stream)
+                launches += h.husky_launch_count() - l0
                 torch.cuda.synchronize()
                 times.append(a.elapsed_time(b))
                 # validation: pairs inside the shard, order across shard
@@ -650,11 +653,28 @@ def run_sharded(args, h, torch, dev, rank, world):
         torch.cuda.synchronize()
         h.husky_profile_enable(False)
         stages = {}
-        for st_name, _, ms in h.husky_profile_launches():
+        plog = h.husky_profile_launches()
+        for st_name, _, ms in plog:
             e = stages.setdefault(st_name, {"ms": 0.0, "launches": 0})
             e["ms"] = round(e["ms"] + ms, 4)
             e["launches"] += 1
         p, su, so, outc = outs
+        # roofline of the dominant kernel, the local sort's radix pass (this
+        # rank's received strings), from the profiled step's per-launch times
+        n_out = int(p.numel())
+        rp = [ms for st_name, el, ms in plog if st_name == "radix_pass" and el == n_out and n_out > 0]
+        passes = int(outc["keys_partitioned"]) // n_out if n_out else 0
+        rp = rp[:passes]
+        roof = None
+        if rp:
+            peak, peak_src = peaks()
+            t = statistics.mean(rp)
+            bytes_alg = 24 * n_out
+            roof = {"kernel": "k_onesweep (A2 radix pass, local sort of rank 0)", "bound": "hbm",
+                    "achieved": round(bytes_alg / (t * 1e-3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(bytes_alg / (t * 1e-3) / 1e9 / peak, 4), "traffic": None,
+                    "ms_per_launch": round(t, 4), "passes_per_sort": passes, "peak_source": peak_src,
+                    "timing": "profiled step (an event pair per launch), outside the timed steps"}
         # boundary check: this shard's last string < the next shard's first
         ends = [None, None]
         if p.numel():
@@ -686,6 +706,7 @@ def run_sharded(args, h, torch, dev, rank, world):
                "validation": {"pairs": int(bp.item()), "boundaries": boundary_bad, "multiset_hash_equal": hash_ok,
                               "steps": steps},
                "outcome": outc, "clocks": clk.summary(), "stages_rank0": stages,
+               "gpu_launches": launches // max(steps, 1), "roofline": roof,
                "nvlink": {"bytes_to_peers_max_rank": int(to.item()),
                           "note": "string bytes + 8 B per string a rank sends to other ranks (peer stores into the "
                                   "destinations' NCCL windows); exchange time in stages.multi"}}
@@ -745,7 +766,8 @@ def run_sharded(args, h, torch, dev, rank, world):
                            "parallelism": f"sample sort over {world} GPU(s), one dataset sharded by global index",
                            "timing": "per step: max over ranks of the CUDA-event time; median over steps",
                            "l2": "inputs > L2; a 256 MiB buffer is also written between timed steps"},
-                "roofline": None, "cpu_baseline": None, "e2e": main.get("e2e"), "gpu_launches": None,
+                "roofline": main["roofline"], "cpu_baseline": None, "e2e": main.get("e2e"),
+                "gpu_launches": main["gpu_launches"],
                 "clocks": main["clocks"], "validation": main["validation"], "nvlink": main["nvlink"],
                 "stages": main["stages_rank0"],
                 "outcome": main["outcome"], "also": also or None}

@@ -140,7 +140,10 @@ void launch_seg_key2(int coder, const uint32_t *perm_seg, uint64_t len, const vo
 
 // A4 gather
 // small tiles, many CTAs: the gather is bound by the latency of random reads
-constexpr int kGatherThreads = 256, kGatherItems = 4, kGatherTile = kGatherThreads * kGatherItems;
+#ifndef HUSKY_GATHER_ITEMS
+#define HUSKY_GATHER_ITEMS 4
+#endif
+constexpr int kGatherThreads = 256, kGatherItems = HUSKY_GATHER_ITEMS, kGatherTile = kGatherThreads * kGatherItems;
 constexpr int kGatherStage = 24 * 1024;  // one window of output bytes (dynamic smem)
 inline uint64_t gather_tiles(uint64_t n) { return (n + kGatherTile - 1) / kGatherTile; }
 // base_ptr (nullable): device pointer to the first output offset of a span
