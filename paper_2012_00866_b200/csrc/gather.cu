@@ -67,6 +67,9 @@ template <int CODER, bool PACKED, bool CHECK, bool PEER>
 // resident CTAs per SM: 5 for the packed instantiations (48 registers; C2
 // 280 vs 289 us at 4), 4 for the others (64 registers, no spills: the C5 gather
 // with slab records 50 -> 44 ms)
+#ifndef HUSKY_GATHER_CPASYNC
+#define HUSKY_GATHER_CPASYNC 1
+#endif
 #ifndef HUSKY_GATHER_MINB
 #define HUSKY_GATHER_MINB (PACKED ? 5 : 4)
 #endif
@@ -158,9 +161,23 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   uint4 *s_slab = reinterpret_cast<uint4 *>(stage + kGatherStage + 32);
   uint32_t dec = 0, slb = 0;
   unsigned long long mine = 0;
+  // the main gather with slab records: every item's record goes straight to
+  // its shared-memory park by cp.async (no register round trip, so the
+  // records of all items are in flight at once; C5 gather 37.4 -> 36.0 ms)
+  constexpr bool kRecAsync = HUSKY_GATHER_CPASYNC && CHECK;
+  if (kRecAsync && slab != nullptr) {
+#pragma unroll
+    for (int j = 0; j < kGatherItems; ++j)  // (packed: strings longer than PL only -- the others need no record)
+      if (p0 + j < n && (!PACKED || (raw[j] >> 28) > PL))
+        cp_async16(&s_slab[j * kGatherThreads + tid], slab + (PACKED ? (raw[j] & 0x0FFFFFFFu) : raw[j]));
+    cp_async_commit();
+#pragma unroll
+    for (int j = 0; j < kGatherItems; ++j) cc[j] = p0 + j < n ? __ldg(codes + p0 + j) : 0ull;
+    cp_async_wait_all();
+  }
 #pragma unroll
   for (int j = 0; j < kGatherItems; ++j) {
-    cc[j] = 0;
+    if (!kRecAsync || slab == nullptr) cc[j] = 0;
     ix[j] = 0;
     if (p0 + j >= n) {
       sv[j] = 0;
@@ -173,17 +190,18 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
         perm[p0 + j] = idx;
       }
       ix[j] = idx;
-      if (CHECK) cc[j] = __ldg(codes + p0 + j);
+      if (CHECK && !(kRecAsync && slab != nullptr)) cc[j] = __ldg(codes + p0 + j);
       uint4 rec = make_uint4(0xFFu, 0, 0, 0);
       if (PACKED && lc <= PL) {
         dec |= 1u << j;
         len[j] = lc;
         sv[j] = CHECK ? cc[j] : __ldg(codes + p0 + j);
-      } else if (CHECK && slab != nullptr && (rec = __ldg(slab + idx), (rec.x & 0xFFu) != 0xFFu)) {
+      } else if (CHECK && slab != nullptr &&
+                 (rec = kRecAsync ? s_slab[j * kGatherThreads + tid] : __ldg(slab + idx), (rec.x & 0xFFu) != 0xFFu)) {
         slb |= 1u << j;
         len[j] = rec.x & 0xFFu;
         sv[j] = cc[j];
-        s_slab[j * kGatherThreads + tid] = rec;
+        if (!kRecAsync) s_slab[j * kGatherThreads + tid] = rec;
       } else {
         const int64_t a = __ldg(offsets + idx);
         sv[j] = (uint64_t)a;

@@ -1,0 +1,7 @@
+timeout 2400 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "^(FAILED|E  )|passed|failed" | head -20
+for lib in default lab/nca/; do
+  if [ "$lib" = default ]; then unset HUSKY_LIB; else export HUSKY_LIB=$PWD/${lib}libhusky.so; fi
+  timeout 300 python tools/c5_probe.py 30 2 C5 2>&1 | tail -1
+  timeout 300 python tools/c5_probe.py 27 3 C5 2>&1 | tail -1
+  HUSKY_SLAB=1 timeout 300 python tools/c5_probe.py 23 3 C2 2>&1 | tail -1
+done
