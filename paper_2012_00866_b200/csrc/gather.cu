@@ -221,15 +221,6 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
     }
     mine += len[j];
   }
-  // CHECK, thread 0: the previous tile's last string (the tile-boundary pair),
-  // its dependent loads issued here so they overlap the scan and the staging
-  unsigned long long b_code = 0;
-  uint32_t b_idx = 0, b_len = 0;
-  if (CHECK && tid == 0 && p0 > 0) {
-    b_code = __ldg(codes + p0 - 1);
-    b_idx = perm[p0 - 1] & (PACKED ? 0x0FFFFFFFu : 0xFFFFFFFFu);  // unpacked or not yet
-    b_len = (uint32_t)(__ldg(offsets + b_idx + 1) - __ldg(offsets + b_idx));
-  }
   // CHECK: run flags.  eqp bit j: position p0+j equals its predecessor; eqn:
   // equals its successor (neighbours across lanes by shuffles, across warps and
   // tiles from global memory)
@@ -250,6 +241,16 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       eqn |= (uint32_t)en << j;
       nstart += (!ep && en);
     }
+  }
+  // CHECK, thread 0: the previous tile's last string when it has this tile's
+  // first code (the tile-boundary pair is then checked); its dependent loads
+  // issued here so they overlap the scan and the staging
+  unsigned long long b_code = 0;
+  uint32_t b_idx = 0, b_len = 0;
+  if (CHECK && tid == 0 && (eqp & 1u)) {
+    b_code = __ldg(codes + p0 - 1);
+    b_idx = perm[p0 - 1] & (PACKED ? 0x0FFFFFFFu : 0xFFFFFFFFu);  // unpacked or not yet
+    b_len = (uint32_t)(__ldg(offsets + b_idx + 1) - __ldg(offsets + b_idx));
   }
   // one scan for both: units in the low 48 bits, run starts above
   unsigned long long tile_total;
