@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(256)
   }
   for (uint32_t e = blockIdx.x; e < nm; e += gridDim.x) {
     uint2 ent = list[cap - 1 - (first_medium + e)];
-    const uint32_t start = ent.x, len = ent.y;
+    const uint32_t start = ent.x, len = ent.y & ~kRunDone;
     // medium runs k_fix_staged sorted and wrote back in place (fixup.cu)
     if (skip_staged && st->trivial_mask != 0xFFu &&
         (uint64_t)(sorted_offsets[start + len] - sorted_offsets[start]) * W <= (uint64_t)kFixStageBytes)

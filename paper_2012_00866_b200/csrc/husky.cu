@@ -236,8 +236,8 @@ static husky_status enqueue_main(Sorter &S, const MainFlags &F, void *d_sorted_u
   // with sorted strings, runs whose units fit the stage are sorted in shared
   // memory and written back in place (k_fix_staged); the others (and perm-only
   // mode) take the global-memory kernels and the re-gather
-  if (d_sorted_units)
-    launch_fix_staged(kc, list_sm, L.cap_sm, st, d_perm, d_sorted_units, d_sorted_offsets, S.sms, s);
+  launch_fix_staged(kc, list_sm, L.cap_sm, st, d_perm, d_sorted_units, d_sorted_units ? d_sorted_offsets : nullptr,
+                    S.sms, s, d_units, d_offsets);
   launch_fix_small(kc, list_sm, st, d_perm, d_units, d_offsets, S.sms, s, 0, d_sorted_units, d_sorted_offsets);
   launch_fix_medium(kc, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s, 0, d_sorted_offsets);
   if (d_sorted_units)
@@ -555,6 +555,7 @@ static husky_status refine_giants(Sorter &S, const DevState &hs0, void *d_sorted
 
   // ---- A5 fix-up of the small / medium sub-runs the refinement appended
   launch_fix_small(coder, list_sm, st, d_perm, d_units, d_offsets, S.sms, s, s0);
+  launch_fix_staged(coder, list_sm, L.cap_sm, st, d_perm, nullptr, nullptr, S.sms, s, d_units, d_offsets, m0);
   launch_fix_medium(coder, list_sm, L.cap_sm, st, d_perm, d_units, d_offsets, S.sms, s, m0);
   debug_check_perm(d_perm, n, "refine fix-up", s);
 

@@ -52,6 +52,9 @@ template <> struct CoderTraits<HUSKY_CODER_ENGLISH6> {
 
 constexpr int kSmallMax = 32;    // dirty runs up to this many strings: one warp
 constexpr uint32_t kTinyMax = 4; // ... and up to this many: one thread
+// medium-list entry flag (length field): the run was sorted by the
+// gather-staged fix-up (perm-only mode / after a refinement)
+constexpr uint32_t kRunDone = 0x80000000u;
 constexpr int kMediumMax = 4096; // ... up to this many: one CTA (bitonic in smem)
 
 // violation bits (OR-reduced; zero-initialised state)

@@ -119,8 +119,12 @@ void launch_runs_classify(const uint32_t *run_start, const uint32_t *run_end, co
 // the sorted offsets), else they take every run (staged_so NULL).  Small runs
 // always take k_fix_small.
 constexpr int kFixStageBytes = 80 * 1024;
+// sorted_units NULL (perm-only mode, sub-runs after a refinement): the runs'
+// strings are gathered into the stage from units / offsets, only perm is
+// written back and handled entries get length 0 (entries [first, n_medium))
 void launch_fix_staged(int coder, const uint2 *list_sm, uint64_t cap_sm, const DevState *st, uint32_t *perm,
-                       void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s);
+                       void *sorted_units, int64_t *sorted_offsets, int num_sms, cudaStream_t s,
+                       const void *units = nullptr, const int64_t *offsets = nullptr, uint32_t first = 0);
 // sorted_units / sorted_offsets (the main pass with sorted strings): runs of
 // <= kTinyMax strings are also written back into the sorted strings (the
 // re-gather then skips them); NULL in perm-only mode and after a refinement

@@ -648,6 +648,9 @@ def test_staged_fixup_dirty_runs(torch, h, oracle_mod, coder, gmax, smax):
     w = W.d1(150_000, group_min=min(100, gmax), group_max=gmax, suffix_max=smax, coder=coder)
     outc = check_against_oracle(torch, h, oracle_mod, w)
     assert outc["runs_by_class"][0] < outc["n_runs"]  # the runs were dirty
+    # perm-only mode: the runs' strings are gathered into the stage from the
+    # input (perm -> offsets -> units) and only perm is written back
+    check_against_oracle(torch, h, oracle_mod, w, with_units=False)
 
 
 def test_staged_fixup_ties_nul_and_prefixes(torch, h, oracle_mod):
@@ -662,6 +665,27 @@ def test_staged_fixup_ties_nul_and_prefixes(torch, h, oracle_mod):
     perm = rng.permutation(len(strings))
     w = W.from_strings([strings[p] for p in perm], ASCII)
     check_against_oracle(torch, h, oracle_mod, w)
+    check_against_oracle(torch, h, oracle_mod, w, with_units=False)
+
+
+@pytest.mark.parametrize("with_units", [True, False])
+def test_refinement_medium_subruns(torch, h, oracle_mod, with_units):
+    """A giant run (every code equal) whose refinement leaves medium sub-runs
+    (groups of 100..3000 strings equal on the 7-unit refinement window and
+    dirty past it): the sub-runs take the gather-staged fix-up, then the span
+    is gathered again (with sorted strings)."""
+    rng = np.random.default_rng(17)
+    strings = []
+    while len(strings) < 40_000:
+        g = int(rng.integers(100, 3000))
+        head = [0x61] * 12 + rng.integers(0x61, 0x7B, size=7).tolist()
+        for _ in range(g):
+            strings.append(head + rng.integers(0x61, 0x7B, size=int(rng.integers(1, 9))).tolist())
+    strings = strings[:40_000]
+    perm = rng.permutation(len(strings))
+    w = W.from_strings([strings[p] for p in perm], ASCII)
+    outc = check_against_oracle(torch, h, oracle_mod, w, with_units=with_units)
+    assert outc["refine_rounds"] >= 1
 
 
 # ------------------------------------- partial key sort (lowest digit unsorted)
