@@ -11,8 +11,8 @@
 // no faster).
 // A pass works on tiles of kRadixTile = 6144 keys (512 threads x 12, warp-striped so every
 // load/store instruction is a coalesced 256-B access).  Each tile is ranked in
-// shared memory with warp-level label matching (three __match_any_sync on the
-// digit's 3 + 3 + 2 bits) + popc into per-warp digit counters, exchanged
+// shared memory with warp-level peer masks (one __match_any_sync on the high 3
+// bits of the digit, a ballot per low bit) + popc into per-warp digit counters, exchanged
 // through shared memory into digit order, and written out as runs of
 // consecutive addresses.  The tile's global base per digit comes from a
 // per-(tile, digit) decoupled look-back (onesweep, Adinets & Merrill) on top of
@@ -210,6 +210,13 @@ void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *
 }
 
 constexpr int kRadixWarps = kRadixThreads / 32;
+// ranking: ballots on the low kRankBallots bits of the digit, one label match
+// on the rest
+#ifndef HUSKY_RANK_BALLOTS
+#define HUSKY_RANK_BALLOTS 5
+#endif
+constexpr int kRankBallots = HUSKY_RANK_BALLOTS;
+
 // Look-back window: predecessors read per round trip (4 / 8 / 12
 // / 16 measured, 12 fastest with the 6144-key tiles)
 #ifndef RADIX_LB_W
@@ -309,17 +316,23 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   const bool is_dg = tid < R;  // threads 0..R-1 own one digit each
   const uint32_t dg = tid & MASK;
 
-  // ---- warp-level match ranking into per-warp counters (stable: (r, lane)
-  // order).  The cost of __match_any_sync grows with the number of distinct
-  // labels in the warp, so the digit is matched as three pieces of 3 + 3 + 2
-  // bits and the peer masks ANDed (fastest of the variants
-  // measured -- one 8-bit match, 4 + 4, 2 + 2 + 2 + 2, per-bit ballots, mixes).
+  // ---- warp-level ranking into per-warp counters (stable: (r, lane) order)
   uint16_t *wc = cnt + warp * R;
 #pragma unroll
   for (int r = 0; r < ITEMS; ++r) {
     uint32_t d = (uint32_t)(k[r] >> shift) & MASK;
-    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> 5) & __match_any_sync(0xFFFFFFFFu, (d >> 2) & 7u) &
-                     __match_any_sync(0xFFFFFFFFu, d & 3u);
+    // lanes with the same digit: one label match on the high bits, a ballot
+    // per low bit (a match costs more the more distinct labels a warp holds, a
+    // ballot one vote; measured, C5 / C2 radix per sort: 3 + 3 + 2-bit matches
+    // 40.3 / 0.430 ms, match + 4 ballots 38.8 / 0.423, + 5 ballots 38.4 /
+    // 0.436, + 6 39.2 / 0.451, 8 ballots 40.5 / 0.473; a per-digit choice made
+    // at run time cost more than it saved)
+    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d >> kRankBallots);
+#pragma unroll
+    for (int b = 0; b < kRankBallots; ++b) {
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bal : ~bal;
+    }
     if (r == 0) HT(tile, 1);
     uint32_t pre = wc[d];
     rk[slot0 + r * 32] = (uint16_t)(pre + __popc(peers & lanemask_lt()));
