@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   const bool general = st->general != 0;
   // compare from unit S (equal codes fix units [0, S)), or from 0 off-domain
   const RunRule rule = run_rule<CODER>(st);
-  const uint32_t kstart = general ? 0u : rule.S * W;
+  const uint32_t kstart0 = general ? 0u : rule.S * W;
   // medium runs only: runs of <= 32 strings go to k_fix_small (a warp each;
   // a CTA-wide staged sort per 2-string run measured 0.8 ms for the ~10K
   // extra pairs of a partial key sort at 2^30)
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   __syncthreads();
   uint32_t phase = 0;
   const bool bulk_ok = ((uintptr_t)su & 15) == 0;
-  const FixLess less{stage, soff, sgid, kstart, (uint32_t)W};
+  __shared__ uint32_t s_lcp;
 #ifdef HUSKY_FIX_TIMING
   long long ft_last = clock64();
 #endif
@@ -230,6 +230,38 @@ __global__ void __launch_bounds__(kFixThreads, 1)
       phase ^= (a1 > a0) ? 1u : 0u;
       __syncthreads();
     }
+    // ---- the run's common prefix: every string agrees with string 0 on its
+    // first lcp bytes, so keys and compares start there (strings of a dirty
+    // run often share more than the S units their codes fix, e.g. URLs)
+    if (threadIdx.x == 0) s_lcp = 0xFFFFFFFFu;
+    __syncthreads();
+    {
+      uint32_t my = 0xFFFFFFFFu;
+      const uint32_t o0 = soff[0], l0 = soff[1] - soff[0];
+#pragma unroll
+      for (int j = 0; j < kFixItems; ++j) {
+        const uint32_t i = threadIdx.x * kFixItems + j;
+        if (i >= len || i == 0) continue;
+        const uint32_t oi = soff[i], li = soff[i + 1] - oi, m = li < l0 ? li : l0;
+        uint32_t cp = m;
+        for (uint32_t k = kstart0; k < m; k += 8) {
+          uint64_t x = stage_load8(stage, oi + k) ^ stage_load8(stage, o0 + k);
+          const uint32_t take = m - k < 8 ? m - k : 8;
+          if (take < 8) x &= (1ull << (8 * take)) - 1;
+          if (x) {
+            cp = k + (uint32_t)((__ffsll((long long)x) - 1) >> 3);
+            break;
+          }
+        }
+        my = cp < my ? cp : my;
+      }
+      my = __reduce_min_sync(0xFFFFFFFFu, my);
+      if (lane_id() == 0 && my != 0xFFFFFFFFu) atomicMin(&s_lcp, my);
+    }
+    __syncthreads();
+    const uint32_t lcp = s_lcp == 0xFFFFFFFFu ? 0u : (s_lcp / W) * W;  // whole units
+    const uint32_t kstart = lcp > kstart0 ? lcp : kstart0;
+    const FixLess less{stage, soff, sgid, kstart, (uint32_t)W};
     FT(0);
     // ---- sort items, blocked: thread t holds strings 8t .. 8t + 7
     uint64_t item[kFixItems];

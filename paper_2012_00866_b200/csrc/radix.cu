@@ -63,9 +63,16 @@ constexpr int kHistBlocksPerSM = 4;  // resident CTAs of 512 threads per SM
 // 0 = never.  def_s / def_pl: the
 // coder's run rule when nothing is skipped.
 #ifndef HUSKY_SKIP2_BAR
-#define HUSKY_SKIP2_BAR 4e-3f
+#define HUSKY_SKIP2_BAR 1e-2f
 #endif
 constexpr float kSkip2Bar = HUSKY_SKIP2_BAR;
+// one pass costs ~7 ps per key at 2^30 (C5), one extra dirty run ~0.8 ns: the
+// break-even is ~0.02 n extra pairs per pass saved; the bars stay below it
+// because the estimate assumes independent digits
+#ifndef HUSKY_SKIP1_BAR
+#define HUSKY_SKIP1_BAR 5e-3f
+#endif
+constexpr float kSkip1Bar = HUSKY_SKIP1_BAR;
 template <bool PLAN>
 __global__ void __launch_bounds__(512) k_hist_slots(uint64_t *__restrict__ keys, uint64_t n, DevState *st,
                                                     uint64_t *keysA, uint64_t *keysB, int compress, int skip,
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(512) k_hist_slots(uint64_t *__restrict__ keys,
         // one more pass costs ~24 B per key, one extra pair a check and at
         // worst a two-string fix-up, so the bar is a small fraction of n
         const float extra = 0.5f * (float)n * (float)n * exp2f(-hhi);
-        const float bar = (k == 1 ? 1e-4f : kSkip2Bar) * (float)n;
+        const float bar = (k == 1 ? kSkip1Bar : kSkip2Bar) * (float)n;
         if (sp >= 1 && (skip >= 2 || extra < bar)) {
           for (uint32_t i = 0; i + k < np; ++i) dig[i] = dig[i + k];
           np -= k;
