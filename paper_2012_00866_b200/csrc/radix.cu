@@ -224,10 +224,11 @@ constexpr int kRadixWarps = kRadixThreads / 32;
 #endif
 constexpr int kRankBallots = HUSKY_RANK_BALLOTS;
 
-// Look-back window: predecessors read per round trip (4 / 8 / 12
-// / 16 measured, 12 fastest with the 6144-key tiles)
+// Look-back window: predecessors read per round trip (with the ballot
+// ranking, C5 radix per sort: 6 / 8 / 10 / 12 / 16 -> 38.16 / 38.22 / 38.75 /
+// 38.43 / 43.2 ms; C2 flat)
 #ifndef RADIX_LB_W
-#define RADIX_LB_W 12
+#define RADIX_LB_W 6
 #endif
 
 #ifdef HUSKY_TIMING
