@@ -43,3 +43,10 @@ def test_c5_above_2p28(oracle_mod):
     for k in np.random.default_rng(3).integers(0, n, size=2000):
         i = hp[k]
         assert np.array_equal(hsu[ref_so[k]:ref_so[k + 1]], hu[ho[i]:ho[i + 1]])
+    # perm-only mode at the same size (the run scan and the gather-staged
+    # fix-up instead of the gather): the unique order, so the same perm
+    del su, so
+    torch.cuda.empty_cache()
+    perm2, _, _, _ = h.sort(0, u, o, with_units=False)
+    torch.cuda.synchronize()
+    assert torch.equal(perm2[:n], perm[:n])
