@@ -95,6 +95,9 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   __shared__ uint8_t s_unrank[64];
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   pdl_wait();  // the main gather is a programmatic dependent of the key sort
+  // the tile id first: its round trip overlaps the DevState reads below (a
+  // CTA that then returns on invalid input returns with every other CTA)
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   uint32_t cbits = 0;
   bool ccomp = false;
   if (CODER == HUSKY_CODER_ASCII && (PACKED || CHECK) && st && st->ccomp) {
@@ -120,7 +123,6 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
     if (st->violations & kOffsetsBad) return;  // invalid input: reported by the caller
     if ((PACKED || CHECK) && codes == nullptr) codes = reinterpret_cast<const uint64_t *>(st->sorted_keys);
   }
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   // re-gather of a span: output positions start at *base_ptr (unchanged by us)
   const unsigned long long gbase = base_ptr ? (unsigned long long)*base_ptr : 0ull;
   __syncthreads();
