@@ -697,9 +697,17 @@ def run_sharded(args, h, torch, dev, rank, world):
             prev = e[1]
         bp = torch.tensor([bad_pairs], device=dev)
         to = torch.tensor([outc["bytes_to_peers"]], dtype=torch.float64, device=dev)
+        # the exchange kernel (the partition-order gather storing into the
+        # peers' windows): the profiled step's "multi" launch over the n_loc
+        # local strings; bandwidth = this rank's bytes to peers / its time
+        xch = [ms for st_name, el, ms in plog if st_name == "multi" and el == n_loc and n_loc > 0]
+        xms = float(xch[0]) if xch else 0.0
+        xgbs = torch.tensor([outc["bytes_to_peers"] / (xms * 1e-3) / 1e9 if xms > 0 else 0.0, xms],
+                            dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(bp)
             dist.all_reduce(to, op=dist.ReduceOp.MAX)
+            dist.all_reduce(xgbs, op=dist.ReduceOp.MIN)
         med = statistics.median(times)
         res = {"n_total": n_tot, "value": round(n_tot / (med * 1e-3) / 1e6, 4), "ms_per_step": round(med, 4),
                "ms_min": round(min(times), 4), "ms_mean": round(statistics.mean(times), 4),
@@ -708,8 +716,12 @@ def run_sharded(args, h, torch, dev, rank, world):
                "outcome": outc, "clocks": clk.summary(), "stages_rank0": stages,
                "gpu_launches": launches // max(steps, 1), "roofline": roof,
                "nvlink": {"bytes_to_peers_max_rank": int(to.item()),
+                          "exchange_ms_rank0": round(xms, 4),
+                          "achieved_gbs_min_rank": round(float(xgbs[0].item()), 1), "peak_gbs": 900.0,
+                          "frac": round(float(xgbs[0].item()) / 900.0, 4),
                           "note": "string bytes + 8 B per string a rank sends to other ranks (peer stores into the "
-                                  "destinations' NCCL windows); exchange time in stages.multi"}}
+                                  "destinations' NCCL windows) / the exchange kernel's time (profiled step); "
+                                  "peak: NVLink 5 per direction per GPU"}}
         # e2e: pinned host block in, shard out, every step
         if want_e2e:
             hu = torch.empty(u.numel(), dtype=u.dtype).pin_memory()
