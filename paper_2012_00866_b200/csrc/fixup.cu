@@ -209,6 +209,12 @@ __global__ void __launch_bounds__(kFixThreads, 1)
     const int64_t B0u = GSTAGE ? 0 : so[start], B1u = GSTAGE ? 0 : so[start + len];
     const uint64_t B0 = (uint64_t)B0u * W, B1 = (uint64_t)B1u * W;  // the run's bytes in su
     if (B1 - B0 > (uint64_t)kFixStageBytes) continue;  // left to k_fix_small / k_fix_medium
+#ifdef HUSKY_CHECKED
+    if (threadIdx.x == 0) {
+      HCHK(kChkFixStagedOffsets, (uint64_t)start + len, st->chk_n + 1);
+      HCHK(kChkFixStagedUnits, B1, st->chk_units + 1);
+    }
+#endif
     // ---- stage: bytes [a0, B1) with a0 = B0 rounded down to 16; the aligned
     // body by one bulk copy (TMA engine, completing on the mbarrier), the
     // ragged tail by plain loads
@@ -467,6 +473,7 @@ __global__ void __launch_bounds__(256)
   for (uint32_t b = first + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; b < nsmall; b += warps * 32) {
     const uint32_t e = b + lane;
     const uint2 mine = e < nsmall ? list[e] : make_uint2(0, 0);
+    if (mine.y) HCHK(kChkFixSmallPerm, (uint64_t)mine.x + mine.y, st->chk_n + 1);
     if (mine.y >= 2 && mine.y <= kTinyMax)
       fix_tiny<CODER>(mine.x, mine.y, perm, units, offsets, rule, general, sorted_units, sorted_offsets);
     uint32_t big = __ballot_sync(0xFFFFFFFFu, mine.y > kTinyMax);

@@ -156,6 +156,11 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   uint32_t raw[kGatherItems];
 #pragma unroll
   for (int j = 0; j < kGatherItems; ++j) raw[j] = p0 + j < n ? perm[p0 + j] : 0u;
+#ifdef HUSKY_CHECKED
+  if (st && !PEER)
+    for (int j = 0; j < kGatherItems; ++j)
+      if (p0 + j < n) HCHK(kChkGatherPerm, PACKED ? (raw[j] & 0x0FFFFFFFu) : raw[j], st->chk_n);
+#endif
   uint64_t sv[kGatherItems], cc[kGatherItems];
   uint32_t len[kGatherItems], ix[kGatherItems];
   // slab records parked in shared memory ([item][thread]: conflict-free 16-B
@@ -531,7 +536,10 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
       for (int j = 0; j < kGatherItems; ++j) {
         const bool ep = (eqp >> j) & 1, en = (eqn >> j) & 1;
         const uint32_t p = (uint32_t)(p0 + j);
-        if (!ep && en) runs.run_start[++rid] = p;
+        if (!ep && en) {
+          HCHK(kChkGatherRuns, rid + 1, n);
+          runs.run_start[++rid] = p;
+        }
         if (ep && !en) runs.run_end[rid] = p;
         if ((bad >> j) & 1) runs.dirty[rid] = 1;
       }
@@ -541,6 +549,9 @@ __global__ void __launch_bounds__(kGatherThreads, HUSKY_GATHER_MINB)
   if (!want_units) return;
 
   uint8_t *g0 = ob + tbase * W;  // first output byte of the tile
+#ifdef HUSKY_CHECKED
+  if (st && !PEER && tid == 0) HCHK(kChkGatherUnits, (tbase + tile_total) * W, st->chk_units + 1);
+#endif
   if (!direct) {
     write_window(g0, 0, first_w1);
     for (uint64_t w0 = first_w1; w0 < tile_bytes; w0 += kGatherStage) {  // large tiles: more windows
@@ -706,6 +717,7 @@ __global__ void __launch_bounds__(256)
         const int64_t o = offsets[i];
         const uint64_t L = (uint64_t)(offsets[i + 1] - o);
         sorted_offsets[mine.x + k] = (int64_t)d;
+        HCHK(kChkRegather, (d + L) * W, st->chk_units + 1);
         copy_units<W>(ub, o, ob, d, L);
         d += L;
       }

@@ -23,6 +23,7 @@ struct Layout {
 Layout make_layout(uint64_t n);
 
 husky_status fail(husky_status st, const char *fmt, ...);
+husky_status checked_result(husky_status st, const char *what);  // husky.cu
 
 inline bool valid_coder(int c) { return c >= HUSKY_CODER_ASCII && c <= HUSKY_CODER_ENGLISH6; }
 inline size_t coder_unit_bytes(int c) { return c == HUSKY_CODER_UNICODE ? 2 : (valid_coder(c) ? 1 : 0); }

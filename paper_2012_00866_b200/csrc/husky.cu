@@ -44,6 +44,53 @@ husky_status fail(husky_status st, const char *fmt, ...) {
   return st;
 }
 
+#ifdef HUSKY_CHECKED
+static std::vector<ChkReader> &chk_readers() {
+  static std::vector<ChkReader> *v = new std::vector<ChkReader>;
+  return *v;
+}
+int checked_register(ChkReader r) {
+  chk_readers().push_back(r);
+  return 1;
+}
+unsigned long long checked_take(unsigned long long *first) {
+  cudaDeviceSynchronize();
+  unsigned long long total = 0;
+  for (ChkReader r : chk_readers()) total += r(first);
+  return total;
+}
+#endif
+
+#ifdef HUSKY_CHECKED
+// shrink (HUSKY_CHK_SELFTEST=1): bounds one short, so that a correct sort
+// must report violations -- the check that the checks fire
+__global__ void k_chk_init(DevState *st, const int64_t *offsets, uint64_t n, uint32_t w, uint32_t shrink) {
+  st->chk_n = n - shrink;
+  st->chk_units = (unsigned long long)offsets[n] * w - shrink;
+}
+static uint32_t chk_shrink() {
+  static const uint32_t v = [] {
+    const char *e = getenv("HUSKY_CHK_SELFTEST");
+    return (e && atoi(e) == 1) ? 1u : 0u;
+  }();
+  return v;
+}
+#endif
+
+// checked builds: the violations counted by the kernels of the call that just
+// returned (synchronises the device); always HUSKY_OK otherwise
+husky_status checked_result(husky_status st, const char *what) {
+#ifdef HUSKY_CHECKED
+  unsigned long long first = 0, v = checked_take(&first);
+  if (st == HUSKY_OK && v)
+    return fail(HUSKY_ERR_CUDA, "checked build: %s: %llu out-of-bounds indices (first: site %llu index %llu)", what,
+                v, first >> 48, first & 0xFFFFFFFFFFFFull);
+#else
+  (void)what;
+#endif
+  return st;
+}
+
 int device_sm_count() {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -170,6 +217,9 @@ static husky_status enqueue_main(Sorter &S, const MainFlags &F, void *d_sorted_u
   const int64_t *d_offsets = S.offsets;
   uint32_t *d_perm = S.perm;
   HCHECK(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+#ifdef HUSKY_CHECKED
+  k_chk_init<<<1, 1, 0, s>>>(st, d_offsets, n, (uint32_t)husky_unit_bytes(coder), chk_shrink());
+#endif
   HCHECK(S.reset_lookback());
   // the dirty-run flags the main gather sets (cleared here, not between the key
   // sort and the gather, so the gather stays a programmatic dependent)
@@ -725,8 +775,9 @@ husky_status husky_sort_workspace(int coder, uint64_t n, uint64_t total_units, s
 husky_status husky_sort(int coder, const void *d_units, const int64_t *d_offsets, uint64_t n,
                         uint32_t *d_perm, void *d_sorted_units, int64_t *d_sorted_offsets, void *d_ws,
                         size_t ws_bytes, husky_outcome *h_out, void *stream) {
-  return sort_impl(coder, d_units, d_offsets, n, d_perm, d_sorted_units, d_sorted_offsets, d_ws, ws_bytes,
-                   h_out, (cudaStream_t)stream);
+  return checked_result(sort_impl(coder, d_units, d_offsets, n, d_perm, d_sorted_units, d_sorted_offsets, d_ws,
+                                   ws_bytes, h_out, (cudaStream_t)stream),
+                         "husky_sort");
 }
 
 // host-buffer variant: [device units | device offsets | device perm | sorted units | sorted offsets | sort ws]

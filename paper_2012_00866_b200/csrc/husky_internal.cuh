@@ -103,7 +103,10 @@ struct DevState {
   // a prefix of the other (R6 / R19)
   uint32_t seq_units, short_len;
   unsigned long long key_mask;
-  uint32_t pad[5];
+  uint32_t pad[1];
+  // checked builds (HUSKY_CHECKED): n and the byte end of the units
+  // (offsets[n] x unit bytes) of this sort, the bounds HCHK compares against
+  unsigned long long chk_n, chk_units;
 };
 
 // The run rule kernels apply: by default equal codes fix units [0, S) and the
@@ -491,5 +494,47 @@ __device__ __forceinline__ int cmp_equal_code(const void *units, const int64_t *
   if (c) return c;
   return ia < ib ? -1 : (ia > ib ? 1 : 0);
 }
+
+
+// ---------------------------------------------------------------- checked build
+// HUSKY_NVCC_DEFS=-DHUSKY_CHECKED (a separate lab build, tools/gpu_checked.sh):
+// the kernels' output indices and random-read indices are checked against
+// their bounds and violations counted -- never trapping, so a bad index cannot
+// take the GPU down.  husky_sort / husky_sort_multi_exec then fail with
+// HUSKY_ERR_CUDA and "checked build: ...".  This stands in for
+// compute-sanitizer memcheck, which is closed on this GPU pool
+// (profiles/r02_sanitizer.txt).  Site ids: kChk* below.
+enum : unsigned {
+  kChkRadixScatter = 1, kChkGatherPerm = 2, kChkGatherOffsets = 3, kChkGatherUnits = 4, kChkGatherRuns = 5,
+  kChkFixStagedUnits = 6, kChkFixStagedOffsets = 7, kChkFixTiny = 8, kChkRegather = 9, kChkEncodeSlab = 10,
+  kChkFixSmallPerm = 11, kChkPeer = 12
+};
+#ifdef HUSKY_CHECKED
+// one counter pair per translation unit (no relocatable device code); the
+// host side sums them through the readers each unit registers at load time
+static __device__ unsigned long long g_chk[2];  // [0] violations, [1] first: site << 48 | index
+#define HCHK(site, idx, bound)                                                                         \
+  do {                                                                                                 \
+    const unsigned long long i_ = (unsigned long long)(idx), b_ = (unsigned long long)(bound);          \
+    if (i_ >= b_ && atomicAdd(&::husky::g_chk[0], 1ull) == 0ull)                                       \
+      ::husky::g_chk[1] = ((unsigned long long)(site) << 48) | (i_ & 0xFFFFFFFFFFFFull);                \
+  } while (0)
+typedef unsigned long long (*ChkReader)(unsigned long long *first);
+int checked_register(ChkReader r);  // husky.cu
+// violations since the last call (summed over the units), *first = one of them
+unsigned long long checked_take(unsigned long long *first);
+static unsigned long long chk_read_unit(unsigned long long *first) {
+  unsigned long long h[2] = {0, 0}, z[2] = {0, 0};
+  cudaMemcpyFromSymbol(h, g_chk, sizeof h);
+  cudaMemcpyToSymbol(g_chk, z, sizeof z);
+  if (h[0] && first) *first = h[1];
+  return h[0];
+}
+static const int g_chk_registered = checked_register(chk_read_unit);
+#else
+#define HCHK(site, idx, bound) \
+  do {                         \
+  } while (0)
+#endif
 
 }  // namespace husky

@@ -1010,7 +1010,7 @@ husky_status husky_sort_multi_exec(void *plan, uint32_t *d_perm_out, void *d_sor
   }
   pc.mark("local sort");
   if (husky_status e = comm_sync(c, P->s)) return e;
-  return HUSKY_OK;
+  return checked_result(HUSKY_OK, "husky_sort_multi_exec");
 }
 
 husky_status husky_plan_destroy(void *plan) {
@@ -1233,7 +1233,7 @@ husky_status husky_sort_multi_loopback(int coder, int world, const void *d_units
   HCHECK(cudaGetLastError());
   agg.exchange = peer ? HUSKY_EXCHANGE_LOOPBACK_PEER : HUSKY_EXCHANGE_LOOPBACK_COPY;
   if (h_out) *h_out = agg;
-  return HUSKY_OK;
+  return checked_result(HUSKY_OK, "husky_sort_multi_loopback");
 }
 
 }  // extern "C"

@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
     uint64_t key = xk[i];
     uint32_t d = (uint32_t)(key >> shift) & MASK;
     uint32_t g = s_gbase[d] + i;
+    HCHK(kChkRadixScatter, g, n);
     keys_out[g] = key;
     vals_out[g] = xv[i];
   }
