@@ -16,3 +16,6 @@ HUSKY_LIB=$LIBC HUSKY_CHK_SELFTEST=1 timeout 900 python tools/sanitize_cases.py 
 grep -m2 "checked build" gpurun_out/checked_selftest.log
 HUSKY_LIB=$LIBC timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/checked_pytest.log 2>&1; echo pytest=$?
 tail -3 gpurun_out/checked_pytest.log
+# the sharded path's phases at 2^27 C5 strings through a one-rank communicator
+HUSKY_MULTI_TIMING=1 timeout 300 python tools/multi_probe.py 27 > gpurun_out/multi_probe27.log 2>&1; echo multi_probe=$?
+tail -30 gpurun_out/multi_probe27.log
