@@ -486,11 +486,12 @@ def e2e_single(h, torch, wl, steps, warmup, dev):
     wl["units"] = wl["offsets"] = None
     torch.cuda.empty_cache()
     # pipelined: the K steps as K batches of husky_sort_host_many, H2D / kernels
-    # / D2H on three streams.  Up to 2^28 strings: 2 device slots (a batch's
-    # copies overlap another batch's kernels).  Above (C5: inputs + outputs +
-    # workspace ~105 GB): ONE slot -- the next batch's inputs go in over PCIe
-    # while this batch's outputs come out (full duplex), the sort of the next
-    # batch waits for both
+    # / D2H on three streams.  Up to 2^28 strings: 2 input slots (a batch's
+    # copies overlap another batch's kernels).  Above (C5: inputs + workspace
+    # ~74 GB per input slot, outputs ~30 GB per output slot): ONE input slot and
+    # two output slots (134 GB) -- the next batch's inputs go in over PCIe while
+    # this batch's outputs come out (full duplex), and the next sort no longer
+    # waits for the copy-out
     depth = 2 if n <= PACK_MAX_N else 1
     mws = torch.empty(h.husky_sort_host_many_workspace(coder, n, total, depth), dtype=torch.uint8, device=dev)
     outs = [(torch.empty(n, dtype=torch.int32).pin_memory(), torch.empty(total + 8, dtype=dt).pin_memory(),
@@ -502,7 +503,8 @@ def e2e_single(h, torch, wl, steps, warmup, dev):
     h.husky_sort_host_many(coder, batches, mws, depth)
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3 / steps
-    api = (f"husky_sort_host_many: {steps} steps as {steps} pipelined batches, {depth} device slot(s), H2D / "
+    api = (f"husky_sort_host_many: {steps} steps as {steps} pipelined batches, {depth} input / {depth + 1} output "
+           "device slot(s), H2D / "
            "kernels / D2H on three streams (pinned host buffers), host wall clock around the call")
     hp = outs[(steps - 1) % depth][0]
     del mws

@@ -174,8 +174,9 @@ husky_status husky_sort_host(int coder, const void *h_units, const int64_t *h_of
                              uint32_t *h_perm, void *h_sorted_units, int64_t *h_sorted_offsets,
                              void *d_ws, size_t ws_bytes, husky_outcome *h_out, void *stream);
 
-/* Many independent sorts on HOST buffers, pipelined: `depth` workspace slots
- * used round robin and three streams -- host->device copies, kernels,
+/* Many independent sorts on HOST buffers, pipelined: `depth` input slots
+ * (device inputs + sort workspace) and depth + 1 output slots (device outputs)
+ * used round robin, and three streams -- host->device copies, kernels,
  * device->host copies -- so batch b+1's input copy, batch b's kernels and batch
  * b-1's output copy overlap (PCIe is full duplex; the copy engines are
  * independent of the SMs); events order the reuse of a slot.  Batch b:
@@ -183,9 +184,7 @@ husky_status husky_sort_host(int coder, const void *h_units, const int64_t *h_of
  * non-NULL, h_sorted_units[b] / h_sorted_offsets[b] (pass NULL arrays for
  * perm-only).  Output copies complete in batch order, so batches may share
  * output buffers only if the caller reads them after the call.  Host buffers
- * must be pinned for the copies to overlap.  (HUSKY_HOST_MANY=threads selects
- * the former scheme: `depth` worker threads, each running husky_sort_host on
- * its own stream.)  d_ws must hold
+ * must be pinned for the copies to overlap.  d_ws must hold
  * husky_sort_host_many_workspace(coder, n_max, units_max, depth) bytes, where
  * n_max / units_max bound every batch.  h_out (nullable) receives k outcomes.
  * Returns after every batch has finished; the first failing batch's status. */

@@ -794,6 +794,33 @@ static size_t host_layout(int coder, uint64_t n, uint64_t total_units, size_t *o
   return off;
 }
 
+// husky_sort_host_many: `depth` input slots [units | offsets | sort ws] and
+// depth + 1 output slots [perm | sorted units | sorted offsets].  The extra
+// output slot lets batch b+1 be sorted while batch b's outputs are still on
+// their way to the host (with one slot of each, the next sort had to wait for
+// the whole copy-out: C5 e2e ~785 ms per batch, of which the sort is ~91).
+struct ManyLayout {
+  size_t units, off, ws, in_slice;  // offsets within an input slot
+  size_t perm, su, so, out_slice;   // offsets within an output slot
+  size_t total(int depth) const { return (size_t)depth * in_slice + (size_t)(depth + 1) * out_slice; }
+};
+static ManyLayout many_layout(int coder, uint64_t n, uint64_t total_units) {
+  const size_t w = husky_unit_bytes(coder);
+  ManyLayout m{};
+  size_t off = 0;
+  auto take = [&](size_t b) { size_t o = off; off = align_up(off + b, 256); return o; };
+  m.units = take(total_units * w + 16);
+  m.off = take((n + 1) * 8);
+  m.ws = take(make_layout(n).total);
+  m.in_slice = off;
+  off = 0;
+  m.perm = take(n * 4 + 4);
+  m.su = take(total_units * w + 16);
+  m.so = take((n + 1) * 8);
+  m.out_slice = off;
+  return m;
+}
+
 husky_status husky_sort_host_workspace(int coder, uint64_t n, uint64_t total_units, size_t *bytes) {
   if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
   if (!bytes) return fail(HUSKY_ERR_INVALID_ARG, "bytes is NULL");
@@ -838,31 +865,30 @@ husky_status husky_sort_host(int coder, const void *h_units, const int64_t *h_of
 }
 
 // husky_sort_host_many, one issuing thread and three streams: host->device
-// copies (sh), kernels (sc) and device->host copies (sd), `depth` workspace
-// slots used round robin.  Batch b+1's input copy is enqueued before batch b
-// is sorted (sort_impl synchronises sc once per sort) and batch b's output
-// copy right after, so in steady state both copy directions and the SMs work on
-// three different batches.  Events order the reuse of a slot: its inputs are
-// overwritten only after the sort that read them, its outputs only after the
-// copy-out that read them.
+// copies (sh), kernels (sc) and device->host copies (sd); batch b uses input
+// slot b % depth and output slot b % (depth + 1).  Batch b+1's input copy is
+// enqueued before batch b is sorted (sort_impl synchronises sc once per sort)
+// and batch b's output copy right after, so in steady state both copy
+// directions and the SMs work on three different batches.  Events order the
+// reuse of a slot: an input slot is overwritten only after the sort that read
+// it, an output slot only after the copy-out that read it.
 static husky_status host_many_pipelined(int coder, int k, const void *const *h_units,
                                         const int64_t *const *h_offsets, const uint64_t *n,
                                         uint32_t *const *h_perm, void *const *h_sorted_units,
-                                        int64_t *const *h_sorted_offsets, int depth, uint8_t *ws, size_t slice,
-                                        uint64_t n_max, uint64_t u_max, husky_outcome *h_out) {
+                                        int64_t *const *h_sorted_offsets, int depth, uint8_t *ws,
+                                        const ManyLayout &m, husky_outcome *h_out) {
   const size_t w = husky_unit_bytes(coder);
+  const int odepth = depth + 1;
   cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
-  std::vector<cudaEvent_t> evH(depth, nullptr), evC(depth, nullptr), evD(depth, nullptr);
+  std::vector<cudaEvent_t> evH(depth, nullptr), evC(depth, nullptr), evO(odepth, nullptr), evD(odepth, nullptr);
   husky_status st = HUSKY_OK;
   auto cleanup = [&]() {
     if (sh) cudaStreamSynchronize(sh);
     if (sc) cudaStreamSynchronize(sc);
     if (sd) cudaStreamSynchronize(sd);
-    for (int i = 0; i < depth; ++i) {
-      if (evH[i]) cudaEventDestroy(evH[i]);
-      if (evC[i]) cudaEventDestroy(evC[i]);
-      if (evD[i]) cudaEventDestroy(evD[i]);
-    }
+    for (auto *v : {&evH, &evC, &evO, &evD})
+      for (cudaEvent_t e : *v)
+        if (e) cudaEventDestroy(e);
     if (sh) cudaStreamDestroy(sh);
     if (sc) cudaStreamDestroy(sc);
     if (sd) cudaStreamDestroy(sd);
@@ -882,61 +908,65 @@ static husky_status host_many_pipelined(int coder, int k, const void *const *h_u
   for (int i = 0; i < depth; ++i) {
     HM_CHECK(cudaEventCreateWithFlags(&evH[i], cudaEventDisableTiming));
     HM_CHECK(cudaEventCreateWithFlags(&evC[i], cudaEventDisableTiming));
+  }
+  for (int i = 0; i < odepth; ++i) {
+    HM_CHECK(cudaEventCreateWithFlags(&evO[i], cudaEventDisableTiming));
     HM_CHECK(cudaEventCreateWithFlags(&evD[i], cudaEventDisableTiming));
   }
   auto total_of = [&](int b) { return n[b] ? (uint64_t)(h_offsets[b][n[b]] - h_offsets[b][0]) : 0ull; };
-  std::vector<bool> used(depth, false);
-  // ONE layout for every batch, sized by the largest: a slot's input regions
-  // never overlap the outputs of the slot's previous batch, which may still be
-  // in flight to the host on sd while the next batch's inputs arrive on sh
-  size_t o_units, o_off, o_perm, o_su, o_so, o_ws;
-  host_layout(coder, n_max, u_max, &o_units, &o_off, &o_perm, &o_su, &o_so, &o_ws);
+  // ONE layout for every batch, sized by the largest batch (a slot's regions
+  // never move between batches)
+  auto in_base = [&](int b) { return ws + m.in_slice * (size_t)(b % depth); };
+  auto out_base = [&](int b) { return ws + m.in_slice * (size_t)depth + m.out_slice * (size_t)(b % odepth); };
+  std::vector<bool> used_in(depth, false), used_out(odepth, false);
   auto issue_in = [&](int b) -> cudaError_t {
     const int sl = b % depth;
-    uint8_t *base = ws + slice * sl;
+    uint8_t *base = in_base(b);
     cudaError_t e = cudaSuccess;
-    if (used[sl]) e = cudaStreamWaitEvent(sh, evC[sl], 0);  // the previous sort of this slot has read its inputs
+    if (used_in[sl]) e = cudaStreamWaitEvent(sh, evC[sl], 0);  // the previous sort of this slot has read its inputs
     const int64_t b0 = n[b] ? h_offsets[b][0] : 0;
     if (e == cudaSuccess && total_of(b))
-      e = cudaMemcpyAsync(base + o_units, (const uint8_t *)h_units[b] + b0 * w, total_of(b) * w,
+      e = cudaMemcpyAsync(base + m.units, (const uint8_t *)h_units[b] + b0 * w, total_of(b) * w,
                           cudaMemcpyHostToDevice, sh);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(base + o_off, h_offsets[b], (n[b] + 1) * 8, cudaMemcpyHostToDevice, sh);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(base + m.off, h_offsets[b], (n[b] + 1) * 8, cudaMemcpyHostToDevice, sh);
     if (e == cudaSuccess) e = cudaEventRecord(evH[sl], sh);
     return e;
   };
   if (k > 0) HM_CHECK(issue_in(0));
   for (int b = 0; b < k; ++b) {
-    const int sl = b % depth;
-    uint8_t *base = ws + slice * sl;
-    if (b + 1 < k && depth > 1) HM_CHECK(issue_in(b + 1));  // (one slot: after this sort)
+    const int sl = b % depth, so_ = b % odepth;
+    uint8_t *ib = in_base(b), *ob = out_base(b);
+    if (b + 1 < k && depth > 1) HM_CHECK(issue_in(b + 1));  // (one input slot: after this sort)
     if (n[b] && h_offsets[b][n[b]] < h_offsets[b][0]) {
       st = fail(HUSKY_ERR_INVALID_ARG, "batch %d: offsets are not non-decreasing", b);
       cleanup();
       return st;
     }
     HM_CHECK(cudaStreamWaitEvent(sc, evH[sl], 0));
-    if (used[sl]) HM_CHECK(cudaStreamWaitEvent(sc, evD[sl], 0));  // outputs of this slot copied out
+    if (used_out[so_]) HM_CHECK(cudaStreamWaitEvent(sc, evD[so_], 0));  // this output slot copied out
     const int64_t b0 = n[b] ? h_offsets[b][0] : 0;
-    const void *du = base + o_units;
+    const void *du = ib + m.units;
     if (b0 != 0) du = (const uint8_t *)du - b0 * (int64_t)w;  // offsets index the original buffer
     const bool want_units = h_sorted_units && h_sorted_offsets && h_sorted_units[b] && h_sorted_offsets[b];
-    st = sort_impl(coder, du, (const int64_t *)(base + o_off), n[b], (uint32_t *)(base + o_perm),
-                   want_units ? (void *)(base + o_su) : nullptr, want_units ? (int64_t *)(base + o_so) : nullptr,
-                   base + o_ws, slice - o_ws, h_out ? h_out + b : nullptr, sc);
+    st = sort_impl(coder, du, (const int64_t *)(ib + m.off), n[b], (uint32_t *)(ob + m.perm),
+                   want_units ? (void *)(ob + m.su) : nullptr, want_units ? (int64_t *)(ob + m.so) : nullptr,
+                   ib + m.ws, m.in_slice - m.ws, h_out ? h_out + b : nullptr, sc);
     if (st != HUSKY_OK) {
       cleanup();
       return st;
     }
     HM_CHECK(cudaEventRecord(evC[sl], sc));
-    HM_CHECK(cudaStreamWaitEvent(sd, evC[sl], 0));
-    if (n[b]) HM_CHECK(cudaMemcpyAsync(h_perm[b], base + o_perm, n[b] * 4, cudaMemcpyDeviceToHost, sd));
+    HM_CHECK(cudaEventRecord(evO[so_], sc));
+    HM_CHECK(cudaStreamWaitEvent(sd, evO[so_], 0));
+    if (n[b]) HM_CHECK(cudaMemcpyAsync(h_perm[b], ob + m.perm, n[b] * 4, cudaMemcpyDeviceToHost, sd));
     if (want_units) {
       if (total_of(b))
-        HM_CHECK(cudaMemcpyAsync(h_sorted_units[b], base + o_su, total_of(b) * w, cudaMemcpyDeviceToHost, sd));
-      HM_CHECK(cudaMemcpyAsync(h_sorted_offsets[b], base + o_so, (n[b] + 1) * 8, cudaMemcpyDeviceToHost, sd));
+        HM_CHECK(cudaMemcpyAsync(h_sorted_units[b], ob + m.su, total_of(b) * w, cudaMemcpyDeviceToHost, sd));
+      HM_CHECK(cudaMemcpyAsync(h_sorted_offsets[b], ob + m.so, (n[b] + 1) * 8, cudaMemcpyDeviceToHost, sd));
     }
-    HM_CHECK(cudaEventRecord(evD[sl], sd));
-    used[sl] = true;
+    HM_CHECK(cudaEventRecord(evD[so_], sd));
+    used_in[sl] = true;
+    used_out[so_] = true;
     if (b + 1 < k && depth == 1) HM_CHECK(issue_in(b + 1));
   }
 #undef HM_CHECK
@@ -951,8 +981,7 @@ husky_status husky_sort_host_many_workspace(int coder, uint64_t n_max, uint64_t 
                                             size_t *bytes) {
   if (!valid_coder(coder)) return fail(HUSKY_ERR_INVALID_ARG, "unknown coder %d", coder);
   if (!bytes || depth < 1 || depth > 16) return fail(HUSKY_ERR_INVALID_ARG, "bad arguments");
-  size_t a, b, c, d, e, f;
-  *bytes = (size_t)depth * align_up(host_layout(coder, n_max, units_max, &a, &b, &c, &d, &e, &f), 256);
+  *bytes = many_layout(coder, n_max, units_max).total(depth);
   return HUSKY_OK;
 }
 
@@ -970,11 +999,11 @@ husky_status husky_sort_host_many(int coder, int k, const void *const *h_units, 
     n_max = std::max<uint64_t>(n_max, n[b]);
     if (n[b]) u_max = std::max<uint64_t>(u_max, (uint64_t)(h_offsets[b][n[b]] - h_offsets[b][0]));
   }
-  size_t a, bb, c, d, e, f;
-  const size_t slice = align_up(host_layout(coder, n_max, u_max, &a, &bb, &c, &d, &e, &f), 256);
-  if (ws_bytes < slice * depth) return fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, slice * depth);
+  const ManyLayout m = many_layout(coder, n_max, u_max);
+  if (ws_bytes < m.total(depth))
+    return fail(HUSKY_ERR_WORKSPACE, "workspace %zu < required %zu", ws_bytes, m.total(depth));
   return host_many_pipelined(coder, k, h_units, h_offsets, n, h_perm, h_sorted_units, h_sorted_offsets, depth,
-                             (uint8_t *)d_ws, slice, n_max, u_max, h_out);
+                             (uint8_t *)d_ws, m, h_out);
 }
 
 }  // extern "C"
