@@ -196,6 +196,11 @@ static bool alpha_env() {
 
 // What one sort enqueues before its single synchronisation (decided on the
 // host from the arguments and the environment; part of the graph cache key).
+// from this many strings the host waits for the device-side pass plan and
+// launches only the planned pass slots (enqueue_main); below, all 8 slots are
+// enqueued without a synchronisation (and the sequence may be a cached graph)
+constexpr uint64_t kHostPlanMinN = 1ull << 26;
+
 struct MainFlags {
   int coder = 0, kc = 0;
   bool packed = false, compress = false, slab = false, pdl = true;
@@ -247,8 +252,19 @@ static husky_status enqueue_main(Sorter &S, const MainFlags &F, void *d_sorted_u
   // exit at once.  Input violations (bad offsets, ASCII domain) make every
   // later kernel a no-op and are reported at the single synchronisation.
   {
-    GroupScope grp(ST_RADIX, s);  // profiler mode 2: the 8 pass slots as one timed group
-    for (int slot = 0; slot < 8; ++slot)
+    // large inputs: the host reads the plan's pass count and launches only
+    // those slots -- an unused slot still launches (and retires) one CTA per
+    // tile, ~0.2 ms each at 2^30, against ~20 us for this synchronisation
+    // (such sorts are never captured into a graph, see sort_impl)
+    int slots = 8;
+    if (n >= kHostPlanMinN) {
+      uint32_t np = 8;
+      HCHECK(cudaMemcpyAsync(&np, &st->np, 4, cudaMemcpyDeviceToHost, s));
+      HCHECK(cudaStreamSynchronize(s));
+      slots = (int)std::min<uint32_t>(np, 8u);
+    }
+    GroupScope grp(ST_RADIX, s);  // profiler mode 2: the pass slots as one timed group
+    for (int slot = 0; slot < slots; ++slot)
       launch_onesweep_slot(slot, keysA, keysB, packed_payload, d_perm, vals_tmp, n, st, S.lb_radix(),
                            S.next_counter(), S.next_epoch(), s);
   }
@@ -455,7 +471,7 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
   DevState hs_local;
   const DevState *hs_src = &hs_local;
   GraphEntry *ge = nullptr;
-  if (allow_graph && graphs_enabled() && !debug_sync() && profiler().on == 0) {
+  if (allow_graph && n < kHostPlanMinN && graphs_enabled() && !debug_sync() && profiler().on == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     GraphKey key;
