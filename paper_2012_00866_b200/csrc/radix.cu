@@ -128,31 +128,50 @@ __global__ void __launch_bounds__(512) k_hist_slots(uint64_t *__restrict__ keys,
   if (!s_last) return;
   __threadfence();
   // the last CTA: exclusive scans and trivial digits (as k_hist_scan), the
-  // entropy of each digit's histogram, then the plan
-  __shared__ float s_h[8], s_hw[512 / 32];
-  uint32_t trivial = 0;
-  for (int d = 0; d < 8; ++d) {
-    const uint32_t v = threadIdx.x < kBins ? __ldcg(&st->hist[d][threadIdx.x]) : 0u;
-    uint32_t total;
-    const uint32_t ex = block_exclusive_scan<uint32_t, 512>(v, &total, s_wt);
-    if (threadIdx.x < kBins) st->digit_start[d][threadIdx.x] = ex;
-    const bool all_here = __syncthreads_or((uint64_t)v == n) != 0;
-    trivial |= (uint32_t)all_here << d;
-    if (skip) {  // H_d = -sum p log2 p over the digit's bins
-      const float pr = (float)v / (float)n;
-      float h = v ? -pr * __log2f(pr) : 0.f;
+  // entropy of each digit's histogram, then the plan.  One warp per digit
+  // (8 bins per lane, shuffle scans): all 8 digits' counts in one round trip
+  // and no block barriers (a digit-serial block scan cost ~12 us of a 1e5 sort)
+  __shared__ float s_h[8];
+  __shared__ uint32_t s_triv[8];
+  {
+    const uint32_t w = threadIdx.x >> 5, lane = lane_id();
+    if (w < 8) {
+      uint32_t v[8], t = 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
-      if (lane_id() == 0) s_hw[threadIdx.x >> 5] = h;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        float t = 0.f;
-        for (int w = 0; w < 512 / 32; ++w) t += s_hw[w];
-        s_h[d] = t;
+      for (int q = 0; q < 8; ++q) {
+        v[q] = __ldcg(&st->hist[w][lane * 8 + q]);
+        t += v[q];
       }
-      __syncthreads();
+      uint32_t incl = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((int)lane >= o) incl += y;
+      }
+      uint32_t run = incl - t;
+      bool all_here = false;
+      float hsum = 0.f;  // H_d = -sum p log2 p over the digit's bins
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        st->digit_start[w][lane * 8 + q] = run;
+        run += v[q];
+        all_here |= (uint64_t)v[q] == n;
+        const float pr = (float)v[q] / (float)n;
+        hsum += v[q] ? -pr * __log2f(pr) : 0.f;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xFFFFFFFFu, hsum, o);
+      const bool triv = __any_sync(0xFFFFFFFFu, all_here);
+      if (lane == 0) {
+        s_h[w] = hsum;
+        s_triv[w] = triv ? 1u : 0u;
+      }
     }
   }
+  __syncthreads();
+  uint32_t trivial = 0;
+#pragma unroll
+  for (int d = 0; d < 8; ++d) trivial |= s_triv[d] << d;
   if (threadIdx.x == 0) {
     st->trivial_mask = trivial;
     st->ccomp = cmp ? 1u : 0u;
