@@ -54,6 +54,22 @@ def test_unit_bytes_and_workspace_queries():
     assert e.value.status == 1 and "coder" in h.husky_last_error()
 
 
+def test_host_many_workspace_slots():
+    """husky_sort_host_many: `depth` input slots (device inputs + sort workspace)
+    and depth + 1 output slots (perm, sorted units, sorted offsets) -- each added
+    input slot costs at least one sort workspace, each added output slot at
+    least the outputs' bytes."""
+    import paper_2012_00866_b200 as h
+    n, u = 1_000_000, 16_000_000
+    sort_ws = h.husky_sort_workspace(0, n, u)
+    outs = n * 4 + u + (n + 1) * 8
+    w1, w2, w3 = (h.husky_sort_host_many_workspace(0, n, u, d) for d in (1, 2, 3))
+    assert w1 >= sort_ws + u + (n + 1) * 8 + 2 * outs
+    assert w2 - w1 == w3 - w2 >= sort_ws + u + (n + 1) * 8 + outs
+    with pytest.raises(h.HuskyError):
+        h.husky_sort_host_many_workspace(0, n, u, 0)
+
+
 def test_select_splitters_host():
     """The sample sort's splitter rule (host copy, no GPU): sample strings sorted
     in the sort order (ties by index), positions floor(k*m/P)."""
