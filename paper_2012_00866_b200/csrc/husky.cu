@@ -244,7 +244,8 @@ static husky_status enqueue_main(Sorter &S, const MainFlags &F, void *d_sorted_u
   }
   launch_hist_plan(keysA, n, st, keysA, keysB, S.sms, s, F.compress, F.skip,
                    kc == HUSKY_CODER_UNICODE ? CoderTraits<HUSKY_CODER_UNICODE>::kS : CoderTraits<HUSKY_CODER_ASCII>::kS,
-                   kc == HUSKY_CODER_UNICODE ? CoderTraits<HUSKY_CODER_UNICODE>::kPL : CoderTraits<HUSKY_CODER_ASCII>::kPL);
+                   kc == HUSKY_CODER_UNICODE ? CoderTraits<HUSKY_CODER_UNICODE>::kPL : CoderTraits<HUSKY_CODER_ASCII>::kPL,
+                   kc == HUSKY_CODER_UNICODE);
 
   // ---- A2 key sort, LSD onesweep: (code, index) -> sorted codes, perm.  The
   // pass plan (which digits are not shared by all keys) is made on device, so
@@ -466,7 +467,8 @@ husky_status sort_impl(int coder, const void *d_units, const int64_t *d_offsets,
            ((n > kSlabMinN && slab_env() != 0) || slab_env() == 1);
   F.pdl = pdl_enabled();
   // partial key sort (R19, ASCII codes only; HUSKY_SKIP=0 never, =2 always)
-  F.skip = coder == HUSKY_CODER_ASCII ? skip_env() : 0;
+  // (the English coders share the ASCII kernels but not its field layout)
+  F.skip = (coder == HUSKY_CODER_ASCII || coder == HUSKY_CODER_UNICODE) ? skip_env() : 0;
 
   DevState hs_local;
   const DevState *hs_src = &hs_local;

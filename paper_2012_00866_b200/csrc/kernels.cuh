@@ -37,7 +37,7 @@ void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_s
 // coder's run rule (DevState::seq_units / short_len when nothing is skipped)
 void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *keysA, uint64_t *keysB,
                       int num_sms, cudaStream_t s, bool compress = false, int skip = 0, uint32_t def_s = 0,
-                      uint32_t def_pl = 0);
+                      uint32_t def_pl = 0, bool unicode = false);
 
 // A2 onesweep radix
 // 512 threads x 12 keys = 6144-key tiles, 92 KB smem (keys, payloads, u16

@@ -76,7 +76,7 @@ constexpr float kSkip1Bar = HUSKY_SKIP1_BAR;
 template <bool PLAN>
 __global__ void __launch_bounds__(512) k_hist_slots(uint64_t *__restrict__ keys, uint64_t n, DevState *st,
                                                     uint64_t *keysA, uint64_t *keysB, int compress, int skip,
-                                                    uint32_t def_s, uint32_t def_pl) {
+                                                    uint32_t def_s, uint32_t def_pl, int uni) {
   constexpr uint32_t M = kBins - 1;
   pdl_wait();  // PLAN: launched as a programmatic dependent of the encoder
   __shared__ uint32_t h[8 * kBins];
@@ -188,7 +188,14 @@ __global__ void __launch_bounds__(512) k_hist_slots(uint64_t *__restrict__ keys,
       for (uint32_t k = 2; k >= 1; --k) {
         if (np < k + 1 || (skip == 2 && k != 1) || (skip == 3 && k != 2)) continue;
         const uint32_t dtop = dig[k - 1];
-        const int sp = 9 - (int)((8 * (dtop + 1) + fb - 1) / fb);
+        // units wholly above the masked bits [0, 8 (dtop + 1)): ASCII fields of
+        // fb bits from bit fb * 8 down; UNICODE units 0..2 at bits 47 - 16 u ..
+        // 62 - 16 u (unit 3 lost its low bit to the >>> 1 and is never fixed)
+        int sp = 9 - (int)((8 * (dtop + 1) + fb - 1) / fb);
+        if (uni) {
+          sp = 0;
+          for (int u = 0; u < 3; ++u) sp += (47 - 16 * u >= (int)(8 * (dtop + 1))) ? 1 : 0;
+        }
         float hhi = 0.f;
         for (uint32_t i = k; i < np; ++i) hhi += s_h[dig[i]];
         // expected extra equal-key pairs if the other digits were independent;
@@ -220,19 +227,20 @@ void launch_hist_slots(const uint64_t *keys, uint64_t n, DevState *st, int num_s
   Scope sc_(ST_HIST_SCAN, s, n);
   const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * kHistBlocksPerSM);
   k_hist_slots<false><<<(unsigned)blocks, 512, 0, s>>>(const_cast<uint64_t *>(keys), n, st, nullptr, nullptr, 0, 0,
-                                                      0u, 0u);
+                                                      0u, 0u, 0);
 }
 
 // histograms + scans + pass plan of the device-planned passes in one launch
 // (DevState::hist_done must be 0: DevState is zeroed per sort)
 void launch_hist_plan(const uint64_t *keys, uint64_t n, DevState *st, uint64_t *keysA, uint64_t *keysB,
-                      int num_sms, cudaStream_t s, bool compress, int skip, uint32_t def_s, uint32_t def_pl) {
+                      int num_sms, cudaStream_t s, bool compress, int skip, uint32_t def_s, uint32_t def_pl,
+                      bool unicode) {
   if (n == 0) return;
   Scope sc_(ST_HIST_SCAN, s, n);
   GroupScope grp(ST_HIST_SCAN, s);
   const uint64_t blocks = std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * kHistBlocksPerSM);
   launch_pdl(k_hist_slots<true>, dim3((unsigned)blocks), dim3(512), 0, s, const_cast<uint64_t *>(keys), n, st, keysA,
-             keysB, compress ? 1 : 0, skip, def_s, def_pl);
+             keysB, compress ? 1 : 0, skip, def_s, def_pl, unicode ? 1 : 0);
 }
 
 constexpr int kRadixWarps = kRadixThreads / 32;

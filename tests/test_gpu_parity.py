@@ -690,9 +690,9 @@ def test_refinement_medium_subruns(torch, h, oracle_mod, with_units):
 
 # ------------------------------------- partial key sort (lowest digit unsorted)
 @pytest.mark.parametrize("name,n", [("C1", 100_000), ("C2", 300_000), ("C5", 300_000), ("C4", 40_000),
-                                    ("D1", 150_000)])
+                                    ("D1", 150_000), ("C3", 300_000)])
 def test_lowest_digit_unsorted_forced(torch, h, oracle_mod, monkeypatch, name, n):
-    """HUSKY_SKIP=2 leaves the lowest varying digit of the ASCII keys unsorted
+    """HUSKY_SKIP=2 leaves the lowest varying digit of the ASCII / UNICODE keys unsorted
     whenever the plan allows (R19): run detection then compares keys under the
     mask, equal masked keys fix fewer leading units and the short rule shrinks
     with them; every extra equal-key pair is resolved by the run machinery.
