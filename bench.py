@@ -532,8 +532,12 @@ def run_single(args, h, torch, dev):
     e2e = None
     if not args.no_e2e:
         perm_dev = r.pop("perm_dev").cpu()
-        e2e, hp = e2e_single(h, torch, wl, args.e2e_steps, 1, dev)
-        e2e["matches_device_perm"] = bool(torch.equal(hp[:n], perm_dev))
+        try:
+            e2e, hp = e2e_single(h, torch, wl, args.e2e_steps, 1, dev)
+            e2e["matches_device_perm"] = bool(torch.equal(hp[:n], perm_dev))
+        except (RuntimeError, MemoryError) as e:  # e.g. a box with less free HBM: keep the line
+            torch.cuda.empty_cache()
+            e2e = {"value": None, "unit": UNIT, "error": str(e)[:200]}
     else:
         r.pop("perm_dev", None)
     del wl
