@@ -535,7 +535,7 @@ def run_single(args, h, torch, dev):
         try:
             e2e, hp = e2e_single(h, torch, wl, args.e2e_steps, 1, dev)
             e2e["matches_device_perm"] = bool(torch.equal(hp[:n], perm_dev))
-        except (RuntimeError, MemoryError) as e:  # e.g. a box with less free HBM: keep the line
+        except (RuntimeError, MemoryError, h.HuskyError) as e:  # e.g. less free HBM on the box: keep the line
             torch.cuda.empty_cache()
             e2e = {"value": None, "unit": UNIT, "error": str(e)[:200]}
     else:
