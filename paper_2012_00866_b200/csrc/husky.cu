@@ -599,17 +599,41 @@ static husky_status refine_giants(Sorter &S, const DevState &hs0, void *d_sorted
     HCHECK(cudaMemcpyAsync(info, &st->seg_L, 8, cudaMemcpyDeviceToHost, s));
     HCHECK(cudaStreamSynchronize(s));
     uint32_t Lcur = info[1] ? seg.from : info[0];
+    // R19 inside the refinement (ASCII windows): leave the tag and the window's
+    // last two units (digits 0..2) unsorted when the sorted units' entropy makes
+    // the extra equal pairs rare; every pair equal under the mask is then
+    // resolved by the fix-ups (or the next round, from two units earlier)
+    uint32_t trivial = snap.trivial_mask, adv = win;
+    unsigned long long refmask = ~0ull;
+    if (coder == HUSKY_CODER_ASCII && skip_env() != 0 && seg.len >= 4096) {
+      std::vector<uint32_t> hh(8 * kBins);
+      HCHECK(cudaMemcpy(hh.data(), st->hist, hh.size() * 4, cudaMemcpyDeviceToHost));
+      double H = 0.0;
+      for (int d = 3; d < 8; ++d)
+        for (int b = 0; b < kBins; ++b) {
+          const double p = (double)hh[d * kBins + b] / (double)seg.len;
+          if (p > 0.0) H -= p * std::log2(p);
+        }
+      const double extra = 0.5 * (double)seg.len * (double)seg.len * std::exp2(-H);
+      // (by the rule only, never forced: a degenerate segment -- identical
+      // strings, H = 0 -- must keep the tag, or its rounds would not end)
+      if (extra < 1e-2 * (double)seg.len) {
+        trivial |= 0x07u;
+        refmask = ~0xFFFFFFull;
+        adv = win - 2;
+      }
+    }
     uint64_t *sorted_key2 = nullptr;
     // payload: the segment's perm entries; sorted back into perm_seg
-    if (husky_status e = S.radix(S.keysA(), perm_seg, seg.len, snap.trivial_mask, perm_seg,
-                                 S.at<uint32_t>(L.vals), &sorted_key2))
+    if (husky_status e = S.radix(S.keysA(), perm_seg, seg.len, trivial, perm_seg, S.at<uint32_t>(L.vals),
+                                 &sorted_key2))
       return e;
     debug_check_perm(d_perm, n, "refine radix", s);
     // sub-runs of equal key with tag == cap are still ambiguous
     HCHECK(cudaMemsetAsync(dirty, 0, seg.len / 2 + 1, s));
     HCHECK(cudaMemsetAsync(&st->n_giant, 0, 4, s));
     launch_runs_scan(coder, 1, sorted_key2, seg.len, perm_seg, d_units, d_offsets, seg.start, run_start,
-                     run_end, dirty, st, S.lb_scan(), S.next_counter(), S.next_epoch(), s);
+                     run_end, dirty, st, S.lb_scan(), S.next_counter(), S.next_epoch(), s, refmask);
     launch_runs_classify(run_start, run_end, dirty, st, list_sm, L.cap_sm, list_g, false, S.sms, s);
     HCHECK(cudaMemcpyAsync(&n_giant, &st->n_giant, 4, cudaMemcpyDeviceToHost, s));
     HCHECK(cudaStreamSynchronize(s));
@@ -617,7 +641,7 @@ static husky_status refine_giants(Sorter &S, const DevState &hs0, void *d_sorted
     if (n_giant) {
       std::vector<uint2> g(n_giant);
       HCHECK(cudaMemcpy(g.data(), list_g, n_giant * sizeof(uint2), cudaMemcpyDeviceToHost));
-      for (auto &x : g) queue.push_back({x.x, x.y, Lcur + win});
+      for (auto &x : g) queue.push_back({x.x, x.y, Lcur + adv});
     }
   }
 

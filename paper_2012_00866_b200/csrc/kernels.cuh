@@ -106,7 +106,7 @@ inline uint64_t scan_tiles(uint64_t n) { return (n + kScanTile - 1) / kScanTile;
 void launch_runs_scan(int coder, int mode, const uint64_t *keys, uint64_t n, const uint32_t *perm,
                       const void *units, const int64_t *offsets, uint32_t base, uint32_t *run_start,
                       uint32_t *run_end, uint8_t *dirty, DevState *st, unsigned long long *lb,
-                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s);
+                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, unsigned long long refmask = ~0ull);
 void launch_runs_classify(const uint32_t *run_start, const uint32_t *run_end, const uint8_t *dirty,
                           DevState *st, uint2 *list_sm, uint64_t cap_sm, uint2 *list_g,
                           bool count_stats, int num_sms, cudaStream_t s);

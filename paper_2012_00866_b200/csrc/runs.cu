@@ -25,7 +25,8 @@ __global__ void __launch_bounds__(kScanThreads)
     k_runs_scan(const uint64_t *__restrict__ keys, uint64_t n, const uint32_t *__restrict__ perm,
                 const void *__restrict__ units, const int64_t *__restrict__ offsets, uint32_t base,
                 uint32_t *__restrict__ run_start, uint32_t *__restrict__ run_end, uint8_t *__restrict__ dirty,
-                DevState *st, unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch) {
+                DevState *st, unsigned long long *lb, uint32_t *tile_counter, uint32_t epoch,
+                unsigned long long refmask) {
   using T = CoderTraits<CODER>;
   // Tile staging of the keys in smem (coalesced async copies).  Each thread then
   // works on kScanItems consecutive positions; the array is padded (one pad
@@ -53,7 +54,9 @@ __global__ void __launch_bounds__(kScanThreads)
 
   // keys at p0-1 .. p0+kScanItems (MODE 0: under the run rule's mask, R19)
   const RunRule rule = run_rule<CODER>(st);
-  const unsigned long long km = MODE == 0 ? rule.mask : ~0ull;
+  // MODE 1: a refinement that left the tag and the window's last units unsorted
+  // compares keys under refmask, and every equal pair under it is unresolved
+  const unsigned long long km = MODE == 0 ? rule.mask : refmask;
   uint64_t c[kScanItems + 2];
 #pragma unroll
   for (int j = 0; j < kScanItems + 2; ++j) {
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(kScanThreads)
         bad = cmp_equal_code<CODER>(units, offsets, __ldg(perm + p), __ldg(perm + p + 1), rule.S, rule.PL) > 0;
       } else {
         constexpr uint64_t tagmask = CODER == HUSKY_CODER_ASCII ? 0xFFull : 0xFFFFull;
-        bad = (c[j + 1] & tagmask) == (uint64_t)(16 + T::kTagCap);
+        bad = refmask != ~0ull || (c[j + 1] & tagmask) == (uint64_t)(16 + T::kTagCap);
       }
       badm |= (uint32_t)bad << j;
     }
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(kScanThreads)
 void launch_runs_scan(int coder, int mode, const uint64_t *keys, uint64_t n, const uint32_t *perm,
                       const void *units, const int64_t *offsets, uint32_t base, uint32_t *run_start,
                       uint32_t *run_end, uint8_t *dirty, DevState *st, unsigned long long *lb,
-                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s) {
+                      uint32_t *tile_counter, uint32_t epoch, cudaStream_t s, unsigned long long refmask) {
   if (n == 0) return;
   constexpr int kSmem0 = kScanKP * 8;  // the padded key staging
   static SmemAttr a0, a1, a2, a3;
@@ -131,7 +134,7 @@ void launch_runs_scan(int coder, int mode, const uint64_t *keys, uint64_t n, con
   a3.ensure(k_runs_scan<HUSKY_CODER_UNICODE, 1>, kSmem0);
   Scope sc_(ST_RUNS_SCAN, s, n);
   dim3 g((unsigned)scan_tiles(n)), b(kScanThreads);
-#define RS_ARGS keys, n, perm, units, offsets, base, run_start, run_end, dirty, st, lb, tile_counter, epoch
+#define RS_ARGS keys, n, perm, units, offsets, base, run_start, run_end, dirty, st, lb, tile_counter, epoch, refmask
   if (coder == HUSKY_CODER_ASCII) {
     if (mode == 0) k_runs_scan<HUSKY_CODER_ASCII, 0><<<g, b, kSmem0, s>>>(RS_ARGS);
     else k_runs_scan<HUSKY_CODER_ASCII, 1><<<g, b, kSmem0, s>>>(RS_ARGS);
