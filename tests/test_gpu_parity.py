@@ -740,3 +740,23 @@ def test_tiny_runs_lane_fixup(torch, h, oracle_mod, n):
     out = check_against_oracle(torch, h, oracle_mod, w)
     assert out["runs_by_class"][1] > 0
     check_against_oracle(torch, h, oracle_mod, w, with_units=False)  # perm-only mode
+
+
+def test_refinement_partial_sort_with_giant_cluster(torch, h, oracle_mod):
+    """The refinement's partial sort (the key2 windows sorted on their first 5
+    units when the entropy rule allows): one giant run (a shared 16-unit prefix,
+    so every code is equal) whose suffixes are mostly random -- the rule takes
+    the partial sort -- plus a cluster of 10,000 strings sharing the next 5 units
+    and differing only in the 2 masked ones and beyond: that cluster is a giant
+    run under the mask and is refined again from 5 units further, not 7."""
+    rng = np.random.default_rng(21)
+    alpha = np.frombuffer(b"0123456789ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz", dtype=np.uint8)
+    prefix = list(b"SHARED-PREFIX-16")
+    strings = [prefix + alpha[rng.integers(0, 62, size=8)].tolist() for _ in range(90_000)]
+    head = list(b"QQQQQ")
+    strings += [prefix + head + alpha[rng.integers(0, 62, size=int(rng.integers(0, 6)))].tolist()
+                for _ in range(10_000)]
+    order = rng.permutation(len(strings))
+    w = W.from_strings([strings[i] for i in order], ASCII)
+    outc = check_against_oracle(torch, h, oracle_mod, w)
+    assert outc["refine_rounds"] >= 2
