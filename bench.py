@@ -547,7 +547,7 @@ def run_single(args, h, torch, dev):
     if not args.no_also and name == "C5":
         # the other single-GPU configs (parity / structure cases of BASELINE.json)
         # and D1, a dirty-run workload that exercises the segmented fix-up (A5)
-        for cfg in ("C2", "C3", "C4", "D1"):
+        for cfg in ("C1", "C2", "C3", "C4", "D1"):
             r2 = measure_single(args, cfg, W.FULL_N[cfg], dev, max(3, args.steps // 2), args.warmup, flush, False, h,
                                 torch)
             r2.pop("perm_dev", None)
